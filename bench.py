@@ -1,0 +1,459 @@
+"""GCUPS benchmark of the B200 NW hot path (BASELINE.json metric).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                [--workload c2|c1|c3|c4|c5]
+
+Default workload = BASELINE.json configs[1] (C2): one DNA pair 20,000 x 20,000,
++1/-1/-1, fill + 2-bit packed directions + traceback. One step = one pass of the
+whole hot path: nw_align_pair_dev (encode + fill + directions) and
+nw_traceback_dev (walk + reverse) on inputs resident in HBM.
+
+value   : GCUPS = m*n cells / device time per step (CUDA events on the context
+          stream, per step, L2 flushed between steps), whole job over N ranks.
+e2e     : the same metric through the host-pointer C ABI (nw_align_pair +
+          nw_traceback on host buffers, H2D of the residues and D2H of the score
+          and path inside the timed region).
+roofline: the fill kernel's integer-op rate vs the issue-limited lane-op peak
+          (DESIGN.md §5).
+cpu_baseline: the oracle (plain C, 1 core) on a bounded sample of the workload.
+--impl reference: the oracle timed on the host as the reference arm.
+Multi-GPU (torchrun): C2 is one pair (no exchange step): N independent
+replicas, weak scaling. c3 shards pairs across ranks and all-gathers scores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import nwgen  # noqa: E402
+
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+ALU_ISSUE_LANES_PER_CLK_PER_SM = 128  # 4 SMSPs x 32 lanes x 1 warp-instr/clk (tools/peaks_int.cu)
+SM_COUNT = 148
+SM_MAX_MHZ = 1965.0
+OPS_PER_CELL = {"dirs": 6, "score": 3}  # SURVEY.md §8(d) algorithmic op floors
+WORKLOADS = {
+    "c1": "C1: single DNA pair 1,000 x 1,000, +1/-1/-1, score + full traceback",
+    "c2": "C2: single DNA pair 20,000 x 20,000, +1/-1/-1, score + 2-bit packed traceback",
+    "c3": "C3: all-pairs of 2,048 DNA sequences of 500-2,000 bp (2,096,128 pairs), score-only",
+    "c4": "C4: 100,000 protein pairs of 100-1,000 residues, BLOSUM62, g=-5, score + traceback",
+    "c5": "C5: single DNA pair 1,000,000 x 1,000,000, score-only (linear memory)",
+}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return {}
+    return {}
+
+
+def cpu_oracle_sample(workload: str, budget_s: float = 15.0):
+    """Time the oracle (as it stands) on a bounded sample of the workload."""
+    import oracle
+    if workload in ("c1", "c2"):
+        a, b = nwgen.config_c1() if workload == "c1" else nwgen.config_c2()
+        # full pair if it fits the budget (~0.06 GCUPS single-core full+dirs), else a prefix
+        side = len(a)
+        est = side * side / 0.06e9
+        if est > budget_s:
+            side = int((budget_s * 0.06e9) ** 0.5)
+        a, b = a[:side], b[:side]
+        t0 = time.perf_counter()
+        oracle.align(a, b, nwgen.PAPER_DNA)
+        dt = time.perf_counter() - t0
+        cells = len(a) * len(b)
+        return {"value": cells / dt / 1e9, "unit": "GCUPS", "cores": 1, "kind": "oracle",
+                "sample": f"{len(a)}x{len(b)} prefix of the {workload.upper()} pair, fill with "
+                          f"full direction matrix + traceback, {dt:.2f} s"}
+    if workload == "c5":
+        a, b = nwgen.config_c5()
+        side = int((budget_s * 0.4e9) ** 0.5)
+        t0 = time.perf_counter()
+        oracle.score(a[:side], b[:side], nwgen.PAPER_DNA)
+        dt = time.perf_counter() - t0
+        return {"value": side * side / dt / 1e9, "unit": "GCUPS", "cores": 1, "kind": "oracle",
+                "sample": f"{side}x{side} prefix of the C5 pair, two-row score-only, {dt:.2f} s"}
+    cores = len(os.sched_getaffinity(0))
+    if workload == "c3":
+        ss = nwgen.config_c3()
+        pairs = nwgen.all_pairs(ss.nseq)
+        rng = np.random.Generator(np.random.PCG64(0))
+        lens = ss.lengths()
+        idx = rng.permutation(len(pairs))
+        cells_per = lens[pairs[idx, 0]] * lens[pairs[idx, 1]]
+        target = budget_s * 0.5e9 * cores
+        k = int(np.searchsorted(np.cumsum(cells_per), target)) + 1
+        sub = pairs[idx[:k]]
+        t0 = time.perf_counter()
+        oracle.batch_score(ss.residues, ss.offs, sub, nwgen.PAPER_DNA, nthreads=cores)
+        dt = time.perf_counter() - t0
+        cells = int(cells_per[:k].sum())
+        return {"value": cells / dt / 1e9, "unit": "GCUPS", "cores": cores, "kind": "oracle",
+                "sample": f"{k} random pairs of C3 ({cells:.3e} cells), score-only, {dt:.2f} s"}
+    if workload == "c4":
+        ss = nwgen.config_c4(2000)
+        t0 = time.perf_counter()
+        cells = 0
+        for k in range(2000):
+            a, b = ss.seq(2 * k), ss.seq(2 * k + 1)
+            oracle.align(a, b, nwgen.PROTEIN_BLOSUM62)
+            cells += len(a) * len(b)
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+        return {"value": cells / dt / 1e9, "unit": "GCUPS", "cores": 1, "kind": "oracle",
+                "sample": f"{k + 1} C4 pairs ({cells:.3e} cells), fill + traceback, 1 core, {dt:.2f} s"}
+    raise ValueError(workload)
+
+
+# ----------------------------------------------------------------------------- ours
+
+class PairWorkload:
+    """C1/C2 (fill + traceback) and C5 (score-only) single-pair steps."""
+
+    def __init__(self, ctx, torch, workload: str, rank: int):
+        import paper_2412_21103_b200 as nwb
+        self.nwb, self.ctx, self.torch = nwb, ctx, torch
+        self.workload = workload
+        gen = {"c1": nwgen.config_c1, "c2": nwgen.config_c2, "c5": nwgen.config_c5}[workload]
+        a, b = gen()
+        self.a, self.b = a, b
+        self.m, self.n = len(a), len(b)
+        self.dirs = workload != "c5"
+        self.sc = nwgen.PAPER_DNA
+        self.da = torch.frombuffer(bytearray(a), dtype=torch.uint8).cuda()
+        self.db = torch.frombuffer(bytearray(b), dtype=torch.uint8).cuda()
+        self.d_score = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.d_ops = torch.zeros(self.m + self.n, dtype=torch.uint8, device="cuda")
+        self.d_len = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.cells = self.m * self.n
+
+    def step(self):
+        if self.dirs:
+            tb = self.nwb.nw_align_pair_dev(self.ctx, self.da, self.db, self.sc, self.d_score)
+            self.nwb.nw_traceback_dev(self.ctx, tb, self.d_ops, self.d_len)
+            tb.free()
+        else:
+            self.nwb.nw_score_only_dev(self.ctx, self.da, self.db, self.sc, self.d_score)
+
+    def step_host(self):
+        """The same step through the host-pointer ABI (e2e)."""
+        if self.dirs:
+            score, tb = self.nwb.nw_align_pair(self.ctx, self.a, self.b, self.sc)
+            ops = self.nwb.nw_traceback(self.ctx, tb)
+            tb.free()
+            return 8 + 8 + len(ops)
+        self.nwb.nw_score_only(self.ctx, self.a, self.b, self.sc)
+        return 8
+
+    @property
+    def h2d_bytes(self):
+        return self.m + self.n
+
+
+class BatchWorkload:
+    """C3 (all pairs, score-only, sharded by rank) and C4 (protein, traceback)."""
+
+    def __init__(self, ctx, torch, workload: str, rank: int, world: int):
+        import paper_2412_21103_b200 as nwb
+        self.nwb, self.ctx, self.torch = nwb, ctx, torch
+        self.workload, self.rank, self.world = workload, rank, world
+        if workload == "c3":
+            ss = nwgen.config_c3()
+            pairs = nwgen.all_pairs(ss.nseq)
+            self.sc = nwgen.PAPER_DNA
+            self.flags = nwb.NW_SCORE_ONLY
+        else:
+            ss = nwgen.config_c4()
+            pairs = nwgen.consecutive_pairs(ss.nseq // 2)
+            self.sc = nwgen.PROTEIN_BLOSUM62
+            self.flags = nwb.NW_TRACEBACK
+        lens = ss.lengths()
+        cost = lens[pairs[:, 0]].astype(np.int64) * lens[pairs[:, 1]]
+        self.total_cells = int(cost.sum())
+        # cost-balanced shard: LPT deal of pairs (sorted by cost) over ranks
+        if world > 1:
+            order = np.argsort(-cost, kind="stable")
+            shard = order[rank::world]
+            pairs_r = pairs[np.sort(shard)]
+        else:
+            pairs_r = pairs if workload == "c4" else None
+        self.ss = ss
+        self.h_pairs = pairs_r
+        self.npairs = len(pairs) if pairs_r is None else len(pairs_r)
+        self.cells = int(cost.sum()) if pairs_r is None else int(
+            (lens[pairs_r[:, 0]].astype(np.int64) * lens[pairs_r[:, 1]]).sum())
+        self.d_seqs = torch.from_numpy(ss.residues).cuda()
+        self.d_offs = torch.from_numpy(ss.offs).cuda()
+        self.d_pairs = None if pairs_r is None else torch.from_numpy(pairs_r).cuda()
+        # padded to the largest shard so the score all-gather has equal-sized parts
+        self.shard_cap = -(-len(pairs) // world)
+        self.d_scores = torch.zeros(max(self.shard_cap, self.npairs), dtype=torch.int32,
+                                    device="cuda")
+        if self.flags:
+            oo = nwb.nw_batch_ops_offsets(ss.offs, pairs_r)
+            self.d_ops_off = torch.from_numpy(oo).cuda()
+            self.d_ops = torch.zeros(int(oo[-1]) + 1, dtype=torch.uint8, device="cuda")
+            self.d_ops_len = torch.zeros(self.npairs, dtype=torch.int32, device="cuda")
+        else:
+            self.d_ops_off = self.d_ops = self.d_ops_len = None
+        if world > 1:
+            import torch.distributed as dist
+            self.dist = dist
+            self.gathered = torch.empty(world * self.d_scores.numel(), dtype=torch.int32,
+                                        device="cuda")
+
+    def step(self):
+        self.nwb.nw_align_batch_dev(self.ctx, self.d_seqs, self.d_offs, self.ss.offs, self.d_pairs,
+                                    self.h_pairs, self.npairs, self.sc, self.flags, self.d_scores,
+                                    self.d_ops_off, self.d_ops, self.d_ops_len)
+        if self.world > 1:
+            # P:131 "gathered back in the main process": every rank gets every shard's scores
+            self.dist.all_gather_into_tensor(self.gathered, self.d_scores)
+
+    def step_host(self):
+        r = self.nwb.nw_align_batch(self.ctx, self.ss.residues, self.ss.offs, self.h_pairs, self.sc,
+                                    self.flags)
+        if self.flags:
+            return r[0].nbytes + sum(len(p) for p in r[1])
+        return r.nbytes
+
+    @property
+    def h2d_bytes(self):
+        return self.ss.residues.nbytes + self.ss.offs.nbytes + (
+            0 if self.h_pairs is None else self.h_pairs.nbytes)
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2412_21103_b200 as nwb
+    stream = torch.cuda.current_stream()
+    ctx = nwb.Context(local, stream.cuda_stream)
+    wl = args.workload
+    if wl in ("c1", "c2", "c5"):
+        W = PairWorkload(ctx, torch, wl, rank)
+    else:
+        W = BatchWorkload(ctx, torch, wl, rank, world)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        W.step()
+    torch.cuda.synchronize()
+    ctx.set_timing(True)
+    ctx.kernel_time(0)
+    ctx.kernel_time(1)
+    launches0 = ctx.launches()
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    evs = []
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        W.step()
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.launches() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    fill_ms, fill_n = ctx.kernel_time(0)
+    tb_ms, tb_n = ctx.kernel_time(1)
+    ctx.set_timing(False)
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    cells_all = W.cells * world if wl in ("c1", "c2", "c5") else W.total_cells
+    value = cells_all / (ms_per_step / 1e3) / 1e9
+    # ---- e2e through the host-pointer ABI
+    torch.cuda.synchronize()
+    barrier()
+    e2e_steps = max(1, min(args.steps, 5 if wl in ("c3", "c4") else args.steps))
+    d2h = 0
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        d2h = W.step_host()
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": cells_all / e2e_s / 1e9, "unit": "GCUPS", "h2d_bytes_per_step": W.h2d_bytes,
+           "d2h_bytes_per_step": d2h}
+    # ---- roofline of the dominant kernel (the fill)
+    fill_avg_ms = fill_ms / max(fill_n, 1)
+    mode = "dirs" if (wl in ("c1", "c2", "c4")) else "score"
+    ops = OPS_PER_CELL[mode]
+    cells_per_launch = W.cells
+    achieved = cells_per_launch * ops / (fill_avg_ms / 1e3) / 1e12 if fill_n else None
+    peak = ALU_ISSUE_LANES_PER_CLK_PER_SM * SM_COUNT * SM_MAX_MHZ * 1e6 / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{wl}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (int32 lane-ops)",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "kernel": "k_fill_pair" if wl in ("c1", "c2", "c5") else "k_batch",
+                "ops_per_cell": ops, "kernel_ms_per_launch": fill_avg_ms,
+                "kernel_share_of_step": (fill_ms / total_ms) if total_ms else None,
+                "traceback_ms_per_step": tb_ms / max(args.steps, 1),
+                "peak_source": "tools/peaks_int.cu issue limit 128 lane-ops/clk/SM x 148 SMs x 1965 MHz"}
+    out = {
+        "metric": "GCUPS (cell updates/s)", "value": value, "unit": "GCUPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (nwgen seeded, SURVEY.md §8(d) recipe)",
+        "config": {"workload": WORKLOADS[wl], "cells_per_step": cells_all,
+                   "parallelism": (f"replicas{world}" if wl in ("c1", "c2", "c5") else f"pairs-sharded{world}"),
+                   "l2": "flushed between steps (256 MB write)"},
+        "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roofline,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_oracle_sample(wl)
+    if rank == 0:
+        print(json.dumps(out))
+    ctx.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_reference(args):
+    """The reference arm = the oracle on the host cores (no GPU work)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    wl = args.workload
+    steps = []
+    budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    samples = None
+    for k in range(args.warmup + args.steps):
+        r = cpu_oracle_sample(wl, budget_s=budget)
+        if k >= args.warmup:
+            steps.append(r["value"])
+            samples = r
+    value = statistics.median(steps)
+    out = {"impl": "reference", "metric": "GCUPS (cell updates/s)", "value": value, "unit": "GCUPS",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "int64", "data": "synthetic (nwgen seeded)",
+           "config": {"workload": WORKLOADS[wl], "parallelism": "host cores"},
+           "cpu_baseline": {"value": value, "unit": "GCUPS", "cores": samples["cores"],
+                            "kind": "oracle", "sample": samples["sample"]},
+           "e2e": {"value": value, "unit": "GCUPS", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,169 @@
+/*
+ * nw.h -- C ABI of the B200-native Needleman-Wunsch hot path
+ *         (arXiv 2412.21103; PAPER.md = the paper text, "P:n" = its line n).
+ *
+ * What the library computes (DESIGN.md §1 states the readings R1-R22):
+ *   Grid      (m+1) x (n+1), sequence a on the rows i, b on the columns j.   P:24, P:33-34 (Sec. 2.1)
+ *   Borders   H(0,0)=0, H(i,0)=i*g, H(0,j)=j*g.                              P:43-45 (Sec. 2.2)
+ *   Fill      H(i,j) = max(H(i-1,j-1)+s(a_i,b_j), H(i-1,j)+g, H(i,j-1)+g)    P:47-54 (Sec. 2.3, Eq. 1, additive reading R1)
+ *   Codes     1 = diagonal, 2 = vertical (gap in b), 3 = horizontal (gap in a),
+ *             the first maximal candidate in the caller's tie order.           P:90 (Sec. 3.1)
+ *   Traceback from (m,n) to (0,0) along the codes, emitted in forward order.  P:65-72 (Sec. 2.4)
+ *   Batch     many independent pairs, e.g. all p<q of a set: n(n-1)/2.        P:131-135 (Sec. 3.2, Eq. 2)
+ *
+ * Conventions shared by every entry point:
+ *   - Residues are bytes; each must occur in scoring->alphabet (case-sensitive,
+ *     callers upper-case first, R10). Otherwise NW_E_ALPHABET and
+ *     nw_last_bad_pos() gives the first bad position (positions in b follow
+ *     those of a; in a batch, the offset into `seqs`).
+ *   - Host-pointer entry points are synchronous: they copy inputs to the device,
+ *     run on the context's stream, copy results back and synchronise.
+ *   - "_dev" entry points take device pointers, enqueue on the context's
+ *     stream and return without synchronising; results are valid once the
+ *     stream reaches that point. Validation that needs only sizes and the
+ *     scoring happens before anything is enqueued.
+ *   - Nothing aborts or throws. Every call returns an nw_status; on error the
+ *     outputs are unspecified (except *len on NW_E_TRUNC) and
+ *     nw_last_error(ctx) describes it.
+ *   - Scores fit int32 for every accepted input: the library rejects inputs
+ *     whose proven score bound |H| <= (m+n)*max(|g|, |s|) exceeds 2^30
+ *     (NW_E_OVERFLOW) (R11).
+ *   - One context per host thread; contexts are independent.
+ */
+#ifndef NW_B200_H
+#define NW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NW_OK = 0,
+  NW_E_INVAL = 1,     /* bad argument: gap >= 0, match <= mismatch, tie not a permutation of {1,2,3},
+                         K out of range, NULL pointer, negative length, cap < m+n in _dev traceback */
+  NW_E_ALPHABET = 2,  /* a residue is not in the alphabet (see nw_last_bad_pos) */
+  NW_E_OVERFLOW = 3,  /* sizes or score bound do not fit the int32 device arithmetic */
+  NW_E_NOMEM = 4,     /* device or host allocation failed */
+  NW_E_CUDA = 5,      /* a CUDA runtime error (message in nw_last_error) */
+  NW_E_TRUNC = 6,     /* ops buffer too small: *len holds the required length */
+  NW_E_STATE = 7,     /* traceback handle belongs to another context or holds no directions */
+  NW_E_DEADLOCK = 8,  /* an inter-warp dependency wait exceeded its watchdog */
+  NW_E_COMM = 9       /* reserved for the multi-GPU path */
+} nw_status;
+
+enum { NW_DIAG = 1, NW_UP = 2, NW_LEFT = 3 }; /* 1 diagonal, 2 vertical, 3 horizontal */
+
+/* Scoring inputs (north_star: "sequences, alphabet, match/mismatch/gap scores and a
+ * fixed traceback tie-break order"). All pointers are HOST pointers, read during the call.
+ *   match, mismatch  s(x,y) when subst == NULL (+1 / -1). Requires match > mismatch.
+ *   gap              linear gap score g (-1). Requires g < 0.
+ *   subst            optional K*K int32 row-major matrix over `alphabet` (e.g. BLOSUM62);
+ *                    when given, match/mismatch are ignored. All scores in [-31, 31]
+ *                    (int8 device profile of s - 2g), 1 <= -g <= 48.
+ *   alphabet, K      the K symbols, 1 <= K <= 64 (DNA "ACGT", protein 20 letters).
+ *   tie              permutation of {NW_DIAG, NW_UP, NW_LEFT}, highest priority first;
+ *                    {1,2,3} = diagonal > vertical > horizontal (default, P:90 code order). */
+typedef struct {
+  int32_t match;
+  int32_t mismatch;
+  int32_t gap;
+  const int32_t *subst;
+  const char *alphabet;
+  int32_t K;
+  uint8_t tie[3];
+} nw_scoring;
+
+typedef struct nw_ctx nw_ctx; /* device, stream, workspace, last error */
+typedef struct nw_tb nw_tb;   /* 2-bit packed directions of one filled pair, resident on the device */
+
+/* Create a context on CUDA device `device`, enqueuing on `cuda_stream`
+ * (a cudaStream_t; NULL = the legacy default stream). *out owned by the caller,
+ * released with nw_ctx_destroy. */
+nw_status nw_ctx_create(int device, void *cuda_stream, nw_ctx **out);
+void nw_ctx_destroy(nw_ctx *ctx);
+const char *nw_strerror(nw_status st);
+const char *nw_last_error(const nw_ctx *ctx);
+int64_t nw_last_bad_pos(const nw_ctx *ctx);
+
+/* ---- nw_score_only: H(m,n) in linear device memory (no directions). ----
+ * Fill of Sec. 2.2-2.3; only strip-boundary rows are kept (O(n) memory).
+ * a: m residues, b: n residues (m, n >= 0). *score receives H(m,n). */
+nw_status nw_score_only(nw_ctx *ctx, const uint8_t *a, int64_t m, const uint8_t *b, int64_t n,
+                        const nw_scoring *sc, int64_t *score);
+/* Device variant: d_a, d_b device residues; d_score device int64. Alphabet errors are
+ * detected on the device and reported by the next synchronising call on ctx
+ * (nw_ctx_sync) as NW_E_ALPHABET. */
+nw_status nw_score_only_dev(nw_ctx *ctx, const uint8_t *d_a, int64_t m, const uint8_t *d_b,
+                            int64_t n, const nw_scoring *sc, int64_t *d_score);
+
+/* ---- nw_align_pair: fill + 2-bit directions kept on the device. ----
+ * Fill of Sec. 2.2-2.3 plus the P:90 code of every interior cell, packed at 2 bits
+ * per cell in HBM. *score receives H(m,n). *tb receives a handle owned by the caller
+ * (nw_tb_free), valid only with this ctx, consumed by nw_traceback. tb may be NULL
+ * (score only, directions discarded). */
+nw_status nw_align_pair(nw_ctx *ctx, const uint8_t *a, int64_t m, const uint8_t *b, int64_t n,
+                        const nw_scoring *sc, int64_t *score, nw_tb **tb);
+nw_status nw_align_pair_dev(nw_ctx *ctx, const uint8_t *d_a, int64_t m, const uint8_t *d_b,
+                            int64_t n, const nw_scoring *sc, int64_t *d_score, nw_tb **tb);
+
+/* ---- nw_traceback: the backtracking of Sec. 2.4. ----
+ * Walks the directions of `tb` from (m,n) to (0,0) and writes the path's codes
+ * (1/2/3) in forward order (first alignment column first) to ops[0..len).
+ * max(m,n) <= len <= m+n. Host variant: if cap < len returns NW_E_TRUNC with *len
+ * set (cap = 0 queries the length). */
+nw_status nw_traceback(nw_ctx *ctx, const nw_tb *tb, uint8_t *ops, int64_t cap, int64_t *len);
+/* Device variant: d_ops device buffer with cap >= m+n (else NW_E_INVAL), d_len device int64. */
+nw_status nw_traceback_dev(nw_ctx *ctx, const nw_tb *tb, uint8_t *d_ops, int64_t cap,
+                           int64_t *d_len);
+void nw_tb_free(nw_tb *tb);
+
+/* ---- nw_align_batch: many independent pairs. ----
+ * seqs: concatenated residues; offs[0..nseq]: sequence k is seqs[offs[k]..offs[k+1]).
+ * pairs: 2*npairs int32 indices (p, q) = (rows, columns) of each alignment, or NULL for
+ *        all p<q in lexicographic order (npairs must then equal nseq*(nseq-1)/2).
+ * flags: NW_SCORE_ONLY, or NW_TRACEBACK to also emit every pair's path.
+ * scores: npairs int32 (H(m,n) per pair, in pair order).
+ * With NW_TRACEBACK: ops_off: npairs+1 int64 filled by the library with the offsets
+ *        (ops_off[k] = sum over k' < k of (m_k' + n_k'), the worst-case path lengths),
+ *        ops: ops_off[npairs] bytes; pair k's path (forward codes) is at
+ *        ops[ops_off[k] .. ops_off[k] + ops_len[k]). Unused otherwise (may be NULL). */
+#define NW_SCORE_ONLY 0u
+#define NW_TRACEBACK 1u
+nw_status nw_align_batch(nw_ctx *ctx, const uint8_t *seqs, const int64_t *offs, int32_t nseq,
+                         const int32_t *pairs, int64_t npairs, const nw_scoring *sc,
+                         uint32_t flags, int32_t *scores, int64_t *ops_off, uint8_t *ops,
+                         int32_t *ops_len);
+/* Device variant: every array is a device pointer (offs/pairs read by the host too:
+ * pass host copies in h_offs / h_pairs, used for sizing and length binning;
+ * h_pairs may be NULL when pairs is NULL). ops_off is then a device array the
+ * caller fills (e.g. from the host prefix sum nw_batch_ops_offsets). */
+nw_status nw_align_batch_dev(nw_ctx *ctx, const uint8_t *d_seqs, const int64_t *d_offs,
+                             const int64_t *h_offs, int32_t nseq, const int32_t *d_pairs,
+                             const int32_t *h_pairs, int64_t npairs, const nw_scoring *sc,
+                             uint32_t flags, int32_t *d_scores, const int64_t *d_ops_off,
+                             uint8_t *d_ops, int32_t *d_ops_len);
+/* Host helper: ops_off[0..npairs] worst-case offsets for NW_TRACEBACK (see above). */
+nw_status nw_batch_ops_offsets(const int64_t *h_offs, int32_t nseq, const int32_t *h_pairs,
+                               int64_t npairs, int64_t *ops_off);
+
+/* Wait for the context's stream and report any deferred device-side error
+ * (alphabet violations, watchdog) raised by earlier _dev calls. */
+nw_status nw_ctx_sync(nw_ctx *ctx);
+
+/* Number of library kernels launched on this context so far (bench accounting). */
+int64_t nw_ctx_launches(const nw_ctx *ctx);
+
+/* Kernel timing (bench accounting). With enable != 0 the context brackets every
+ * launch of its hot kernels with CUDA events recorded on its own stream:
+ * class 0 = the DP fill (single-pair or batch kernel), class 1 = the traceback
+ * (walk + reverse). nw_ctx_kernel_time synchronises, returns the summed event
+ * milliseconds and launch count of one class since the last read, and resets it. */
+nw_status nw_ctx_set_timing(nw_ctx *ctx, int enable);
+nw_status nw_ctx_kernel_time(nw_ctx *ctx, int kernel_class, double *total_ms, int64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NW_B200_H */

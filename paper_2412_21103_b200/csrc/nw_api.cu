@@ -1,0 +1,872 @@
+// nw_api.cu -- host side of the C ABI declared in include/nw.h.
+//
+// Validation, alphabet/profile tables, workspace, kernel dispatch and error
+// reporting. Every step of the computation runs in the kernels of
+// nw_kernels.cuh; this file only marshals. There is no CPU fallback: without
+// a CUDA device every entry point returns NW_E_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/nw.h"
+#define NW_COMMON_KERNELS 1
+#include "nw_launch.cuh"
+
+using namespace nwk;
+
+namespace {
+
+constexpr int SCORE_MAX = 31;
+constexpr int GAP_MAX = 48;
+
+}  // namespace
+
+struct nw_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 0;
+  char err[512] = {0};
+  long long bad_pos = -1;
+  long long launches = 0;
+  // workspace (grow-only)
+  uint8_t* d_lut = nullptr;     // 256
+  int8_t* d_prof = nullptr;     // 64*64
+  long long* d_bad = nullptr;   // 1 (+ spare)
+  int* d_ints = nullptr;        // small ints: [0] ticket [1] err [2] hm [3..] prog
+  size_t ints_cap = 0;
+  uint8_t* d_codes = nullptr;   // encoded inputs
+  size_t codes_cap = 0;
+  uint8_t* d_raw = nullptr;     // raw residues copied from the host
+  size_t raw_cap = 0;
+  int* d_bnd = nullptr;
+  size_t bnd_cap = 0;
+  uint8_t* d_rev = nullptr;     // reversed traceback
+  size_t rev_cap = 0;
+  long long* d_len = nullptr;   // traceback length
+  long long* d_score = nullptr; // score staging
+  void* d_scratch = nullptr;    // batch per-warp scratch
+  size_t scratch_cap = 0;
+  void* d_aux = nullptr;        // batch perm/order/offs/pairs staging
+  size_t aux_cap = 0;
+  // kernel timing (nw_ctx_set_timing): event pairs per kernel class
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_open[2];
+  std::vector<cudaEvent_t> ev_pool;
+  // last scoring uploaded (avoid re-uploading identical tables)
+  bool have_tables = false;
+  uint8_t lut_h[256];
+  int8_t prof_h[64 * 64];
+};
+
+struct nw_tb {
+  nw_ctx* ctx;
+  uint32_t* dirs;
+  long long wpl;
+  int m, n;
+  uint8_t tie[3];
+};
+
+namespace {
+
+nw_status fail(nw_ctx* c, nw_status st, const char* fmt, ...) {
+  if (c) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(c->err, sizeof c->err, fmt, ap);
+    va_end(ap);
+  }
+  return st;
+}
+
+#define CUDA_TRY(c, x)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess) {                                                              \
+      return fail((c), e_ == cudaErrorMemoryAllocation ? NW_E_NOMEM : NW_E_CUDA,          \
+                  "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__);      \
+    }                                                                                     \
+  } while (0)
+
+#define LAUNCHED(c) ((c)->launches++)
+
+cudaEvent_t take_event(nw_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets kernel launches of one class with events when timing is enabled.
+struct KernelTimer {
+  nw_ctx* c;
+  int cls;
+  cudaEvent_t e0 = nullptr;
+  KernelTimer(nw_ctx* ctx, int k) : c(ctx), cls(k) {
+    if (c->timing) {
+      e0 = take_event(c);
+      cudaEventRecord(e0, c->stream);
+    }
+  }
+  ~KernelTimer() {
+    if (c->timing) {
+      cudaEvent_t e1 = take_event(c);
+      cudaEventRecord(e1, c->stream);
+      c->ev_open[cls].push_back({e0, e1});
+    }
+  }
+};
+
+template <class T>
+nw_status grow(nw_ctx* c, T*& p, size_t& cap, size_t need_bytes) {
+  if (need_bytes <= cap && p) return NW_OK;
+  if (p) {
+    cudaFreeAsync(p, c->stream);
+    p = nullptr;
+    cap = 0;
+  }
+  size_t bytes = std::max<size_t>(need_bytes, 256);
+  bytes = bytes + bytes / 4;
+  CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, c->stream));
+  cap = bytes;
+  return NW_OK;
+}
+
+nw_status check_scoring(nw_ctx* c, const nw_scoring* sc) {
+  if (!sc) return fail(c, NW_E_INVAL, "scoring is NULL");
+  if (!sc->alphabet) return fail(c, NW_E_INVAL, "alphabet is NULL");
+  if (sc->K < 1 || sc->K > 64) return fail(c, NW_E_INVAL, "K=%d outside [1,64]", sc->K);
+  if (sc->gap >= 0) return fail(c, NW_E_INVAL, "gap %d must be negative", sc->gap);
+  if (sc->gap < -GAP_MAX) return fail(c, NW_E_INVAL, "gap %d below -%d", sc->gap, GAP_MAX);
+  int seen[4] = {0, 0, 0, 0};
+  for (int t = 0; t < 3; ++t) {
+    if (sc->tie[t] < 1 || sc->tie[t] > 3 || seen[sc->tie[t]])
+      return fail(c, NW_E_INVAL, "tie order is not a permutation of {1,2,3}");
+    seen[sc->tie[t]] = 1;
+  }
+  for (int x = 0; x < sc->K; ++x)
+    for (int y = 0; y < x; ++y)
+      if (sc->alphabet[x] == sc->alphabet[y])
+        return fail(c, NW_E_INVAL, "alphabet symbol '%c' repeated", sc->alphabet[x]);
+  if (sc->subst) {
+    for (int k = 0; k < sc->K * sc->K; ++k)
+      if (sc->subst[k] < -SCORE_MAX || sc->subst[k] > SCORE_MAX)
+        return fail(c, NW_E_INVAL, "substitution score %d outside [-%d,%d]", sc->subst[k],
+                    SCORE_MAX, SCORE_MAX);
+  } else {
+    if (sc->match <= sc->mismatch)
+      return fail(c, NW_E_INVAL, "match %d must exceed mismatch %d", sc->match, sc->mismatch);
+    if (sc->match > SCORE_MAX || sc->mismatch < -SCORE_MAX)
+      return fail(c, NW_E_INVAL, "match/mismatch outside [-%d,%d]", SCORE_MAX, SCORE_MAX);
+  }
+  return NW_OK;
+}
+
+int score_of(const nw_scoring* sc, int x, int y) {
+  return sc->subst ? sc->subst[x * sc->K + y] : (x == y ? sc->match : sc->mismatch);
+}
+
+// Upload the 256-entry residue -> code table and the K x K profile of
+// s(x,y) - 2g (the shifted recurrence, nw_fill.cuh).
+nw_status upload_tables(nw_ctx* c, const nw_scoring* sc) {
+  uint8_t lut[256];
+  memset(lut, 0xff, sizeof lut);
+  for (int k = 0; k < sc->K; ++k) lut[(uint8_t)sc->alphabet[k]] = (uint8_t)k;
+  int8_t prof[64 * 64];
+  memset(prof, 0, sizeof prof);
+  for (int x = 0; x < sc->K; ++x)
+    for (int y = 0; y < sc->K; ++y) prof[x * sc->K + y] = (int8_t)(score_of(sc, x, y) - 2 * sc->gap);
+  if (c->have_tables && !memcmp(lut, c->lut_h, sizeof lut) && !memcmp(prof, c->prof_h, sizeof prof))
+    return NW_OK;
+  memcpy(c->lut_h, lut, sizeof lut);
+  memcpy(c->prof_h, prof, sizeof prof);
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_lut, c->lut_h, 256, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_prof, c->prof_h, sizeof prof, cudaMemcpyHostToDevice, c->stream));
+  c->have_tables = true;
+  return NW_OK;
+}
+
+// |H| <= (m+n) * max(|g|, max|s|) must leave headroom in int32 (R11);
+// the shifted H' adds up to (m+n)*|g| more.
+nw_status check_bounds(nw_ctx* c, const nw_scoring* sc, long long m, long long n) {
+  if (m < 0 || n < 0) return fail(c, NW_E_INVAL, "negative length");
+  int smax = std::abs(sc->gap);
+  for (int x = 0; x < sc->K; ++x)
+    for (int y = 0; y < sc->K; ++y) smax = std::max(smax, std::abs(score_of(sc, x, y)));
+  const double bound = (double)(m + n) * (double)(smax + 2 * std::abs(sc->gap));
+  if (bound >= (double)(1 << 30) || m > (1 << 28) || n > (1 << 28))
+    return fail(c, NW_E_OVERFLOW, "m=%lld n=%lld exceed the int32 score bound", m, n);
+  return NW_OK;
+}
+
+int pi_code(const uint8_t tie[3]) { return tie[0] * 100 + tie[1] * 10 + tie[2]; }
+
+// ---- kernel dispatch: score-only kernels here, one TU per tie order for DIRS ----
+}  // namespace
+namespace nwk {
+NW_DEFINE_DIRS_LAUNCHERS(123)
+}  // namespace nwk
+namespace {
+
+bool dispatch_fill(bool dirs, int pi, bool profreg, const FillArgs& A, int grid, size_t smem,
+                   cudaStream_t st) {
+  if (!dirs) {
+    if (profreg) launch_fill_t<KR_PAIR, false, true, 123>(A, grid, smem, st);
+    else launch_fill_t<KR_PAIR, false, false, 123>(A, grid, smem, st);
+    return true;
+  }
+  switch (pi) {
+    case 123: launch_fill_dirs<123>(A, profreg, grid, smem, st); return true;
+    case 132: launch_fill_dirs<132>(A, profreg, grid, smem, st); return true;
+    case 213: launch_fill_dirs<213>(A, profreg, grid, smem, st); return true;
+    case 231: launch_fill_dirs<231>(A, profreg, grid, smem, st); return true;
+    case 312: launch_fill_dirs<312>(A, profreg, grid, smem, st); return true;
+    case 321: launch_fill_dirs<321>(A, profreg, grid, smem, st); return true;
+  }
+  return false;
+}
+
+bool dispatch_batch(bool dirs, int pi, bool profreg, const BatchArgs& B, int grid, size_t smem,
+                    cudaStream_t st) {
+  if (!dirs) {
+    if (profreg) launch_batch_t<KR_BATCH, false, true, 123>(B, grid, smem, st);
+    else launch_batch_t<KR_BATCH, false, false, 123>(B, grid, smem, st);
+    return true;
+  }
+  switch (pi) {
+    case 123: launch_batch_dirs<123>(B, profreg, grid, smem, st); return true;
+    case 132: launch_batch_dirs<132>(B, profreg, grid, smem, st); return true;
+    case 213: launch_batch_dirs<213>(B, profreg, grid, smem, st); return true;
+    case 231: launch_batch_dirs<231>(B, profreg, grid, smem, st); return true;
+    case 312: launch_batch_dirs<312>(B, profreg, grid, smem, st); return true;
+    case 321: launch_batch_dirs<321>(B, profreg, grid, smem, st); return true;
+  }
+  return false;
+}
+
+// Encode `len` device residues at `raw` into codes at `out` (PAD zero bytes
+// on both sides are the caller's allocation). Positions reported + pos_base.
+void launch_encode(nw_ctx* c, const uint8_t* raw, long long len, uint8_t* out, long long pos_base) {
+  if (len <= 0) return;
+  long long blocks = (len + 4 * 256 - 1) / (4 * 256);
+  blocks = std::min<long long>(blocks, (long long)c->sm_count * 8);
+  k_encode<<<(int)blocks, 256, 0, c->stream>>>(raw, len, c->d_lut, out, c->d_bad, pos_base);
+  LAUNCHED(c);
+}
+
+nw_status init_small(nw_ctx* c, int nints) {
+  nw_status st = grow(c, c->d_ints, c->ints_cap, sizeof(int) * (size_t)nints);
+  if (st) return st;
+  int blocks = std::min(1024, (nints + 255) / 256);
+  k_init<<<blocks, 256, 0, c->stream>>>(c->d_ints, nints, c->d_bad);
+  LAUNCHED(c);
+  return NW_OK;
+}
+
+// Device-side core of nw_score_only / nw_align_pair on already-encoded codes.
+// ca, cb: codes with PAD before and >= R + PAD after. Writes H(m,n) to d_score.
+nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb, long long n,
+                    const nw_scoring* sc, long long* d_score, nw_tb* tb);
+
+}  // namespace
+
+// ---- kernels for tiny bookkeeping ----
+namespace nwk {
+__global__ void k_finish_score(const int* hm, long long gmn, long long* out, int m_or_n_zero) {
+  *out = (m_or_n_zero ? 0 : (long long)*hm) + gmn;
+}
+}  // namespace nwk
+
+namespace {
+
+nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb, long long n,
+                    const nw_scoring* sc, long long* d_score, nw_tb* tb) {
+  constexpr int R = 32 * KR_PAIR;
+  const int nstrips = (int)((m + R - 1) / R);
+  const bool dirs = tb != nullptr;
+  nw_status st = NW_OK;
+  int* ticket = c->d_ints;
+  int* errf = c->d_ints + 1;
+  int* hm = c->d_ints + 2;
+  int* prog = c->d_ints + 3;
+  const long long gmn = (long long)sc->gap * (m + n);
+  if (m > 0 && n > 0) {
+    const long long bstride = n + 1 + 64;
+    st = grow(c, c->d_bnd, c->bnd_cap, sizeof(int) * 2 * (size_t)bstride);
+    if (st) return st;
+    FillArgs A;
+    A.a = ca; A.b = cb; A.prof = c->d_prof; A.K = sc->K;
+    A.m = (int)m; A.n = (int)n; A.nstrips = nstrips; A.nslots = 2;
+    A.bnd = c->d_bnd; A.bstride = bstride; A.prog = prog; A.ticket = ticket;
+    A.dirs = dirs ? tb->dirs : nullptr;
+    A.wpl = dirs ? tb->wpl : 0;
+    A.hm = hm; A.err = errf;
+    const bool profreg = sc->K <= 4;
+    const size_t smem = profreg ? 0 : (size_t)sc->K * R;
+    // persistent grid: one warp per CTA, at most the resident capacity
+    int per_sm = 16;
+    int grid = std::min<long long>(nstrips, (long long)c->sm_count * per_sm);
+    const int pi = dirs ? pi_code(sc->tie) : 123;
+    bool ok;
+    {
+      KernelTimer kt(c, 0);
+      ok = dispatch_fill(dirs, pi, profreg, A, grid, smem, c->stream);
+    }
+    if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
+    LAUNCHED(c);
+    CUDA_TRY(c, cudaGetLastError());
+  }
+  k_finish_score<<<1, 1, 0, c->stream>>>(hm, gmn, d_score, (m == 0 || n == 0) ? 1 : 0);
+  LAUNCHED(c);
+  CUDA_TRY(c, cudaGetLastError());
+  return NW_OK;
+}
+
+nw_status check_deferred(nw_ctx* c) {
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  long long bad = 0;
+  int errf = 0;
+  CUDA_TRY(c, cudaMemcpy(&bad, c->d_bad, sizeof bad, cudaMemcpyDeviceToHost));
+  if (c->d_ints) CUDA_TRY(c, cudaMemcpy(&errf, c->d_ints + 1, sizeof errf, cudaMemcpyDeviceToHost));
+  if (bad != 0x7fffffffffffffffll) {
+    c->bad_pos = bad;
+    return fail(c, NW_E_ALPHABET, "residue at position %lld is not in the alphabet", bad);
+  }
+  if (errf) return fail(c, NW_E_DEADLOCK, "inter-warp dependency watchdog fired");
+  return NW_OK;
+}
+
+// Stage host residues into device codes (PAD | a | pad to R + PAD).
+nw_status stage_pair(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b, long long n,
+                     bool host, uint8_t** ca, uint8_t** cb) {
+  constexpr long long R = 32 * KR_PAIR;
+  const long long la = PAD + m + R + PAD, lb = PAD + n + R + PAD;
+  nw_status st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
+  if (st) return st;
+  CUDA_TRY(c, cudaMemsetAsync(c->d_codes, 0, (size_t)(la + lb), c->stream));
+  *ca = c->d_codes + PAD;
+  *cb = c->d_codes + la + PAD;
+  const uint8_t *ra = a, *rb = b;
+  if (host) {
+    st = grow(c, c->d_raw, c->raw_cap, (size_t)(m + n + 16));
+    if (st) return st;
+    if (m) CUDA_TRY(c, cudaMemcpyAsync(c->d_raw, a, (size_t)m, cudaMemcpyHostToDevice, c->stream));
+    if (n) CUDA_TRY(c, cudaMemcpyAsync(c->d_raw + m, b, (size_t)n, cudaMemcpyHostToDevice, c->stream));
+    ra = c->d_raw;
+    rb = c->d_raw + m;
+  }
+  launch_encode(c, ra, m, *ca, 0);
+  launch_encode(c, rb, n, *cb, m);
+  CUDA_TRY(c, cudaGetLastError());
+  return NW_OK;
+}
+
+nw_status new_tb(nw_ctx* c, long long m, long long n, const nw_scoring* sc, nw_tb** out) {
+  constexpr int R = 32 * KR_PAIR, SPW = 16 / KR_PAIR;
+  nw_tb* tb = new (std::nothrow) nw_tb;
+  if (!tb) return fail(c, NW_E_NOMEM, "host allocation");
+  tb->ctx = c;
+  tb->m = (int)m;
+  tb->n = (int)n;
+  memcpy(tb->tie, sc->tie, 3);
+  const long long nstrips = (m + R - 1) / R;
+  const long long nblk = (n + 62) / 32;
+  tb->wpl = nblk * (32 / SPW);
+  tb->dirs = nullptr;
+  const size_t bytes = (size_t)std::max<long long>(nstrips, 1) * tb->wpl * 32 * sizeof(uint32_t);
+  if (m > 0 && n > 0) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&tb->dirs), bytes, c->stream);
+    if (e != cudaSuccess) {
+      delete tb;
+      return fail(c, NW_E_NOMEM, "direction buffer of %zu bytes: %s", bytes, cudaGetErrorString(e));
+    }
+  }
+  *out = tb;
+  return NW_OK;
+}
+
+nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b, long long n,
+                     const nw_scoring* sc, bool host, long long* score_out, nw_tb** tb_out,
+                     bool want_dirs) {
+  if (!c) return NW_E_INVAL;
+  if ((m > 0 && !a) || (n > 0 && !b) || !score_out) return fail(c, NW_E_INVAL, "NULL argument");
+  nw_status st = check_scoring(c, sc);
+  if (st) return st;
+  st = check_bounds(c, sc, m, n);
+  if (st) return st;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  st = upload_tables(c, sc);
+  if (st) return st;
+  // zero ticket/err/hm/progress counters and the bad-position flag before encoding
+  st = init_small(c, 3 + (int)std::max<long long>((m + 32 * KR_PAIR - 1) / (32 * KR_PAIR), 1));
+  if (st) return st;
+  uint8_t *ca, *cb;
+  st = stage_pair(c, a, m, b, n, host, &ca, &cb);
+  if (st) return st;
+  nw_tb* tb = nullptr;
+  if (want_dirs) {
+    st = new_tb(c, m, n, sc, &tb);
+    if (st) return st;
+  }
+  long long* d_score = host ? c->d_score : score_out;
+  st = pair_core(c, ca, m, cb, n, sc, d_score, tb);
+  if (st) {
+    if (tb) nw_tb_free(tb);
+    return st;
+  }
+  if (host) {
+    CUDA_TRY(c, cudaMemcpyAsync(score_out, c->d_score, sizeof(long long), cudaMemcpyDeviceToHost,
+                                c->stream));
+    st = check_deferred(c);
+    if (st) {
+      if (tb) nw_tb_free(tb);
+      return st;
+    }
+  }
+  if (tb_out) *tb_out = tb;
+  else if (tb) nw_tb_free(tb);
+  return NW_OK;
+}
+
+}  // namespace
+
+// ======================= exported C ABI =======================
+
+extern "C" {
+
+const char* nw_strerror(nw_status st) {
+  switch (st) {
+    case NW_OK: return "ok";
+    case NW_E_INVAL: return "invalid argument";
+    case NW_E_ALPHABET: return "residue not in alphabet";
+    case NW_E_OVERFLOW: return "input too large for int32 scores";
+    case NW_E_NOMEM: return "out of memory";
+    case NW_E_CUDA: return "CUDA error";
+    case NW_E_TRUNC: return "ops buffer too small";
+    case NW_E_STATE: return "traceback handle not valid for this context";
+    case NW_E_DEADLOCK: return "dependency watchdog fired";
+    case NW_E_COMM: return "communication error";
+  }
+  return "unknown status";
+}
+
+nw_status nw_ctx_create(int device, void* cuda_stream, nw_ctx** out) {
+  if (!out) return NW_E_INVAL;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return NW_E_CUDA;
+  if (device < 0 || device >= ndev) return NW_E_INVAL;
+  nw_ctx* c = new (std::nothrow) nw_ctx;
+  if (!c) return NW_E_NOMEM;
+  c->device = device;
+  c->stream = (cudaStream_t)cuda_stream;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+    delete c;
+    return NW_E_CUDA;
+  }
+  if (cudaMalloc(&c->d_lut, 256) != cudaSuccess || cudaMalloc(&c->d_prof, 64 * 64) != cudaSuccess ||
+      cudaMalloc(&c->d_bad, 4 * sizeof(long long)) != cudaSuccess ||
+      cudaMalloc(&c->d_len, sizeof(long long)) != cudaSuccess ||
+      cudaMalloc(&c->d_score, sizeof(long long)) != cudaSuccess) {
+    nw_ctx_destroy(c);
+    return NW_E_NOMEM;
+  }
+  long long init_bad = 0x7fffffffffffffffll;
+  cudaMemcpy(c->d_bad, &init_bad, sizeof init_bad, cudaMemcpyHostToDevice);
+  // keep freed stream-ordered allocations in the pool (steady-state calls allocate nothing new)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = c;
+  return NW_OK;
+}
+
+void nw_ctx_destroy(nw_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  cudaFree(c->d_lut);
+  cudaFree(c->d_prof);
+  cudaFree(c->d_bad);
+  cudaFree(c->d_len);
+  cudaFree(c->d_score);
+  if (c->d_ints) cudaFreeAsync(c->d_ints, c->stream);
+  if (c->d_codes) cudaFreeAsync(c->d_codes, c->stream);
+  if (c->d_raw) cudaFreeAsync(c->d_raw, c->stream);
+  if (c->d_bnd) cudaFreeAsync(c->d_bnd, c->stream);
+  if (c->d_rev) cudaFreeAsync(c->d_rev, c->stream);
+  if (c->d_scratch) cudaFreeAsync(c->d_scratch, c->stream);
+  if (c->d_aux) cudaFreeAsync(c->d_aux, c->stream);
+  cudaStreamSynchronize(c->stream);
+  for (auto& v : c->ev_open)
+    for (auto& pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  delete c;
+}
+
+const char* nw_last_error(const nw_ctx* c) { return c ? c->err : "no context"; }
+int64_t nw_last_bad_pos(const nw_ctx* c) { return c ? c->bad_pos : -1; }
+int64_t nw_ctx_launches(const nw_ctx* c) { return c ? c->launches : 0; }
+
+nw_status nw_ctx_set_timing(nw_ctx* c, int enable) {
+  if (!c) return NW_E_INVAL;
+  c->timing = enable != 0;
+  return NW_OK;
+}
+
+nw_status nw_ctx_kernel_time(nw_ctx* c, int cls, double* total_ms, int64_t* launches) {
+  if (!c || cls < 0 || cls > 1 || !total_ms || !launches) return NW_E_INVAL;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  double tot = 0;
+  for (auto& pr : c->ev_open[cls]) {
+    CUDA_TRY(c, cudaEventSynchronize(pr.second));
+    float ms = 0;
+    CUDA_TRY(c, cudaEventElapsedTime(&ms, pr.first, pr.second));
+    tot += ms;
+    c->ev_pool.push_back(pr.first);
+    c->ev_pool.push_back(pr.second);
+  }
+  *launches = (int64_t)c->ev_open[cls].size();
+  c->ev_open[cls].clear();
+  *total_ms = tot;
+  return NW_OK;
+}
+
+nw_status nw_ctx_sync(nw_ctx* c) {
+  if (!c) return NW_E_INVAL;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  return check_deferred(c);
+}
+
+nw_status nw_score_only(nw_ctx* c, const uint8_t* a, int64_t m, const uint8_t* b, int64_t n,
+                        const nw_scoring* sc, int64_t* score) {
+  return pair_entry(c, a, m, b, n, sc, true, reinterpret_cast<long long*>(score), nullptr, false);
+}
+
+nw_status nw_score_only_dev(nw_ctx* c, const uint8_t* d_a, int64_t m, const uint8_t* d_b,
+                            int64_t n, const nw_scoring* sc, int64_t* d_score) {
+  return pair_entry(c, d_a, m, d_b, n, sc, false, reinterpret_cast<long long*>(d_score), nullptr,
+                    false);
+}
+
+nw_status nw_align_pair(nw_ctx* c, const uint8_t* a, int64_t m, const uint8_t* b, int64_t n,
+                        const nw_scoring* sc, int64_t* score, nw_tb** tb) {
+  return pair_entry(c, a, m, b, n, sc, true, reinterpret_cast<long long*>(score), tb, true);
+}
+
+nw_status nw_align_pair_dev(nw_ctx* c, const uint8_t* d_a, int64_t m, const uint8_t* d_b,
+                            int64_t n, const nw_scoring* sc, int64_t* d_score, nw_tb** tb) {
+  return pair_entry(c, d_a, m, d_b, n, sc, false, reinterpret_cast<long long*>(d_score), tb, true);
+}
+
+void nw_tb_free(nw_tb* tb) {
+  if (!tb) return;
+  if (tb->dirs) cudaFreeAsync(tb->dirs, tb->ctx->stream);
+  delete tb;
+}
+
+static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops) {
+  const long long L = (long long)tb->m + tb->n;
+  nw_status st = grow(c, c->d_rev, c->rev_cap, (size_t)std::max<long long>(L, 1));
+  if (st) return st;
+  {
+    KernelTimer kt(c, 1);
+    k_tb_walk<KR_PAIR><<<1, 32, 0, c->stream>>>(tb->dirs, tb->wpl, tb->m, tb->n, tb->tie[0],
+                                                tb->tie[1], tb->tie[2], c->d_rev, c->d_len);
+    LAUNCHED(c);
+    int blocks = (int)std::min<long long>((L + 255) / 256 + 1, (long long)c->sm_count * 4);
+    k_reverse<<<blocks, 256, 0, c->stream>>>(c->d_rev, c->d_len, d_ops);
+    LAUNCHED(c);
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  return NW_OK;
+}
+
+nw_status nw_traceback(nw_ctx* c, const nw_tb* tb, uint8_t* ops, int64_t cap, int64_t* len) {
+  if (!c || !tb || !len) return c ? fail(c, NW_E_INVAL, "NULL argument") : NW_E_INVAL;
+  if (tb->ctx != c) return fail(c, NW_E_STATE, "traceback handle belongs to another context");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const long long L = (long long)tb->m + tb->n;
+  if (tb->m == 0 || tb->n == 0) {
+    *len = L;
+    if (cap < L) return fail(c, NW_E_TRUNC, "cap %lld < length %lld", (long long)cap, L);
+    for (long long k = 0; k < L; ++k) ops[k] = tb->m > 0 ? NW_UP : NW_LEFT;
+    return NW_OK;
+  }
+  uint8_t* d_ops = nullptr;
+  CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&d_ops), (size_t)L, c->stream));
+  nw_status st = traceback_core(c, tb, d_ops);
+  if (st) { cudaFreeAsync(d_ops, c->stream); return st; }
+  long long hl = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&hl, c->d_len, sizeof hl, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  *len = hl;
+  if (cap < hl) {
+    cudaFreeAsync(d_ops, c->stream);
+    return fail(c, NW_E_TRUNC, "cap %lld < length %lld", (long long)cap, hl);
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(ops, d_ops, (size_t)hl, cudaMemcpyDeviceToHost, c->stream));
+  cudaFreeAsync(d_ops, c->stream);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return NW_OK;
+}
+
+nw_status nw_traceback_dev(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops, int64_t cap, int64_t* d_len) {
+  if (!c || !tb || !d_ops || !d_len) return c ? fail(c, NW_E_INVAL, "NULL argument") : NW_E_INVAL;
+  if (tb->ctx != c) return fail(c, NW_E_STATE, "traceback handle belongs to another context");
+  const long long L = (long long)tb->m + tb->n;
+  if (cap < L) return fail(c, NW_E_INVAL, "cap %lld < m+n = %lld", (long long)cap, L);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (tb->m == 0 || tb->n == 0) {
+    if (L) CUDA_TRY(c, cudaMemsetAsync(d_ops, tb->m > 0 ? NW_UP : NW_LEFT, (size_t)L, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(d_len, &L, sizeof L, cudaMemcpyHostToDevice, c->stream));
+    return NW_OK;
+  }
+  nw_status st = traceback_core(c, tb, d_ops);
+  if (st) return st;
+  CUDA_TRY(c, cudaMemcpyAsync(d_len, c->d_len, sizeof(long long), cudaMemcpyDeviceToDevice,
+                              c->stream));
+  return NW_OK;
+}
+
+nw_status nw_batch_ops_offsets(const int64_t* h_offs, int32_t nseq, const int32_t* h_pairs,
+                               int64_t npairs, int64_t* ops_off) {
+  if (!h_offs || !ops_off || nseq < 0 || npairs < 0) return NW_E_INVAL;
+  long long acc = 0;
+  ops_off[0] = 0;
+  if (h_pairs) {
+    for (long long k = 0; k < npairs; ++k) {
+      const int p = h_pairs[2 * k], q = h_pairs[2 * k + 1];
+      if (p < 0 || p >= nseq || q < 0 || q >= nseq) return NW_E_INVAL;
+      acc += (h_offs[p + 1] - h_offs[p]) + (h_offs[q + 1] - h_offs[q]);
+      ops_off[k + 1] = acc;
+    }
+  } else {
+    long long k = 0;
+    if (npairs != (long long)nseq * (nseq - 1) / 2) return NW_E_INVAL;
+    for (int p = 0; p < nseq; ++p)
+      for (int q = p + 1; q < nseq; ++q) {
+        acc += (h_offs[p + 1] - h_offs[p]) + (h_offs[q + 1] - h_offs[q]);
+        ops_off[++k] = acc;
+      }
+  }
+  return NW_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Shared body of the batch entry points. All pointers device; h_offs/h_pairs host.
+nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool already_coded,
+                     const long long* d_offs, const long long* h_offs, int nseq, const int* d_pairs,
+                     const int* h_pairs, long long npairs, const nw_scoring* sc, uint32_t flags,
+                     int* d_scores, const long long* d_ops_off, uint8_t* d_ops, int* d_ops_len) {
+  constexpr int R = 32 * KR_BATCH;
+  const bool tbk = (flags & NW_TRACEBACK) != 0;
+  const long long total = h_offs[nseq];
+  long long maxlen = 0;
+  for (int k = 0; k < nseq; ++k) maxlen = std::max<long long>(maxlen, h_offs[k + 1] - h_offs[k]);
+  nw_status st = check_bounds(c, sc, maxlen, maxlen);
+  if (st) return st;
+  st = init_small(c, 4);
+  if (st) return st;
+  // codes buffer: PAD | codes | R + PAD
+  const long long lc = PAD + total + R + PAD;
+  st = grow(c, c->d_codes, c->codes_cap, (size_t)lc);
+  if (st) return st;
+  CUDA_TRY(c, cudaMemsetAsync(c->d_codes, 0, (size_t)lc, c->stream));
+  uint8_t* codes = c->d_codes + PAD;
+  (void)already_coded;
+  launch_encode(c, d_codes_raw_or_codes, total, codes, 0);
+  // order: implicit all-pairs -> perm of sequences by length (descending);
+  // explicit pairs -> LPT order by m*n (descending), bucketed.
+  std::vector<int> aux;
+  if (!h_pairs) {
+    aux.resize(nseq);
+    for (int k = 0; k < nseq; ++k) aux[k] = k;
+    std::stable_sort(aux.begin(), aux.end(), [&](int x, int y) {
+      return (h_offs[x + 1] - h_offs[x]) > (h_offs[y + 1] - h_offs[y]);
+    });
+  } else {
+    aux.resize(npairs);
+    for (long long k = 0; k < npairs; ++k) aux[k] = (int)k;
+    auto cost = [&](int k) {
+      const int p = h_pairs[2 * k], q = h_pairs[2 * k + 1];
+      return (h_offs[p + 1] - h_offs[p]) * (h_offs[q + 1] - h_offs[q]);
+    };
+    std::stable_sort(aux.begin(), aux.end(), [&](int x, int y) { return cost(x) > cost(y); });
+  }
+  st = grow(c, c->d_aux, c->aux_cap, sizeof(int) * aux.size() + 16);
+  if (st) return st;
+  if (!aux.empty())
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_aux, aux.data(), sizeof(int) * aux.size(),
+                                cudaMemcpyHostToDevice, c->stream));
+  // per-warp scratch
+  const int warps_per_cta = 4;
+  const bool profreg = sc->K <= 4;
+  const size_t smem = profreg ? 0 : (size_t)warps_per_cta * sc->K * R;
+  int ctas_per_sm = 4;
+  const long long nwarps = (long long)c->sm_count * ctas_per_sm * warps_per_cta;
+  const long long bstride = maxlen + 1 + 64;
+  const long long nblk = (maxlen + 62) / 32;
+  const long long wpl = nblk * (32 / (16 / KR_BATCH));
+  const long long dstride = tbk ? ((maxlen + R - 1) / R) * wpl * 32 : 0;
+  const size_t bytes_bnd = sizeof(int) * (size_t)(nwarps * 2 * bstride);
+  const size_t bytes_hm = sizeof(int) * (size_t)nwarps;
+  const size_t bytes_dirs = sizeof(uint32_t) * (size_t)(nwarps * dstride);
+  st = grow(c, c->d_scratch, c->scratch_cap, bytes_bnd + bytes_hm + bytes_dirs + 256);
+  if (st) return st;
+  BatchArgs B;
+  B.codes = codes;
+  B.offs = d_offs;
+  B.nseq = nseq;
+  B.pairs = d_pairs;
+  B.order = d_pairs ? static_cast<const int*>(c->d_aux) : nullptr;
+  B.perm = d_pairs ? nullptr : static_cast<const int*>(c->d_aux);
+  B.npairs = npairs;
+  B.prof = c->d_prof;
+  B.K = sc->K;
+  B.g = sc->gap;
+  B.ticket = c->d_ints;
+  B.err = c->d_ints + 1;
+  B.scores = d_scores;
+  char* base = static_cast<char*>(c->d_scratch);
+  B.wbnd = reinterpret_cast<int*>(base);
+  B.bstride = bstride;
+  B.whm = reinterpret_cast<int*>(base + bytes_bnd);
+  B.wdirs = tbk ? reinterpret_cast<uint32_t*>(base + ((bytes_bnd + bytes_hm + 255) & ~size_t(255)))
+                : nullptr;
+  B.dstride = dstride;
+  B.ops_off = d_ops_off;
+  B.ops = d_ops;
+  B.ops_len = d_ops_len;
+  B.X = sc->tie[0];
+  B.Y = sc->tie[1];
+  B.Z = sc->tie[2];
+  if (tbk && bytes_bnd + bytes_hm + 256 + bytes_dirs > c->scratch_cap)
+    return fail(c, NW_E_NOMEM, "batch scratch");
+  const int grid = (int)(nwarps / warps_per_cta);
+  const int pi = tbk ? pi_code(sc->tie) : 123;
+  bool ok;
+  {
+    KernelTimer kt(c, 0);
+    ok = dispatch_batch(tbk, pi, profreg, B, grid, smem, c->stream);
+  }
+  if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
+  LAUNCHED(c);
+  CUDA_TRY(c, cudaGetLastError());
+  return NW_OK;
+}
+
+nw_status batch_check(nw_ctx* c, const long long* h_offs, int nseq, const int* h_pairs,
+                      long long npairs, const nw_scoring* sc, uint32_t flags) {
+  nw_status st = check_scoring(c, sc);
+  if (st) return st;
+  if (nseq < 0 || npairs < 0 || !h_offs) return fail(c, NW_E_INVAL, "bad batch sizes");
+  if (flags & ~1u) return fail(c, NW_E_INVAL, "unknown flags 0x%x", flags);
+  if (h_offs[0] != 0) return fail(c, NW_E_INVAL, "offs[0] must be 0");
+  for (int k = 0; k < nseq; ++k)
+    if (h_offs[k + 1] < h_offs[k]) return fail(c, NW_E_INVAL, "offs not non-decreasing");
+  if (!h_pairs) {
+    if (npairs != (long long)nseq * (nseq - 1) / 2)
+      return fail(c, NW_E_INVAL, "pairs=NULL requires npairs = nseq*(nseq-1)/2");
+  } else {
+    for (long long k = 0; k < 2 * npairs; ++k)
+      if (h_pairs[k] < 0 || h_pairs[k] >= nseq) return fail(c, NW_E_INVAL, "pair index out of range");
+  }
+  if (npairs > (1ll << 31) - 2) return fail(c, NW_E_OVERFLOW, "too many pairs");
+  return NW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+nw_status nw_align_batch(nw_ctx* c, const uint8_t* seqs, const int64_t* offs, int32_t nseq,
+                         const int32_t* pairs, int64_t npairs, const nw_scoring* sc,
+                         uint32_t flags, int32_t* scores, int64_t* ops_off, uint8_t* ops,
+                         int32_t* ops_len) {
+  if (!c) return NW_E_INVAL;
+  const long long* h_offs = reinterpret_cast<const long long*>(offs);
+  nw_status st = batch_check(c, h_offs, nseq, pairs, npairs, sc, flags);
+  if (st) return st;
+  const bool tbk = flags & NW_TRACEBACK;
+  if (!scores || (h_offs[nseq] > 0 && !seqs) || (tbk && (!ops_off || !ops || !ops_len)))
+    return fail(c, NW_E_INVAL, "NULL argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  st = upload_tables(c, sc);
+  if (st) return st;
+  if (tbk) {
+    st = nw_batch_ops_offsets(offs, nseq, pairs, npairs, ops_off);
+    if (st) return fail(c, st, "ops offsets");
+  }
+  if (npairs == 0) return NW_OK;
+  const long long total = h_offs[nseq];
+  // device staging: raw residues, offs, pairs, scores, (ops_off, ops, ops_len)
+  const size_t b_raw = (size_t)total + 16, b_offs = sizeof(long long) * (nseq + 1),
+               b_pairs = pairs ? sizeof(int) * 2 * npairs : 0, b_sc = sizeof(int) * npairs,
+               b_oo = tbk ? sizeof(long long) * (npairs + 1) : 0,
+               b_ops = tbk ? (size_t)ops_off[npairs] + 16 : 0, b_ol = tbk ? sizeof(int) * npairs : 0;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t need = al(b_raw) + al(b_offs) + al(b_pairs) + al(b_sc) + al(b_oo) + al(b_ops) + al(b_ol);
+  char* d = nullptr;
+  CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&d), need, c->stream));
+  char* p = d;
+  uint8_t* d_raw = reinterpret_cast<uint8_t*>(p); p += al(b_raw);
+  long long* d_offs = reinterpret_cast<long long*>(p); p += al(b_offs);
+  int* d_pairs = pairs ? reinterpret_cast<int*>(p) : nullptr; p += al(b_pairs);
+  int* d_scores = reinterpret_cast<int*>(p); p += al(b_sc);
+  long long* d_oo = tbk ? reinterpret_cast<long long*>(p) : nullptr; p += al(b_oo);
+  uint8_t* d_ops = tbk ? reinterpret_cast<uint8_t*>(p) : nullptr; p += al(b_ops);
+  int* d_ol = tbk ? reinterpret_cast<int*>(p) : nullptr;
+  if (total) CUDA_TRY(c, cudaMemcpyAsync(d_raw, seqs, (size_t)total, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(d_offs, offs, b_offs, cudaMemcpyHostToDevice, c->stream));
+  if (pairs) CUDA_TRY(c, cudaMemcpyAsync(d_pairs, pairs, b_pairs, cudaMemcpyHostToDevice, c->stream));
+  if (tbk) CUDA_TRY(c, cudaMemcpyAsync(d_oo, ops_off, b_oo, cudaMemcpyHostToDevice, c->stream));
+  st = batch_core(c, d_raw, false, d_offs, h_offs, nseq, d_pairs, pairs, npairs, sc, flags, d_scores,
+                  d_oo, d_ops, d_ol);
+  if (st) { cudaFreeAsync(d, c->stream); return st; }
+  CUDA_TRY(c, cudaMemcpyAsync(scores, d_scores, b_sc, cudaMemcpyDeviceToHost, c->stream));
+  if (tbk) {
+    CUDA_TRY(c, cudaMemcpyAsync(ops, d_ops, (size_t)ops_off[npairs], cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(ops_len, d_ol, b_ol, cudaMemcpyDeviceToHost, c->stream));
+  }
+  cudaFreeAsync(d, c->stream);
+  return check_deferred(c);
+}
+
+nw_status nw_align_batch_dev(nw_ctx* c, const uint8_t* d_seqs, const int64_t* d_offs,
+                             const int64_t* h_offs, int32_t nseq, const int32_t* d_pairs,
+                             const int32_t* h_pairs, int64_t npairs, const nw_scoring* sc,
+                             uint32_t flags, int32_t* d_scores, const int64_t* d_ops_off,
+                             uint8_t* d_ops, int32_t* d_ops_len) {
+  if (!c) return NW_E_INVAL;
+  const long long* ho = reinterpret_cast<const long long*>(h_offs);
+  nw_status st = batch_check(c, ho, nseq, h_pairs, npairs, sc, flags);
+  if (st) return st;
+  const bool tbk = flags & NW_TRACEBACK;
+  if (!d_scores || !d_offs || (ho[nseq] > 0 && !d_seqs) || (d_pairs && !h_pairs) ||
+      (!d_pairs && h_pairs) || (tbk && (!d_ops_off || !d_ops || !d_ops_len)))
+    return fail(c, NW_E_INVAL, "NULL argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  st = upload_tables(c, sc);
+  if (st) return st;
+  if (npairs == 0) return NW_OK;
+  return batch_core(c, d_seqs, false, reinterpret_cast<const long long*>(d_offs), ho, nseq, d_pairs,
+                    h_pairs, npairs, sc, flags, d_scores, reinterpret_cast<const long long*>(d_ops_off),
+                    d_ops, d_ops_len);
+}
+
+}  // extern "C"

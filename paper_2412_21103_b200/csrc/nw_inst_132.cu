@@ -1,0 +1,5 @@
+// Kernel instantiations for tie order pi = 132 (P:90 codes, highest priority first).
+#include "nw_launch.cuh"
+namespace nwk {
+NW_DEFINE_DIRS_LAUNCHERS(132)
+}  // namespace nwk

@@ -1,0 +1,47 @@
+// nw_launch.cuh -- host launchers for the templated kernels, split across
+// translation units (one per tie order) so the library compiles in parallel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "nw_kernels.cuh"
+
+namespace nwk {
+
+constexpr int KR_PAIR = 8;   // rows per lane, single-pair kernels
+constexpr int KR_BATCH = 8;  // rows per lane, batch kernel
+
+// DIRS = true launchers, one instantiation per tie order PI (nw_inst_<PI>.cu)
+template <int PI>
+void launch_fill_dirs(const FillArgs& A, bool profreg, int grid, size_t smem, cudaStream_t st);
+template <int PI>
+void launch_batch_dirs(const BatchArgs& B, bool profreg, int grid, size_t smem, cudaStream_t st);
+
+template <int KR, bool DIRS, bool PROFREG, int PI>
+void launch_fill_t(const FillArgs& A, int grid, size_t smem, cudaStream_t st) {
+  auto k = k_fill_pair<KR, DIRS, PROFREG, PI>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<grid, 32, smem, st>>>(A);
+}
+
+template <int KR, bool DIRS, bool PROFREG, int PI>
+void launch_batch_t(const BatchArgs& B, int grid, size_t smem, cudaStream_t st) {
+  auto k = k_batch<KR, DIRS, PROFREG, PI>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<grid, 128, smem, st>>>(B);
+}
+
+#define NW_DEFINE_DIRS_LAUNCHERS(PI)                                                          \
+  template <>                                                                                 \
+  void launch_fill_dirs<PI>(const FillArgs& A, bool profreg, int grid, size_t smem,           \
+                            cudaStream_t st) {                                                \
+    if (profreg) launch_fill_t<KR_PAIR, true, true, PI>(A, grid, smem, st);                   \
+    else launch_fill_t<KR_PAIR, true, false, PI>(A, grid, smem, st);                          \
+  }                                                                                           \
+  template <>                                                                                 \
+  void launch_batch_dirs<PI>(const BatchArgs& B, bool profreg, int grid, size_t smem,         \
+                             cudaStream_t st) {                                               \
+    if (profreg) launch_batch_t<KR_BATCH, true, true, PI>(B, grid, smem, st);                 \
+    else launch_batch_t<KR_BATCH, true, false, PI>(B, grid, smem, st);                        \
+  }
+
+}  // namespace nwk

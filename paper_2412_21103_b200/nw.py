@@ -1,0 +1,294 @@
+"""Thin ctypes binding of include/nw.h (argument marshalling only).
+
+Every step of the hot path runs in libnw_b200.so's CUDA kernels; this module
+converts Python/numpy/torch arguments to the C ABI and back. If the shared
+library is missing or has no CUDA device, calls raise -- there is no CPU path.
+
+Names follow the C ABI: nw_score_only, nw_align_pair, nw_traceback,
+nw_align_batch (+ the _dev variants on device pointers / torch CUDA tensors).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnw_b200.so")
+
+NW_OK, NW_E_INVAL, NW_E_ALPHABET, NW_E_OVERFLOW, NW_E_NOMEM, NW_E_CUDA, NW_E_TRUNC, \
+    NW_E_STATE, NW_E_DEADLOCK, NW_E_COMM = range(10)
+NW_DIAG, NW_UP, NW_LEFT = 1, 2, 3
+NW_SCORE_ONLY, NW_TRACEBACK = 0, 1
+
+
+class NWError(RuntimeError):
+    def __init__(self, status: int, message: str, bad_pos: int = -1):
+        super().__init__(f"[{status}] {message}")
+        self.status = status
+        self.bad_pos = bad_pos
+
+
+class _Scoring(ctypes.Structure):
+    _fields_ = [("match", ctypes.c_int32), ("mismatch", ctypes.c_int32), ("gap", ctypes.c_int32),
+                ("subst", ctypes.POINTER(ctypes.c_int32)), ("alphabet", ctypes.c_char_p),
+                ("K", ctypes.c_int32), ("tie", ctypes.c_uint8 * 3)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libnw_b200.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32
+    P = ctypes.POINTER
+    sig = {
+        "nw_ctx_create": ([ctypes.c_int, vp, P(vp)], ctypes.c_int),
+        "nw_ctx_destroy": ([vp], None),
+        "nw_strerror": ([ctypes.c_int], ctypes.c_char_p),
+        "nw_last_error": ([vp], ctypes.c_char_p),
+        "nw_last_bad_pos": ([vp], i64),
+        "nw_ctx_sync": ([vp], ctypes.c_int),
+        "nw_ctx_launches": ([vp], i64),
+        "nw_ctx_set_timing": ([vp, ctypes.c_int], ctypes.c_int),
+        "nw_ctx_kernel_time": ([vp, ctypes.c_int, P(ctypes.c_double), P(i64)], ctypes.c_int),
+        "nw_score_only": ([vp, vp, i64, vp, i64, P(_Scoring), P(i64)], ctypes.c_int),
+        "nw_score_only_dev": ([vp, vp, i64, vp, i64, P(_Scoring), vp], ctypes.c_int),
+        "nw_align_pair": ([vp, vp, i64, vp, i64, P(_Scoring), P(i64), P(vp)], ctypes.c_int),
+        "nw_align_pair_dev": ([vp, vp, i64, vp, i64, P(_Scoring), vp, P(vp)], ctypes.c_int),
+        "nw_traceback": ([vp, vp, vp, i64, P(i64)], ctypes.c_int),
+        "nw_traceback_dev": ([vp, vp, vp, i64, vp], ctypes.c_int),
+        "nw_tb_free": ([vp], None),
+        "nw_align_batch": ([vp, vp, vp, i32, vp, i64, P(_Scoring), u32, vp, vp, vp, vp],
+                           ctypes.c_int),
+        "nw_align_batch_dev": ([vp, vp, vp, vp, i32, vp, vp, i64, P(_Scoring), u32, vp, vp, vp,
+                                vp], ctypes.c_int),
+        "nw_batch_ops_offsets": ([vp, i32, vp, i64, vp], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+EXPORTED = ("nw_ctx_create", "nw_ctx_destroy", "nw_strerror", "nw_last_error", "nw_last_bad_pos",
+            "nw_ctx_sync", "nw_ctx_launches", "nw_ctx_set_timing", "nw_ctx_kernel_time", "nw_score_only", "nw_score_only_dev",
+            "nw_align_pair", "nw_align_pair_dev", "nw_traceback", "nw_traceback_dev",
+            "nw_tb_free", "nw_align_batch", "nw_align_batch_dev", "nw_batch_ops_offsets")
+
+
+def _scoring(sc) -> tuple[_Scoring, object]:
+    """nw_scoring from any object with match/mismatch/gap/alphabet/subst/tie."""
+    s = _Scoring()
+    s.match, s.mismatch, s.gap = int(sc.match), int(sc.mismatch), int(sc.gap)
+    keep = None
+    if getattr(sc, "subst", None) is not None:
+        keep = np.ascontiguousarray(np.asarray(sc.subst, dtype=np.int32))
+        s.subst = keep.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    alpha = sc.alphabet.encode() if isinstance(sc.alphabet, str) else bytes(sc.alphabet)
+    s.alphabet = alpha
+    s.K = len(alpha)
+    tie = tuple(getattr(sc, "tie", (1, 2, 3)))
+    s.tie = (ctypes.c_uint8 * 3)(*tie)
+    return s, (keep, alpha)
+
+
+def _host_bytes(x) -> np.ndarray:
+    if isinstance(x, (bytes, bytearray, memoryview)):
+        return np.frombuffer(bytes(x), dtype=np.uint8)
+    return np.ascontiguousarray(x, dtype=np.uint8)
+
+
+def _ptr(x) -> int | None:
+    """Address of a numpy array or torch tensor (host or device)."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr() if x.numel() else None
+    return x.ctypes.data if x.size else None
+
+
+class Context:
+    """nw_ctx on one CUDA device; stream = a cudaStream_t handle (int) or None."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        self._h = ctypes.c_void_p()
+        st = lib().nw_ctx_create(device, stream, ctypes.byref(self._h))
+        if st != NW_OK:
+            raise NWError(st, f"nw_ctx_create(device={device}): {lib().nw_strerror(st).decode()}")
+        self.device = device
+
+    def _check(self, st: int):
+        if st != NW_OK:
+            msg = lib().nw_last_error(self._h).decode(errors="replace")
+            bad = lib().nw_last_bad_pos(self._h) if st == NW_E_ALPHABET else -1
+            raise NWError(st, msg, bad)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def launches(self) -> int:
+        return int(lib().nw_ctx_launches(self._h))
+
+    def set_timing(self, enable: bool = True):
+        self._check(lib().nw_ctx_set_timing(self._h, int(enable)))
+
+    def kernel_time(self, kernel_class: int) -> tuple[float, int]:
+        """(summed event ms, launches) of class 0 = fill, 1 = traceback; resets."""
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        self._check(lib().nw_ctx_kernel_time(self._h, kernel_class, ctypes.byref(ms),
+                                             ctypes.byref(n)))
+        return ms.value, n.value
+
+    def sync(self):
+        self._check(lib().nw_ctx_sync(self._h))
+
+    def close(self):
+        if self._h:
+            lib().nw_ctx_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+class Traceback:
+    """nw_tb handle: 2-bit packed directions resident on the device."""
+
+    def __init__(self, ctx: Context, h: ctypes.c_void_p, m: int, n: int):
+        self.ctx, self._h, self.m, self.n = ctx, h, m, n
+
+    def free(self):
+        if self._h:
+            lib().nw_tb_free(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def nw_score_only(ctx: Context, a, b, sc) -> int:
+    a, b = _host_bytes(a), _host_bytes(b)
+    s, keep = _scoring(sc)
+    out = ctypes.c_int64()
+    ctx._check(lib().nw_score_only(ctx.handle, _ptr(a), len(a), _ptr(b), len(b), ctypes.byref(s),
+                                   ctypes.byref(out)))
+    return out.value
+
+
+def nw_score_only_dev(ctx: Context, d_a, d_b, sc, d_score) -> None:
+    """d_a, d_b: uint8 CUDA tensors; d_score: int64 CUDA tensor (1 element). Async."""
+    s, keep = _scoring(sc)
+    ctx._check(lib().nw_score_only_dev(ctx.handle, _ptr(d_a), d_a.numel(), _ptr(d_b), d_b.numel(),
+                                       ctypes.byref(s), _ptr(d_score)))
+
+
+def nw_align_pair(ctx: Context, a, b, sc) -> tuple[int, Traceback]:
+    a, b = _host_bytes(a), _host_bytes(b)
+    s, keep = _scoring(sc)
+    out = ctypes.c_int64()
+    tb = ctypes.c_void_p()
+    ctx._check(lib().nw_align_pair(ctx.handle, _ptr(a), len(a), _ptr(b), len(b), ctypes.byref(s),
+                                   ctypes.byref(out), ctypes.byref(tb)))
+    return out.value, Traceback(ctx, tb, len(a), len(b))
+
+
+def nw_align_pair_dev(ctx: Context, d_a, d_b, sc, d_score) -> Traceback:
+    s, keep = _scoring(sc)
+    tb = ctypes.c_void_p()
+    ctx._check(lib().nw_align_pair_dev(ctx.handle, _ptr(d_a), d_a.numel(), _ptr(d_b), d_b.numel(),
+                                       ctypes.byref(s), _ptr(d_score), ctypes.byref(tb)))
+    return Traceback(ctx, tb, d_a.numel(), d_b.numel())
+
+
+def nw_traceback(ctx: Context, tb: Traceback) -> np.ndarray:
+    """Forward-order P:90 codes of the path (uint8 array)."""
+    cap = tb.m + tb.n
+    ops = np.empty(max(cap, 1), dtype=np.uint8)
+    ln = ctypes.c_int64()
+    ctx._check(lib().nw_traceback(ctx.handle, tb._h, ops.ctypes.data, cap, ctypes.byref(ln)))
+    return ops[:ln.value].copy()
+
+
+def nw_traceback_dev(ctx: Context, tb: Traceback, d_ops, d_len) -> None:
+    """d_ops: uint8 CUDA tensor with >= m+n elements; d_len: int64 CUDA tensor. Async."""
+    ctx._check(lib().nw_traceback_dev(ctx.handle, tb._h, _ptr(d_ops), d_ops.numel(), _ptr(d_len)))
+
+
+def nw_batch_ops_offsets(offs: np.ndarray, pairs: np.ndarray | None) -> np.ndarray:
+    offs = np.ascontiguousarray(offs, dtype=np.int64)
+    nseq = len(offs) - 1
+    if pairs is None:
+        npairs = nseq * (nseq - 1) // 2
+    else:
+        pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+        npairs = len(pairs)
+    out = np.empty(npairs + 1, dtype=np.int64)
+    st = lib().nw_batch_ops_offsets(offs.ctypes.data, nseq, _ptr(pairs), npairs, out.ctypes.data)
+    if st != NW_OK:
+        raise NWError(st, "nw_batch_ops_offsets")
+    return out
+
+
+def nw_align_batch(ctx: Context, seqs, offs, pairs, sc, flags: int = NW_SCORE_ONLY):
+    """Host batch. Returns scores (int32[npairs]) or (scores, list of op arrays)."""
+    seqs = _host_bytes(seqs)
+    offs = np.ascontiguousarray(offs, dtype=np.int64)
+    nseq = len(offs) - 1
+    if pairs is None:
+        npairs = nseq * (nseq - 1) // 2
+    else:
+        pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+        npairs = len(pairs)
+    s, keep = _scoring(sc)
+    scores = np.empty(npairs, dtype=np.int32)
+    tbk = bool(flags & NW_TRACEBACK)
+    ops_off = np.empty(npairs + 1, dtype=np.int64) if tbk else None
+    if tbk:
+        tot = int(nw_batch_ops_offsets(offs, pairs)[-1])
+        ops = np.empty(max(tot, 1), dtype=np.uint8)
+        ops_len = np.empty(max(npairs, 1), dtype=np.int32)
+    else:
+        ops = ops_len = None
+    ctx._check(lib().nw_align_batch(ctx.handle, _ptr(seqs), offs.ctypes.data, nseq, _ptr(pairs),
+                                    npairs, ctypes.byref(s), flags, _ptr(scores), _ptr(ops_off),
+                                    _ptr(ops), _ptr(ops_len)))
+    if not tbk:
+        return scores
+    paths = [ops[ops_off[k]:ops_off[k] + ops_len[k]].copy() for k in range(npairs)]
+    return scores, paths
+
+
+def nw_align_batch_dev(ctx: Context, d_seqs, d_offs, h_offs, d_pairs, h_pairs, npairs: int, sc,
+                       flags: int, d_scores, d_ops_off=None, d_ops=None, d_ops_len=None) -> None:
+    """Device batch (torch CUDA tensors; h_offs/h_pairs numpy host copies). Async."""
+    h_offs = np.ascontiguousarray(h_offs, dtype=np.int64)
+    if h_pairs is not None:
+        h_pairs = np.ascontiguousarray(h_pairs, dtype=np.int32)
+    s, keep = _scoring(sc)
+    ctx._check(lib().nw_align_batch_dev(ctx.handle, _ptr(d_seqs), _ptr(d_offs), h_offs.ctypes.data,
+                                        len(h_offs) - 1, _ptr(d_pairs), _ptr(h_pairs), npairs,
+                                        ctypes.byref(s), flags, _ptr(d_scores), _ptr(d_ops_off),
+                                        _ptr(d_ops), _ptr(d_ops_len)))

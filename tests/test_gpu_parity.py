@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact.
+
+Scores and traceback op strings must be identical (north_star: "bit-exact
+against this oracle for both scores and traceback strings"); all arithmetic is
+integer, so the tolerance is zero. Inputs come from nwgen (seeded), sized to
+span several strips (R = 256 rows) and ragged tails.
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+import pytest
+
+import nwgen
+import oracle
+import paper_2412_21103_b200 as nwb
+
+pytestmark = pytest.mark.gpu
+
+ORDERS = [(1, 2, 3), (1, 3, 2), (2, 1, 3), (2, 3, 1), (3, 1, 2), (3, 2, 1)]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = nwb.Context(0)
+    yield c
+    c.close()
+
+
+def _pair(seed, m, n, alphabet=nwgen.DNA):
+    return nwgen.random_pair(seed, m, n, alphabet)
+
+
+def check_pair(ctx, a, b, sc, with_ops=True):
+    want_score, want_ops = oracle.align(a, b, sc)
+    got_score, tb = nwb.nw_align_pair(ctx, a, b, sc)
+    assert got_score == want_score, (len(a), len(b), sc.tie)
+    if with_ops:
+        got_ops = nwb.nw_traceback(ctx, tb)
+        assert got_ops.tolist() == want_ops.tolist(), (len(a), len(b), sc.tie)
+    tb.free()
+    assert nwb.nw_score_only(ctx, a, b, sc) == want_score
+
+
+SIZES = [1, 2, 31, 32, 33, 255, 256, 257, 513, 1000]
+
+
+@pytest.mark.parametrize("m,n", [(m, n) for m, n in itertools.product(SIZES, SIZES)
+                                 if (m * 7 + n) % 3 == 0 or m == n])
+def test_pair_dna_sizes(ctx, m, n):
+    a, b = _pair(1000 * m + n, m, n)
+    check_pair(ctx, a, b, nwgen.PAPER_DNA)
+
+
+@pytest.mark.parametrize("tie", ORDERS)
+def test_pair_tie_orders(ctx, tie):
+    for k, (m, n) in enumerate([(300, 277), (64, 700), (1200, 90), (7, 7)]):
+        a, b = _pair(77 + k, m, n)
+        check_pair(ctx, a, b, nwgen.Scoring(tie=tie))
+    # low-complexity inputs make ties frequent
+    rng = np.random.Generator(np.random.PCG64(3))
+    a = nwgen.random_seq(rng, 600, "AC")
+    b = nwgen.random_seq(rng, 555, "AC")
+    check_pair(ctx, a, b, nwgen.Scoring(tie=tie))
+
+
+@pytest.mark.parametrize("tie", [(1, 2, 3), (2, 3, 1)])
+def test_pair_protein_blosum62(ctx, tie):
+    sc = nwgen.Scoring(match=0, mismatch=0, gap=-5, alphabet=nwgen.PROTEIN,
+                       subst=nwgen.BLOSUM62, tie=tie)
+    for k, (m, n) in enumerate([(100, 1000), (999, 301), (257, 256), (5, 2)]):
+        a, b = _pair(500 + k, m, n, nwgen.PROTEIN)
+        check_pair(ctx, a, b, sc)
+
+
+def test_pair_other_scorings(ctx):
+    for k, (ma, mi, g) in enumerate([(2, -3, -2), (5, -4, -10), (1, 0, -1), (0, -1, -1)]):
+        a, b = _pair(900 + k, 400, 380)
+        check_pair(ctx, a, b, nwgen.Scoring(match=ma, mismatch=mi, gap=g))
+
+
+def test_empty_and_degenerate(ctx):
+    sc = nwgen.PAPER_DNA
+    for a, b in [(b"", b""), (b"", b"ACG"), (b"ACGT", b""), (b"A", b"A"), (b"A", b"C")]:
+        check_pair(ctx, a, b, sc)
+    a = b"ACGT" * 200
+    check_pair(ctx, a, a, sc)                      # identical: all diagonal
+    check_pair(ctx, b"A" * 700, b"C" * 300, sc)    # disjoint alphabets
+
+
+def test_golden_worked_grid(ctx):
+    sc = nwgen.Scoring(alphabet="ACGTU")
+    for tie in ORDERS:
+        check_pair(ctx, b"GATTACA", b"GCATGCU", nwgen.Scoring(alphabet="ACGTU", tie=tie))
+    assert nwb.nw_score_only(ctx, b"GATTACA", b"GCATGCU", sc) == 0
+
+
+def test_errors(ctx):
+    sc = nwgen.PAPER_DNA
+    with pytest.raises(nwb.NWError) as e:
+        nwb.nw_align_pair(ctx, b"ACGTACGT", b"ACGNAC", sc)
+    assert e.value.status == 2 and e.value.bad_pos == 8 + 3
+    with pytest.raises(nwb.NWError) as e:
+        nwb.nw_score_only(ctx, b"AC", b"AC", nwgen.Scoring(gap=1))
+    assert e.value.status == 1
+    with pytest.raises(nwb.NWError) as e:
+        nwb.nw_score_only(ctx, b"AC", b"AC", nwgen.Scoring(tie=(1, 1, 2)))
+    assert e.value.status == 1
+    # traceback handle from another context
+    other = nwb.Context(0)
+    _, tb = nwb.nw_align_pair(other, b"ACGT", b"AGT", sc)
+    with pytest.raises(nwb.NWError) as e:
+        nwb.nw_traceback(ctx, tb)
+    assert e.value.status == 7
+    tb.free()
+    other.close()
+
+
+def test_c1_config(ctx):
+    a, b = nwgen.config_c1()
+    check_pair(ctx, a, b, nwgen.PAPER_DNA)
+
+
+def test_c2_config_full(ctx):
+    """BASELINE configs[1] at full size: 20,000 x 20,000, score + traceback."""
+    a, b = nwgen.config_c2()
+    check_pair(ctx, a, b, nwgen.PAPER_DNA)
+
+
+def test_c2_closed_forms(ctx):
+    n = 20000
+    a = nwgen.config_c2()[0]
+    s, tb = nwb.nw_align_pair(ctx, a, a, nwgen.PAPER_DNA)
+    assert s == n and (nwb.nw_traceback(ctx, tb) == 1).all()
+    s, tb = nwb.nw_align_pair(ctx, b"A" * n, b"C" * (n - 1), nwgen.PAPER_DNA)
+    assert s == -n
+    ops = nwb.nw_traceback(ctx, tb)
+    assert ops.tolist() == [2] + [1] * (n - 1)
+
+
+def test_dev_variants_match_host(ctx):
+    import torch
+    a, b = _pair(4242, 3000, 2500)
+    sc = nwgen.PAPER_DNA
+    want_score, want_ops = oracle.align(a, b, sc)
+    da = torch.frombuffer(bytearray(a), dtype=torch.uint8).cuda()
+    db = torch.frombuffer(bytearray(b), dtype=torch.uint8).cuda()
+    d_score = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tb = nwb.nw_align_pair_dev(ctx, da, db, sc, d_score)
+    d_ops = torch.zeros(len(a) + len(b), dtype=torch.uint8, device="cuda")
+    d_len = torch.zeros(1, dtype=torch.int64, device="cuda")
+    nwb.nw_traceback_dev(ctx, tb, d_ops, d_len)
+    ctx.sync()
+    assert int(d_score.item()) == want_score
+    L = int(d_len.item())
+    assert d_ops[:L].cpu().numpy().tolist() == want_ops.tolist()
+    tb.free()
+    d2 = torch.zeros(1, dtype=torch.int64, device="cuda")
+    nwb.nw_score_only_dev(ctx, da, db, sc, d2)
+    ctx.sync()
+    assert int(d2.item()) == want_score
+
+
+# ---------------------------------------------------------------- batch
+
+def test_batch_all_pairs_dna(ctx):
+    ss = nwgen.random_set(31, 40, 0, 700)
+    want = oracle.batch_score(ss.residues, ss.offs, nwgen.all_pairs(ss.nseq), nwgen.PAPER_DNA)
+    got = nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, nwgen.PAPER_DNA)
+    assert got.tolist() == want.tolist()
+
+
+def test_batch_explicit_pairs_traceback_protein(ctx):
+    ss = nwgen.random_set(32, 60, 0, 600, nwgen.PROTEIN)
+    rng = np.random.Generator(np.random.PCG64(9))
+    pairs = rng.integers(0, ss.nseq, size=(150, 2)).astype(np.int32)
+    for tie in [(1, 2, 3), (3, 1, 2)]:
+        sc = nwgen.Scoring(match=0, mismatch=0, gap=-5, alphabet=nwgen.PROTEIN,
+                           subst=nwgen.BLOSUM62, tie=tie)
+        scores, paths = nwb.nw_align_batch(ctx, ss.residues, ss.offs, pairs, sc, nwb.NW_TRACEBACK)
+        for k, (p, q) in enumerate(pairs):
+            ws, wops = oracle.align(ss.seq(p), ss.seq(q), sc)
+            assert scores[k] == ws, k
+            assert paths[k].tolist() == wops.tolist(), k
+
+
+def test_batch_traceback_dna_all_pairs(ctx):
+    ss = nwgen.random_set(33, 25, 1, 400)
+    sc = nwgen.PAPER_DNA
+    scores, paths = nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc, nwb.NW_TRACEBACK)
+    for k, (p, q) in enumerate(nwgen.all_pairs(ss.nseq)):
+        ws, wops = oracle.align(ss.seq(p), ss.seq(q), sc)
+        assert scores[k] == ws and paths[k].tolist() == wops.tolist()
+
+
+def test_c3_full_size_sampled(ctx):
+    """configs[2] at full size (2,048 seqs, 2,096,128 pairs), sampled vs oracle."""
+    ss = nwgen.config_c3()
+    got = nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, nwgen.PAPER_DNA)
+    pairs = nwgen.all_pairs(ss.nseq)
+    assert len(got) == len(pairs) == 2096128
+    rng = np.random.Generator(np.random.PCG64(1))
+    idx = np.concatenate([rng.integers(0, len(pairs), 150), [0, len(pairs) - 1]])
+    want = oracle.batch_score(ss.residues, ss.offs, pairs[idx], nwgen.PAPER_DNA)
+    assert got[idx].tolist() == want.tolist()
+    # symmetry of the score matrix: reversed pairs through the explicit path
+    rev = pairs[idx][:, ::-1].copy()
+    got_rev = nwb.nw_align_batch(ctx, ss.residues, ss.offs, rev, nwgen.PAPER_DNA)
+    assert got_rev.tolist() == want.tolist()
+
+
+def test_c4_full_size_sampled(ctx):
+    """configs[3] at full size (100,000 protein pairs, traceback), sampled."""
+    ss = nwgen.config_c4()
+    pairs = nwgen.consecutive_pairs(100_000)
+    sc = nwgen.PROTEIN_BLOSUM62
+    scores, paths = nwb.nw_align_batch(ctx, ss.residues, ss.offs, pairs, sc, nwb.NW_TRACEBACK)
+    rng = np.random.Generator(np.random.PCG64(2))
+    for k in np.concatenate([rng.integers(0, len(pairs), 60), [0, len(pairs) - 1]]):
+        p, q = pairs[k]
+        ws, wops = oracle.align(ss.seq(p), ss.seq(q), sc)
+        assert scores[k] == ws and paths[k].tolist() == wops.tolist(), k
+
+
+# ---------------------------------------------------------------- score-only, large
+
+def test_score_only_prefix_and_closed_forms_c5(ctx):
+    """configs[4] sequences: a 40k x 40k prefix vs the oracle, and the 1M x 1M
+    closed forms (identical -> 1e6; A^m vs C^n -> -1e6; (0,-1,-1) -> -edit distance
+    checked at a smaller size)."""
+    a, b = nwgen.config_c5()
+    pa, pb = a[:40000], b[:40000]
+    assert nwb.nw_score_only(ctx, pa, pb, nwgen.PAPER_DNA) == oracle.score(pa, pb, nwgen.PAPER_DNA)
+    n = 1_000_000
+    assert nwb.nw_score_only(ctx, a, a, nwgen.PAPER_DNA) == n
+    assert nwb.nw_score_only(ctx, b"A" * n, b"C" * n, nwgen.PAPER_DNA) == -n
+    from pins import myers_edit_distance
+    sc = nwgen.Scoring(match=0, mismatch=-1, gap=-1)
+    qa, qb = a[:3000], b[:2900]
+    assert nwb.nw_score_only(ctx, qa, qb, sc) == -myers_edit_distance(qa, qb)
