@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -37,13 +38,13 @@ struct nw_ctx {
   uint8_t* d_lut = nullptr;     // 256
   int8_t* d_prof = nullptr;     // 64*64
   long long* d_bad = nullptr;   // 1 (+ spare)
-  int* d_ints = nullptr;        // small ints: [0] ticket [1] err [2] hm [3..] prog
+  int* d_ints = nullptr;        // small ints: [0] ticket [1] err [2] hm [3] em
   size_t ints_cap = 0;
   uint8_t* d_codes = nullptr;   // encoded inputs
   size_t codes_cap = 0;
   uint8_t* d_raw = nullptr;     // raw residues copied from the host
   size_t raw_cap = 0;
-  int* d_bnd = nullptr;
+  unsigned long long* d_bnd = nullptr;  // 2-slot tagged boundary ring
   size_t bnd_cap = 0;
   uint8_t* d_rev = nullptr;     // reversed traceback
   size_t rev_cap = 0;
@@ -65,9 +66,18 @@ struct nw_ctx {
 
 struct nw_tb {
   nw_ctx* ctx;
-  uint32_t* dirs;
-  long long wpl;
-  int m, n;
+  void* mem;          // one device allocation holding everything below
+  uint16_t* dirs;     // [S][wpl][KR][32] decision-bit halfwords (nw_fill.cuh)
+  long long wpl;      // 8-step groups per strip
+  int* ebnd;          // [S][n+1] exit columns of each strip's bottom row
+  int* cs;            // [S] entry column per strip (traceback)
+  int* seglen;        // [S]
+  long long* segoff;  // [S]
+  int* em;            // E(m, n): exit column of the path's start (written by the fill)
+  uint8_t* seg;       // [S][segstride] reversed per-strip path segments
+  long long segstride;
+  int m, n, S;
+  int kr;             // rows per lane of the fill that wrote `dirs`
   uint8_t tie[3];
 };
 
@@ -209,6 +219,11 @@ nw_status check_bounds(nw_ctx* c, const nw_scoring* sc, long long m, long long n
 
 int pi_code(const uint8_t tie[3]) { return tie[0] * 100 + tie[1] * 10 + tie[2]; }
 
+long long pad16(long long x) { return (x + 15) & ~15ll; }
+
+// Entries per boundary-ring slot (columns 0..n plus the sweep's overhang), 16-byte multiple.
+long long bnd_stride(long long n) { return (n + 1 + 64 + 1) & ~1ll; }
+
 // ---- kernel dispatch: score-only kernels here, one TU per tie order for DIRS ----
 }  // namespace
 namespace nwk {
@@ -216,22 +231,45 @@ NW_DEFINE_DIRS_LAUNCHERS(123)
 }  // namespace nwk
 namespace {
 
-bool dispatch_fill(bool dirs, int pi, bool profreg, const FillArgs& A, int grid, size_t smem,
-                   cudaStream_t st) {
+template <int KR>
+void launch_score(const FillArgs& A, bool profreg, int grid, size_t smem, cudaStream_t st) {
+  if (profreg) launch_fill_t<KR, false, true, 123>(A, grid, smem, st);
+  else launch_fill_t<KR, false, false, 123>(A, grid, smem, st);
+}
+
+bool dispatch_fill(bool dirs, int pi, int kr, bool profreg, const FillArgs& A, int grid,
+                   size_t smem, cudaStream_t st) {
   if (!dirs) {
-    if (profreg) launch_fill_t<KR_PAIR, false, true, 123>(A, grid, smem, st);
-    else launch_fill_t<KR_PAIR, false, false, 123>(A, grid, smem, st);
+    if (kr == 2) launch_score<2>(A, profreg, grid, smem, st);
+    else if (kr == 4) launch_score<4>(A, profreg, grid, smem, st);
+    else launch_score<8>(A, profreg, grid, smem, st);
     return true;
   }
   switch (pi) {
-    case 123: launch_fill_dirs<123>(A, profreg, grid, smem, st); return true;
-    case 132: launch_fill_dirs<132>(A, profreg, grid, smem, st); return true;
-    case 213: launch_fill_dirs<213>(A, profreg, grid, smem, st); return true;
-    case 231: launch_fill_dirs<231>(A, profreg, grid, smem, st); return true;
-    case 312: launch_fill_dirs<312>(A, profreg, grid, smem, st); return true;
-    case 321: launch_fill_dirs<321>(A, profreg, grid, smem, st); return true;
+    case 123: launch_fill_dirs<123>(A, kr, profreg, grid, smem, st); return true;
+    case 132: launch_fill_dirs<132>(A, kr, profreg, grid, smem, st); return true;
+    case 213: launch_fill_dirs<213>(A, kr, profreg, grid, smem, st); return true;
+    case 231: launch_fill_dirs<231>(A, kr, profreg, grid, smem, st); return true;
+    case 312: launch_fill_dirs<312>(A, kr, profreg, grid, smem, st); return true;
+    case 321: launch_fill_dirs<321>(A, kr, profreg, grid, smem, st); return true;
   }
   return false;
+}
+
+// Rows per lane for a single pair: the strip count m/(32 KR)
+// is the number of warps that can work at once; small KR buys parallelism at the
+// cost of a longer lane skew (m/KR steps). NW_KR overrides (2, 4 or 8).
+int choose_kr(long long m, long long n, bool dirs) {
+  const char* env = getenv("NW_KR");
+  if (env) {
+    const int k = atoi(env);
+    if (k == 2 || k == 4 || k == 8) return k;
+  }
+  (void)n;
+  (void)dirs;
+  if (m >= 32 * 8 * 592) return 8;  // enough strips for every SMSP at KR = 8
+  if (m >= 32 * 4 * 300) return 4;
+  return 2;
 }
 
 bool dispatch_batch(bool dirs, int pi, bool profreg, const BatchArgs& B, int grid, size_t smem,
@@ -262,11 +300,13 @@ void launch_encode(nw_ctx* c, const uint8_t* raw, long long len, uint8_t* out, l
   LAUNCHED(c);
 }
 
-nw_status init_small(nw_ctx* c, int nints) {
+nw_status init_small(nw_ctx* c, int nints, ZeroRanges zr = ZeroRanges{{nullptr, nullptr, nullptr, nullptr}, {0, 0, 0, 0}}) {
   nw_status st = grow(c, c->d_ints, c->ints_cap, sizeof(int) * (size_t)nints);
   if (st) return st;
-  int blocks = std::min(1024, (nints + 255) / 256);
-  k_init<<<blocks, 256, 0, c->stream>>>(c->d_ints, nints, c->d_bad);
+  long long work = nints;
+  for (int r = 0; r < 4; ++r) work = std::max(work, zr.bytes[r] / 16);
+  const int blocks = (int)std::min<long long>((long long)c->sm_count * 4, (work + 255) / 256 + 1);
+  k_init<<<blocks, 256, 0, c->stream>>>(c->d_ints, nints, c->d_bad, zr);
   LAUNCHED(c);
   return NW_OK;
 }
@@ -274,7 +314,7 @@ nw_status init_small(nw_ctx* c, int nints) {
 // Device-side core of nw_score_only / nw_align_pair on already-encoded codes.
 // ca, cb: codes with PAD before and >= R + PAD after. Writes H(m,n) to d_score.
 nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb, long long n,
-                    const nw_scoring* sc, long long* d_score, nw_tb* tb);
+                    const nw_scoring* sc, long long* d_score, nw_tb* tb, int kr);
 
 }  // namespace
 
@@ -288,27 +328,25 @@ __global__ void k_finish_score(const int* hm, long long gmn, long long* out, int
 namespace {
 
 nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb, long long n,
-                    const nw_scoring* sc, long long* d_score, nw_tb* tb) {
-  constexpr int R = 32 * KR_PAIR;
+                    const nw_scoring* sc, long long* d_score, nw_tb* tb, int kr) {
+  const int R = 32 * kr;
   const int nstrips = (int)((m + R - 1) / R);
   const bool dirs = tb != nullptr;
   nw_status st = NW_OK;
   int* ticket = c->d_ints;
   int* errf = c->d_ints + 1;
   int* hm = c->d_ints + 2;
-  int* prog = c->d_ints + 3;
+  int* em = c->d_ints + 3;
   const long long gmn = (long long)sc->gap * (m + n);
   if (m > 0 && n > 0) {
-    const long long bstride = n + 1 + 64;
-    st = grow(c, c->d_bnd, c->bnd_cap, sizeof(int) * 2 * (size_t)bstride);
-    if (st) return st;
     FillArgs A;
     A.a = ca; A.b = cb; A.prof = c->d_prof; A.K = sc->K;
     A.m = (int)m; A.n = (int)n; A.nstrips = nstrips; A.nslots = 2;
-    A.bnd = c->d_bnd; A.bstride = bstride; A.prog = prog; A.ticket = ticket;
+    A.bnd = c->d_bnd; A.bstride = bnd_stride(n); A.ticket = ticket;
     A.dirs = dirs ? tb->dirs : nullptr;
     A.wpl = dirs ? tb->wpl : 0;
-    A.hm = hm; A.err = errf;
+    A.ebnd = dirs ? tb->ebnd : nullptr;
+    A.hm = hm; A.em = dirs ? tb->em : em; A.err = errf;
     const bool profreg = sc->K <= 4;
     const size_t smem = profreg ? 0 : (size_t)sc->K * R;
     // persistent grid: one warp per CTA, at most the resident capacity
@@ -318,7 +356,7 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     bool ok;
     {
       KernelTimer kt(c, 0);
-      ok = dispatch_fill(dirs, pi, profreg, A, grid, smem, c->stream);
+      ok = dispatch_fill(dirs, pi, kr, profreg, A, grid, smem, c->stream);
     }
     if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
     LAUNCHED(c);
@@ -344,19 +382,18 @@ nw_status check_deferred(nw_ctx* c) {
   return NW_OK;
 }
 
-// Stage host residues into device codes (PAD | a | pad to R + PAD).
+
+// Stage residues into device codes (PAD | a | pad to R + PAD), after k_init
+// has zeroed the code buffer and the tagged boundary ring (pair_entry).
 nw_status stage_pair(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b, long long n,
                      bool host, uint8_t** ca, uint8_t** cb) {
-  constexpr long long R = 32 * KR_PAIR;
-  const long long la = PAD + m + R + PAD, lb = PAD + n + R + PAD;
-  nw_status st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
-  if (st) return st;
-  CUDA_TRY(c, cudaMemsetAsync(c->d_codes, 0, (size_t)(la + lb), c->stream));
+  constexpr long long R = R_MAX;
+  const long long la = pad16(PAD + m + R + PAD);
   *ca = c->d_codes + PAD;
   *cb = c->d_codes + la + PAD;
   const uint8_t *ra = a, *rb = b;
   if (host) {
-    st = grow(c, c->d_raw, c->raw_cap, (size_t)(m + n + 16));
+    nw_status st = grow(c, c->d_raw, c->raw_cap, (size_t)(m + n + 16));
     if (st) return st;
     if (m) CUDA_TRY(c, cudaMemcpyAsync(c->d_raw, a, (size_t)m, cudaMemcpyHostToDevice, c->stream));
     if (n) CUDA_TRY(c, cudaMemcpyAsync(c->d_raw + m, b, (size_t)n, cudaMemcpyHostToDevice, c->stream));
@@ -369,25 +406,41 @@ nw_status stage_pair(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
   return NW_OK;
 }
 
-nw_status new_tb(nw_ctx* c, long long m, long long n, const nw_scoring* sc, nw_tb** out) {
-  constexpr int R = 32 * KR_PAIR, SPW = 16 / KR_PAIR;
+nw_status new_tb(nw_ctx* c, long long m, long long n, const nw_scoring* sc, int kr, nw_tb** out) {
+  const int R = 32 * kr;
   nw_tb* tb = new (std::nothrow) nw_tb;
   if (!tb) return fail(c, NW_E_NOMEM, "host allocation");
+  memset(tb, 0, sizeof *tb);
   tb->ctx = c;
   tb->m = (int)m;
   tb->n = (int)n;
+  tb->kr = kr;
   memcpy(tb->tie, sc->tie, 3);
-  const long long nstrips = (m + R - 1) / R;
-  const long long nblk = (n + 62) / 32;
-  tb->wpl = nblk * (32 / SPW);
-  tb->dirs = nullptr;
-  const size_t bytes = (size_t)std::max<long long>(nstrips, 1) * tb->wpl * 32 * sizeof(uint32_t);
+  const long long S = std::max<long long>((m + R - 1) / R, 1);
+  tb->S = (int)S;
+  tb->wpl = (n + 31 + 7) / 8;
+  tb->segstride = pad16(R + n + 1);
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t b_dirs = al((size_t)S * tb->wpl * kr * 32 * sizeof(uint16_t));
+  const size_t b_ebnd = al((size_t)S * (n + 1) * sizeof(int));
+  const size_t b_cs = al((size_t)S * sizeof(int)), b_len = b_cs;
+  const size_t b_off = al((size_t)S * sizeof(long long)), b_em = al(sizeof(int));
+  const size_t b_seg = al((size_t)S * tb->segstride);
+  const size_t bytes = b_dirs + b_ebnd + b_cs + b_len + b_off + b_em + b_seg;
   if (m > 0 && n > 0) {
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&tb->dirs), bytes, c->stream);
+    cudaError_t e = cudaMallocAsync(&tb->mem, bytes, c->stream);
     if (e != cudaSuccess) {
       delete tb;
-      return fail(c, NW_E_NOMEM, "direction buffer of %zu bytes: %s", bytes, cudaGetErrorString(e));
+      return fail(c, NW_E_NOMEM, "traceback buffers of %zu bytes: %s", bytes, cudaGetErrorString(e));
     }
+    char* p = static_cast<char*>(tb->mem);
+    tb->dirs = reinterpret_cast<uint16_t*>(p); p += b_dirs;
+    tb->ebnd = reinterpret_cast<int*>(p); p += b_ebnd;
+    tb->cs = reinterpret_cast<int*>(p); p += b_cs;
+    tb->seglen = reinterpret_cast<int*>(p); p += b_len;
+    tb->segoff = reinterpret_cast<long long*>(p); p += b_off;
+    tb->em = reinterpret_cast<int*>(p); p += b_em;
+    tb->seg = reinterpret_cast<uint8_t*>(p);
   }
   *out = tb;
   return NW_OK;
@@ -405,19 +458,30 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
   CUDA_TRY(c, cudaSetDevice(c->device));
   st = upload_tables(c, sc);
   if (st) return st;
-  // zero ticket/err/hm/progress counters and the bad-position flag before encoding
-  st = init_small(c, 3 + (int)std::max<long long>((m + 32 * KR_PAIR - 1) / (32 * KR_PAIR), 1));
+  // workspace: padded code buffers and the tagged 2-slot boundary ring
+  constexpr long long R = R_MAX;
+  const long long la = pad16(PAD + m + R + PAD), lb = pad16(PAD + n + R + PAD);
+  const int kr = choose_kr(m, n, want_dirs);
+  st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
+  if (st) return st;
+  const long long bbytes = (long long)sizeof(unsigned long long) * 2 * bnd_stride(n);
+  st = grow(c, c->d_bnd, c->bnd_cap, (size_t)bbytes);
+  if (st) return st;
+  // one launch zeroes ticket/err/hm/em, the bad-position flag, the code
+  // buffers (their padding must hold valid codes) and the boundary ring (tags)
+  ZeroRanges zr{{c->d_codes, c->d_bnd, nullptr, nullptr}, {la + lb, bbytes, 0, 0}};
+  st = init_small(c, 4, zr);
   if (st) return st;
   uint8_t *ca, *cb;
   st = stage_pair(c, a, m, b, n, host, &ca, &cb);
   if (st) return st;
   nw_tb* tb = nullptr;
   if (want_dirs) {
-    st = new_tb(c, m, n, sc, &tb);
+    st = new_tb(c, m, n, sc, kr, &tb);
     if (st) return st;
   }
   long long* d_score = host ? c->d_score : score_out;
-  st = pair_core(c, ca, m, cb, n, sc, d_score, tb);
+  st = pair_core(c, ca, m, cb, n, sc, d_score, tb, kr);
   if (st) {
     if (tb) nw_tb_free(tb);
     return st;
@@ -572,7 +636,7 @@ nw_status nw_align_pair_dev(nw_ctx* c, const uint8_t* d_a, int64_t m, const uint
 
 void nw_tb_free(nw_tb* tb) {
   if (!tb) return;
-  if (tb->dirs) cudaFreeAsync(tb->dirs, tb->ctx->stream);
+  if (tb->mem) cudaFreeAsync(tb->mem, tb->ctx->stream);
   delete tb;
 }
 
@@ -580,13 +644,22 @@ static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops) {
   const long long L = (long long)tb->m + tb->n;
   nw_status st = grow(c, c->d_rev, c->rev_cap, (size_t)std::max<long long>(L, 1));
   if (st) return st;
+  (void)L;
   {
     KernelTimer kt(c, 1);
-    k_tb_walk<KR_PAIR><<<1, 32, 0, c->stream>>>(tb->dirs, tb->wpl, tb->m, tb->n, tb->tie[0],
-                                                tb->tie[1], tb->tie[2], c->d_rev, c->d_len);
+    const int S = tb->S;
+    k_tb_chain<<<1, 32, 0, c->stream>>>(tb->ebnd, tb->n, S, tb->em, tb->cs);
     LAUNCHED(c);
-    int blocks = (int)std::min<long long>((L + 255) / 256 + 1, (long long)c->sm_count * 4);
-    k_reverse<<<blocks, 256, 0, c->stream>>>(c->d_rev, c->d_len, d_ops);
+    const int smem_bytes = 96 * 1024;
+    auto kseg = tb->kr == 2 ? k_tb_segments<2> : (tb->kr == 4 ? k_tb_segments<4> : k_tb_segments<8>);
+    cudaFuncSetAttribute(kseg, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    kseg<<<S, 32, smem_bytes, c->stream>>>(tb->dirs, tb->wpl, tb->m, tb->n, tb->tie[0],
+                                           tb->tie[1], tb->tie[2], tb->cs, tb->seg, tb->segstride,
+                                           tb->seglen, smem_bytes / 2);
+    LAUNCHED(c);
+    k_tb_offsets<<<1, 1024, 0, c->stream>>>(tb->seglen, S, tb->segoff, c->d_len);
+    LAUNCHED(c);
+    k_tb_assemble<<<S, 256, 0, c->stream>>>(tb->seg, tb->segstride, tb->seglen, tb->segoff, d_ops);
     LAUNCHED(c);
   }
   CUDA_TRY(c, cudaGetLastError());
@@ -720,12 +793,11 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   int ctas_per_sm = 4;
   const long long nwarps = (long long)c->sm_count * ctas_per_sm * warps_per_cta;
   const long long bstride = maxlen + 1 + 64;
-  const long long nblk = (maxlen + 62) / 32;
-  const long long wpl = nblk * (32 / (16 / KR_BATCH));
-  const long long dstride = tbk ? ((maxlen + R - 1) / R) * wpl * 32 : 0;
+  const long long wpl = (maxlen + 31 + 7) / 8;  // 8-step groups per strip
+  const long long dstride = tbk ? ((maxlen + R - 1) / R) * wpl * KR_BATCH * 32 : 0;
   const size_t bytes_bnd = sizeof(int) * (size_t)(nwarps * 2 * bstride);
   const size_t bytes_hm = sizeof(int) * (size_t)nwarps;
-  const size_t bytes_dirs = sizeof(uint32_t) * (size_t)(nwarps * dstride);
+  const size_t bytes_dirs = sizeof(uint16_t) * (size_t)(nwarps * dstride);
   st = grow(c, c->d_scratch, c->scratch_cap, bytes_bnd + bytes_hm + bytes_dirs + 256);
   if (st) return st;
   BatchArgs B;
@@ -746,7 +818,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   B.wbnd = reinterpret_cast<int*>(base);
   B.bstride = bstride;
   B.whm = reinterpret_cast<int*>(base + bytes_bnd);
-  B.wdirs = tbk ? reinterpret_cast<uint32_t*>(base + ((bytes_bnd + bytes_hm + 255) & ~size_t(255)))
+  B.wdirs = tbk ? reinterpret_cast<uint16_t*>(base + ((bytes_bnd + bytes_hm + 255) & ~size_t(255)))
                 : nullptr;
   B.dstride = dstride;
   B.ops_off = d_ops_off;

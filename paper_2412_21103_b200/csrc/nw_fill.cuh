@@ -10,20 +10,28 @@
 // which has the same argmax as Eq. 1 (the shift adds the same g*(i+j) to all
 // three candidates) and needs no gap add on the up/left chains.
 //
-// Work decomposition (DESIGN.md §3): a warp owns a strip of R = 32*KR rows;
+// Work decomposition (DESIGN.md §3.2): a warp owns a strip of R = 32*KR rows;
 // lane l owns rows [l*KR, l*KR+KR) of it and sweeps the columns, lane l running
 // one column behind lane l-1 (the anti-diagonal skew), so at step t lane l
 // computes column j = t - l + 1 for its KR rows. The bottom cell of lane l-1 at
-// column j arrives by __shfl_sync; the strip's top row comes from the strip
-// above through a boundary row in global memory guarded by a release/acquire
-// progress counter (replacing the per-cell spin of P:88-92, Code 1 P:110).
+// column j arrives by __shfl_sync. Between strips (MULTIWARP), lane 31 of strip
+// s publishes its bottom row as 64-bit entries (tag = s+1, H') that strip s+1
+// polls directly: a single-copy-atomic 8-byte store carries its own validity,
+// so no fence or flag is needed (replacing the per-cell spin of P:88-92,
+// Code 1 P:110, which had no memory ordering at all).
 //
 // With directions, every cell also yields two decision bits for the tie
-// order pi = (X, Y, Z):  nb1 = [c_Y < c_Z],  nb0 = [c_X < max(c_Y, c_Z)]  (the
-// sign bits of two differences); the code is X if !nb0, else Y if !nb1, else Z
-// -- the first maximal candidate in pi. They are packed 16 cells per 32-bit
-// word: word row w of lane l in strip s covers steps [w*SPW, w*SPW+SPW), cell
-// index c = (t % SPW)*KR + r, bits (31-2c, 30-2c) = (nb1, nb0).
+// order pi = (X, Y, Z):  nbX = [c_X < H'],  nbY = [c_Y < H']  (the sign bits of
+// c_X - H' and c_Y - H'); the code is X if !nbX, else Y if !nbY, else Z -- the
+// first maximal candidate in pi. Each lane packs one row's bits of 8 steps into
+// a halfword: group g = t/8, halfword index ((s*G + g)*KR + r)*32 + lane, step
+// k = t%8 at bits (15-2k, 14-2k) = (nbX, nbY); every store is 64 contiguous bytes.
+//
+// TBE (traceback exits): every cell also carries E(i,j), the
+// column at which the traceback path from (i,j) first reaches the strip's top
+// boundary row: E = E(predecessor chosen by the decision bits), E(top, j) = j,
+// E(i, 0) = 0. The bottom row's E values let the traceback split into
+// independent per-strip walks.
 #pragma once
 #include <cstdint>
 
@@ -40,35 +48,24 @@ struct FillArgs {
   int m, n;
   int nstrips;
   int nslots;          // boundary ring slots (>= 2)
-  int* bnd;            // [nslots][bstride] boundary rows H'(strip top, j), j = 0..n
-  long long bstride;
-  int* prog;           // [nstrips] columns of strip s's bottom row published
-  int* ticket;         // strip dispenser
-  uint32_t* dirs;      // [nstrips][wpl][32] packed decision bits (DIRS)
-  long long wpl;       // words per lane per strip
+  void* bnd;           // [nslots][bstride] boundary rows: MULTIWARP 64-bit (tag<<32 | H'), else int H'
+  long long bstride;   // entries per slot
+  int* ticket;         // strip dispenser (MULTIWARP)
+  uint16_t* dirs;      // [nstrips][wpl][KR][32] decision-bit halfwords (DIRS)
+  long long wpl;       // 8-step groups per strip
+  int* ebnd;           // [nstrips][n+1] exit columns E of each strip's bottom row (TBE)
   int* hm;             // H'(m, n) output
+  int* em;             // E(m, n) output (TBE)
   int* err;            // watchdog flag (NW_E_DEADLOCK)
 };
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// Spin until *p >= need (acquire). Watchdog: ~2^24 polls with backoff, then flag.
-__device__ __forceinline__ void wait_progress(const int* p, int need, int* err) {
-  if (ld_acquire(p) >= need) return;
-  unsigned ns = 32;
-  for (long long it = 0;; ++it) {
-    if (ld_acquire(p) >= need) return;
-    __nanosleep(ns);
-    if (ns < 256) ns <<= 1;
-    if (it > (1ll << 24)) { atomicExch(err, 8); return; }
-  }
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // PRMT in its default mode: selector nibble = byte index (bits 0-2) + sign
@@ -96,24 +93,26 @@ __device__ __forceinline__ int pick(int cD, int cU, int cL) {
 template <int KR>
 struct LaneState {
   int Hl[KR];        // H'(row r, previous column)
+  int El[KR];        // E(row r, previous column) (TBE)
   uint32_t P[KR];    // register profile (PROFREG): byte c = s(a_r, c) - 2g
-  int diag;          // H'(top-1, j-1)
-  int send;          // H'(bottom, j), sent to lane+1
-  int chunk_cur, chunk_nxt;  // boundary-row chunks (lane q holds column 32*blk+1+q)
-  uint32_t acc;      // direction accumulator
+  uint32_t acc[KR];  // decision bits of row r for the current 8-step group (DIRS)
+  int diag, ediag;   // H'(top-1, j-1), E(top-1, j-1)
+  int send, esend;   // H'(bottom, j), E(bottom, j): sent to lane+1
+  int chunk_cur, chunk_nxt;  // boundary values for 8 columns (lane q < 8 holds column t0+1+q)
+  uint32_t bc_nxt;   // prefetched column code for the next step
 };
 
 // Strip geometry / pointers that stay fixed during one sweep.
 struct StripCtx {
   const uint8_t* b;
-  const int8_t* sprof;   // shared profile [K][R] (not PROFREG)
-  const int* bnd_in;     // boundary row read (strip s-1's bottom), null for s == 0
-  int* bnd_out;          // boundary row written (this strip's bottom)
-  uint32_t* dir_base;    // this lane's direction words
-  int* prog_in;          // strip s-1's progress counter (MULTIWARP)
-  int* prog_out;         // this strip's progress counter (MULTIWARP)
+  const int8_t* sprof;              // shared profile [K][R] (not PROFREG)
+  const void* bnd_in;               // boundary row read (strip s-1's bottom), null for s == 0
+  void* bnd_out;                    // boundary row written (this strip's bottom)
+  uint16_t* dir_base;               // this lane's decision-bit halfwords
+  int* ebnd_out;                    // this strip's bottom-row exits (TBE)
   int* err;
   int* hm;
+  int* em;
   int n, s, lane;
   int hm_lane, hm_r, hm_t;  // where H'(m, n) lives in this strip (hm_lane < 0: not here)
 };
@@ -126,80 +125,147 @@ __device__ __forceinline__ int cell_score(const LaneState<KR>& st, int r, uint32
   return prmt(w, rr | ((rr | 8u) * 0x1110u));
 }
 
-// 32 steps of the sweep: steps t0 .. t0+31, lane column j = t - lane + 1.
-// MASKED blocks contain columns outside [1, n] for some lane (first / last blocks).
-template <int KR, bool DIRS, bool PROFREG, int PI, bool MULTIWARP, bool MASKED>
-__device__ __forceinline__ void sweep_block(LaneState<KR>& st, const StripCtx& C, int blk) {
-  constexpr int R = 32 * KR, SPW = 16 / KR, WPB = 32 / SPW;
-  using T = Tie<PI>;
-  const int t0 = blk * 32;
-  const int lane = C.lane, n = C.n;
-  // boundary chunk for the next block: wait for the producer, then load
-  st.chunk_cur = st.chunk_nxt;
-  if (C.s > 0) {
-    const int c0 = t0 + 32;  // chunk blk+1 covers columns c0+1 .. c0+32
-    if (c0 < n) {
-      if (MULTIWARP) wait_progress(C.prog_in, min(n, c0 + 32), C.err);
-      const int jj = c0 + 1 + lane;
-      st.chunk_nxt = (jj <= n) ? (MULTIWARP ? __ldcg(C.bnd_in + jj) : C.bnd_in[jj]) : 0;
+// Boundary chunk = the strip-above's bottom-row values of 8 columns c0+1..c0+8,
+// lane q < 8 holding column c0+1+q. Issued one 8-step group before it is used
+// and verified (MULTIWARP: tag == s) just before, so the L2 round trip overlaps
+// a whole group of steps.
+template <bool MULTIWARP>
+__device__ __forceinline__ unsigned long long chunk_issue(const StripCtx& C, int c0) {
+  const int jj = c0 + 1 + C.lane;
+  if (C.lane >= 8 || jj > C.n) return 0ull;
+  if (!MULTIWARP) return (unsigned)static_cast<const int*>(C.bnd_in)[jj];
+  return ld_relaxed_u64(static_cast<const unsigned long long*>(C.bnd_in) + jj);
+}
+
+template <bool MULTIWARP>
+__device__ __forceinline__ int chunk_verify(const StripCtx& C, int c0, unsigned long long v) {
+  if (!MULTIWARP) return (int)(unsigned)v;
+  const int jj = c0 + 1 + C.lane;
+  const bool need = C.lane < 8 && jj <= C.n;
+  const unsigned tag = (unsigned)C.s;  // strip s-1 writes tag (s-1)+1
+  bool ok = !need || (unsigned)(v >> 32) == tag;
+  if (__all_sync(FULL, ok)) return (int)(unsigned)v;
+  const unsigned long long* p = static_cast<const unsigned long long*>(C.bnd_in) + jj;
+  for (long long it = 0;; ++it) {
+    __nanosleep(20);
+    if (!ok) {
+      v = ld_relaxed_u64(p);
+      ok = (unsigned)(v >> 32) == tag;
+    }
+    if (__all_sync(FULL, ok)) break;
+    if (it > (1ll << 26)) {  // watchdog: report and stop waiting (results invalid)
+      if (C.lane == 0) atomicExch(C.err, 8);
+      break;
     }
   }
+  return (int)(unsigned)v;
+}
+
+// One 8-step group of the sweep starting at t0 (t0 % 8 == 0): lane column j = t - lane + 1.
+// MASKED groups contain columns outside [1, n] for some lane (or the H'(m,n) cell).
+template <int KR, bool DIRS, bool PROFREG, int PI, bool MULTIWARP, bool TBE, bool MASKED>
+__device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C, int t0) {
+  constexpr int R = 32 * KR;
+  using T = Tie<PI>;
+  const int lane = C.lane, n = C.n;
 #pragma unroll
-  for (int q = 0; q < 32; ++q) {
+  for (int q = 0; q < 8; ++q) {
     const int t = t0 + q;
     const int j = t - lane + 1;  // this lane's column (1-based)
-    const uint32_t bc = C.b[j - 1];  // PAD bytes make j in [-31, n+62] readable
+    const uint32_t bc = st.bc_nxt;
+    st.bc_nxt = __ldg(C.b + j);  // next step's b_{j+1} (PAD makes j in [-31, n+62] readable)
     uint32_t sel = 0;
     uint2 pw = make_uint2(0, 0);
     if (PROFREG) {
       sel = bc * 0x1111u | 0x8880u;  // byte bc, sign-replicated into bytes 1..3
     } else if (KR == 8) {
       pw = *reinterpret_cast<const uint2*>(C.sprof + bc * R + lane * KR);
-    } else {
+    } else if (KR == 4) {
       pw.x = *reinterpret_cast<const uint32_t*>(C.sprof + bc * R + lane * KR);
+    } else {
+      static_assert(KR == 2 || KR == 4 || KR == 8, "KR must be 2, 4 or 8");
+      pw.x = *reinterpret_cast<const uint16_t*>(C.sprof + bc * R + lane * KR);
     }
     // up = H'(top-1, j): lane 0 from the boundary row (0 for strip 0), others from lane-1
     const int recv = __shfl_up_sync(FULL, st.send, 1);
-    const int bval = (C.s == 0) ? 0 : __shfl_sync(FULL, st.chunk_cur, q);  // s is warp-uniform
+    const int bval = __shfl_sync(FULL, st.chunk_cur, q);  // strip 0: chunks hold H'(0, j) = 0
     const int up = (lane == 0) ? bval : recv;
-    int hd = st.diag, hu = up;
+    int eup = 0;
+    if (TBE) {
+      const int erecv = __shfl_up_sync(FULL, st.esend, 1);
+      eup = (lane == 0) ? j : erecv;  // E(top boundary row, j) = j
+    }
+    int hd = st.diag, hu = up, ed = st.ediag, eu = eup;
 #pragma unroll
     for (int r = 0; r < KR; ++r) {
       const int S = cell_score<KR, PROFREG>(st, r, sel, pw);
       const int cD = hd + S, cU = hu, cL = st.Hl[r];
-      int h;
+      // the up candidate arrives last (vertical chain): fold diag and left first
+      int h = max(max(cD, cL), cU);
+      int e = 0;
       if (DIRS) {
         const int cX = pick<T::X>(cD, cU, cL);
         const int cY = pick<T::Y>(cD, cU, cL);
-        const int cZ = pick<T::Z>(cD, cU, cL);
-        const int m1 = max(cY, cZ);
-        h = max(cX, m1);
-        const int d1 = cY - cZ;  // < 0  <=>  c_Y <  c_Z           (bit nb1)
-        const int d0 = cX - m1;  // < 0  <=>  c_X <  max(c_Y, c_Z)  (bit nb0)
-        st.acc = __funnelshift_l((uint32_t)d1, st.acc, 1);
-        st.acc = __funnelshift_l((uint32_t)d0, st.acc, 1);
-      } else {
-        h = __vimax3_s32(cD, cU, cL);
+        const int dX = cX - h;  // 0 iff X is maximal, else < 0  (bit nbX = sign)
+        const int dY = cY - h;  // 0 iff Y is maximal, else < 0  (bit nbY = sign)
+        st.acc[r] = __funnelshift_l((uint32_t)dX, st.acc[r], 1);
+        st.acc[r] = __funnelshift_l((uint32_t)dY, st.acc[r], 1);
+        if (TBE) {
+          // E follows the chosen predecessor: X if dX == 0, else Y if dY == 0, else Z.
+          // Written so that the up value eu (the vertical chain) enters one select.
+          const bool isX = dX >= 0, isY = dY >= 0;
+          const int el = st.El[r];
+          if (T::X == 2) {
+            e = isX ? eu : (isY ? pick<T::Y>(ed, eu, el) : pick<T::Z>(ed, eu, el));
+          } else if (T::Y == 2) {
+            const int o = isX ? pick<T::X>(ed, eu, el) : pick<T::Z>(ed, eu, el);
+            e = (!isX && isY) ? eu : o;
+          } else {
+            const int o = isX ? pick<T::X>(ed, eu, el) : pick<T::Y>(ed, eu, el);
+            e = (!isX && !isY) ? eu : o;
+          }
+        }
       }
-      if (MASKED) h = (j >= 1) ? h : 0;  // border column H'(i, 0) = 0 until the lane starts
+      if (MASKED) {  // border column H'(i, 0) = 0, E(i, 0) = 0 until the lane starts
+        h = (j >= 1) ? h : 0;
+        if (TBE) e = (j >= 1) ? e : 0;
+      }
       hd = st.Hl[r];
       hu = h;
       st.Hl[r] = h;
+      if (TBE) {
+        ed = st.El[r];
+        eu = e;
+        st.El[r] = e;
+      }
     }
     st.diag = MASKED ? ((j >= 1) ? up : 0) : up;
     st.send = st.Hl[KR - 1];
-    if (DIRS && (q % SPW) == SPW - 1) C.dir_base[((long long)blk * WPB + q / SPW) * 32] = st.acc;
-    if (lane == 31 && (!MASKED || (j >= 1 && j <= n))) C.bnd_out[j] = st.send;
+    if (TBE) {
+      st.ediag = MASKED ? ((j >= 1) ? eup : 0) : eup;
+      st.esend = st.El[KR - 1];
+    }
+    if (lane == 31 && (!MASKED || (j >= 1 && j <= n))) {
+      if (MULTIWARP)
+        st_relaxed_u64(static_cast<unsigned long long*>(C.bnd_out) + j,
+                       ((unsigned long long)(unsigned)(C.s + 1) << 32) | (unsigned)st.send);
+      else
+        static_cast<int*>(C.bnd_out)[j] = st.send;
+      if (TBE) C.ebnd_out[j] = st.esend;
+    }
     if (MASKED && lane == C.hm_lane && t == C.hm_t) {
 #pragma unroll
       for (int r = 0; r < KR; ++r)
-        if (r == C.hm_r) *C.hm = st.Hl[r];
+        if (r == C.hm_r) {
+          *C.hm = st.Hl[r];
+          if (TBE) *C.em = st.El[r];
+        }
     }
   }
-  // publish this block's bottom-row columns (lane 31 wrote up to j = t0 + 1)
-  if (MULTIWARP && lane == 31) {
-    const int jdone = min(n, t0 + 1);
-    if (jdone >= 1) st_release(C.prog_out, jdone);
+  if (DIRS) {  // group g = t0/8: halfword (g, r, lane), step k at bits (15-2k, 14-2k) = (nbX, nbY)
+    uint16_t* d = C.dir_base + (long long)(t0 >> 3) * (KR * 32);
+#pragma unroll
+    for (int r = 0; r < KR; ++r) d[r * 32] = (uint16_t)st.acc[r];
   }
 }
 
@@ -207,7 +273,7 @@ __device__ __forceinline__ void sweep_block(LaneState<KR>& st, const StripCtx& C
 // PROFREG: K <= 4, the lane's KR profile words live in registers and each
 // cell's score is one PRMT; otherwise the profile column for b_j is read from
 // shared memory (sprof, K x R bytes per warp).
-template <int KR, bool DIRS, bool PROFREG, int PI, bool MULTIWARP>
+template <int KR, bool DIRS, bool PROFREG, int PI, bool MULTIWARP, bool TBE>
 __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, int8_t* sprof) {
   constexpr int R = 32 * KR;
   const int n = A.n;
@@ -231,21 +297,26 @@ __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, 
     __syncwarp();
   }
 #pragma unroll
-  for (int r = 0; r < KR; ++r) st.Hl[r] = 0;
-  st.diag = 0;
-  st.send = 0;
-  st.acc = 0;
+  for (int r = 0; r < KR; ++r) {
+    st.Hl[r] = 0;
+    st.El[r] = 0;
+    st.acc[r] = 0;
+  }
+  st.diag = st.ediag = 0;
+  st.send = st.esend = 0;
   st.chunk_cur = st.chunk_nxt = 0;
   StripCtx C;
   C.b = A.b;
   C.sprof = sprof;
-  C.bnd_in = (s > 0) ? A.bnd + (long long)(s % A.nslots) * A.bstride : nullptr;
-  C.bnd_out = A.bnd + (long long)((s + 1) % A.nslots) * A.bstride;
-  C.dir_base = DIRS ? A.dirs + (long long)s * A.wpl * 32 + lane : nullptr;
-  C.prog_in = (MULTIWARP && s > 0) ? A.prog + (s - 1) : nullptr;
-  C.prog_out = MULTIWARP ? A.prog + s : nullptr;
+  const size_t esz = MULTIWARP ? 8 : 4;
+  char* bnd = static_cast<char*>(A.bnd);
+  C.bnd_in = (s > 0) ? bnd + esz * (size_t)((s % A.nslots) * A.bstride) : nullptr;
+  C.bnd_out = bnd + esz * (size_t)(((s + 1) % A.nslots) * A.bstride);
+  C.dir_base = DIRS ? A.dirs + (long long)s * A.wpl * (KR * 32) + lane : nullptr;
+  C.ebnd_out = TBE ? A.ebnd + (long long)s * (n + 1) : nullptr;
   C.err = A.err;
   C.hm = A.hm;
+  C.em = A.em;
   C.n = n;
   C.s = s;
   C.lane = lane;
@@ -254,18 +325,21 @@ __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, 
     const int rr = (A.m - 1) % R;
     C.hm_lane = rr / KR; C.hm_r = rr % KR; C.hm_t = n - 1 + C.hm_lane;
   }
-  // the first boundary chunk (block 0's columns 1..32)
-  if (s > 0) {
-    if (MULTIWARP) wait_progress(C.prog_in, min(n, 32), C.err);
-    st.chunk_nxt = (lane + 1 <= n) ? (MULTIWARP ? __ldcg(C.bnd_in + lane + 1) : C.bnd_in[lane + 1]) : 0;
+  st.bc_nxt = __ldg(A.b - lane);  // b_{j-1} for step 0 (j = 1 - lane)
+  if (s > 0) st.chunk_nxt = chunk_verify<MULTIWARP>(C, 0, chunk_issue<MULTIWARP>(C, 0));
+  const int ngrp = (n + 31 + 7) / 8;  // steps 0 .. n+30 in groups of 8
+#pragma unroll 1
+  for (int g = 0; g < ngrp; ++g) {
+    const int t0 = g * 8;
+    st.chunk_cur = st.chunk_nxt;
+    const bool more = s > 0 && t0 + 8 < n;
+    unsigned long long raw = 0;
+    if (more) raw = chunk_issue<MULTIWARP>(C, t0 + 8);
+    const bool masked = t0 < 31 || t0 + 7 >= n - 1;
+    if (masked) sweep_group<KR, DIRS, PROFREG, PI, MULTIWARP, TBE, true>(st, C, t0);
+    else sweep_group<KR, DIRS, PROFREG, PI, MULTIWARP, TBE, false>(st, C, t0);
+    if (more) st.chunk_nxt = chunk_verify<MULTIWARP>(C, t0 + 8, raw);
   }
-  const int nblk = (n + 31 + 31) / 32;  // steps 0 .. n+30
-  for (int blk = 0; blk < nblk; ++blk) {
-    const bool masked = blk == 0 || blk * 32 + 31 >= n - 1;
-    if (masked) sweep_block<KR, DIRS, PROFREG, PI, MULTIWARP, true>(st, C, blk);
-    else sweep_block<KR, DIRS, PROFREG, PI, MULTIWARP, false>(st, C, blk);
-  }
-  if (MULTIWARP && lane == 31) st_release(C.prog_out, n);
   __syncwarp();
 }
 

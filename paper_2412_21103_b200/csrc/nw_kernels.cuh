@@ -2,9 +2,11 @@
 //
 //   k_init      zero the per-call progress counters / tickets / flags
 //   k_encode    residues -> alphabet codes (R10), first bad position (atomicMin)
-//   k_fill_pair one pair, many warps: strips chained by release/acquire counters
-//   k_tb_walk   backtracking of Sec. 2.4 over the packed decision bits
-//   k_reverse   reversed walk -> forward-order codes (P:90 codes 1/2/3)
+//   k_fill_pair one pair, many warps: strips chained by tagged boundary entries
+//   k_tb_chain  traceback exits: entry column of every strip (one thread)
+//   k_tb_segments per-strip backtracking of Sec. 2.4, all strips at once
+//   k_tb_offsets / k_tb_assemble  segment offsets, forward-order codes
+//   (the batch kernel walks each pair with tb_walk inside the same warp)
 //   k_batch     many pairs: one warp per pair, strips in sequence,
 //               optional per-pair traceback by the same warp
 #pragma once
@@ -13,10 +15,23 @@
 namespace nwk {
 
 #ifdef NW_COMMON_KERNELS  // defined in exactly one TU (nw_api.cu)
-__global__ void k_init(int* ints, int nints, long long* bad) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nints; i += gridDim.x * blockDim.x)
-    ints[i] = 0;
-  if (bad && blockIdx.x == 0 && threadIdx.x == 0) *bad = 0x7fffffffffffffffll;
+struct ZeroRanges {
+  void* p[4];
+  long long bytes[4];  // multiples of 16, 16-byte aligned
+};
+
+// Per-call reset: small counters, the bad-position flag and up to 4 buffers
+// (tagged boundary ring, padded code buffers) that must start zeroed.
+__global__ void k_init(int* ints, int nints, long long* bad, ZeroRanges zr) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < nints; i += nth) ints[i] = 0;
+  if (bad && tid == 0) *bad = 0x7fffffffffffffffll;
+  for (int r = 0; r < 4; ++r) {
+    uint4* q = static_cast<uint4*>(zr.p[r]);
+    const long long n16 = zr.bytes[r] / 16;
+    for (long long i = tid; i < n16; i += nth) q[i] = make_uint4(0, 0, 0, 0);
+  }
 }
 
 // out[k] = lut[in[k]] (0xff marks a symbol outside the alphabet: code 0 is
@@ -65,35 +80,40 @@ __global__ void __launch_bounds__(32) k_fill_pair(FillArgs A) {
     if (lane == 0) s = atomicAdd(A.ticket, 1);
     s = __shfl_sync(FULL, s, 0);
     if (s >= A.nstrips) break;
-    strip_sweep<KR, DIRS, PROFREG, PI, true>(A, s, lane, smem);
+    strip_sweep<KR, DIRS, PROFREG, PI, true, DIRS>(A, s, lane, smem);
   }
 }
 
-// Decode the 2 decision bits of cell (i, j) (1-based, interior) -> P:90 code.
+// Decode the decision bits of interior cell (i, j) (1-based) -> P:90 code
+// (layout in nw_fill.cuh: halfword ((s*G + g)*KR + r)*32 + l, step k = t%8 at
+// bits (15-2k, 14-2k) = (nbX, nbY); code X if !nbX, else Y if !nbY, else Z).
 template <int KR>
-__device__ __forceinline__ int tb_code(const uint32_t* dirs, long long wpl, int i, int j, int X,
-                                       int Y, int Z, long long& cur_w, uint32_t& word) {
-  constexpr int R = 32 * KR, SPW = 16 / KR;
+__device__ __forceinline__ int tb_decode(uint32_t hw, int k, int X, int Y, int Z) {
+  const uint32_t f = (hw >> (14 - 2 * k)) & 3u;
+  return !(f & 2u) ? X : (!(f & 1u) ? Y : Z);
+}
+
+template <int KR>
+__device__ __forceinline__ long long tb_index(long long G, int i, int j, int& k) {
+  constexpr int R = 32 * KR;
   const int ia = i - 1;
   const int s = ia / R, l = (ia % R) / KR, r = ia % KR;
   const int t = (j - 1) + l;
-  const long long widx = ((long long)s * wpl + t / SPW) * 32 + l;
-  if (widx != cur_w) { word = __ldcg(dirs + widx); cur_w = widx; }
-  const int c = (t % SPW) * KR + r;
-  const uint32_t f = (word >> (30 - 2 * c)) & 3u;
-  return !(f & 1u) ? X : (!(f & 2u) ? Y : Z);  // f = (nb1, nb0), nw_fill.cuh
+  k = t & 7;
+  return (((long long)s * G + (t >> 3)) * KR + r) * 32 + l;
 }
 
 // Walk from (m, n) to (0, 0); rev[k] = k-th code from the end.
 // Border cells follow R7: column 0 -> vertical, row 0 -> horizontal.
 template <int KR>
-__device__ long long tb_walk(const uint32_t* dirs, long long wpl, int m, int n, int X, int Y,
+__device__ long long tb_walk(const uint16_t* dirs, long long G, int m, int n, int X, int Y,
                              int Z, uint8_t* rev) {
   int i = m, j = n;
-  long long k = 0, cur_w = -1;
-  uint32_t word = 0;
+  long long k = 0;
   while (i > 0 && j > 0) {
-    const int code = tb_code<KR>(dirs, wpl, i, j, X, Y, Z, cur_w, word);
+    int kk;
+    const long long idx = tb_index<KR>(G, i, j, kk);
+    const int code = tb_decode<KR>(__ldcg(dirs + idx), kk, X, Y, Z);
     rev[k++] = (uint8_t)code;
     i -= (code != 3);
     j -= (code != 2);
@@ -103,23 +123,116 @@ __device__ long long tb_walk(const uint32_t* dirs, long long wpl, int m, int n, 
   return k;
 }
 
-template <int KR>
-__global__ void k_tb_walk(const uint32_t* dirs, long long wpl, int m, int n, int X, int Y, int Z,
-                          uint8_t* rev, long long* len) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) *len = tb_walk<KR>(dirs, wpl, m, n, X, Y, Z, rev);
-}
-
 #ifdef NW_COMMON_KERNELS
-// out[p] = rev[len-1-p], p < len
-__global__ void k_reverse(const uint8_t* __restrict__ rev, const long long* __restrict__ len,
-                          uint8_t* __restrict__ out) {
-  const long long L = *len;
-  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < L;
-       p += (long long)gridDim.x * blockDim.x)
-    out[p] = rev[L - 1 - p];
+// ---- single-pair traceback split at strip boundaries ----
+// cs[s] = column where the path enters strip s: at row m for the last strip
+// (cs[S-1] = n), else on strip s's bottom row R*(s+1). Exits chain through the
+// fill's E values: cs[S-2] = E(m, n), cs[s-1] = ebnd[s][cs[s]].
+__global__ void k_tb_chain(const int* __restrict__ ebnd, int n, int S, const int* em, int* cs) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int c = n;
+  cs[S - 1] = c;
+  if (S >= 2) {
+    c = *em;
+    cs[S - 2] = c;
+    for (int s = S - 2; s >= 1; --s) {
+      // column 0 is the left border: a path there stays there (E(i, 0) = 0)
+      c = (c == 0) ? 0 : __ldcg(ebnd + (long long)s * (n + 1) + c);
+      cs[s - 1] = c;
+    }
+  }
 }
 
 #endif  // NW_COMMON_KERNELS
+
+// One warp per strip: walk from the strip's entry to its top boundary row (the
+// last row of the strip above), codes written last-first into seg + s*segstride.
+// The decision halfwords the walk can touch (columns cs[s-1] .. cs[s]) are
+// staged in shared memory when they fit, so each step is a shared-memory read.
+template <int KR>
+__global__ void __launch_bounds__(32) k_tb_segments(const uint16_t* __restrict__ dirs, long long G,
+                                                   int m, int n, int X, int Y, int Z,
+                                                   const int* __restrict__ cs, uint8_t* seg,
+                                                   long long segstride, int* seglen, int smem_hw) {
+  constexpr int R = 32 * KR;
+  constexpr int GS = KR * 32;  // halfwords per (strip, group)
+  extern __shared__ __align__(16) uint16_t sh[];
+  const int s = blockIdx.x, lane = threadIdx.x;
+  const int S = gridDim.x;
+  int i = (s == S - 1) ? m : R * (s + 1);
+  int j = cs[s];
+  const int i_stop = R * s;
+  const int j_lo = (s > 0) ? cs[s - 1] : 0;
+  // groups g holding steps t = j' - 1 + l for j' in [j_lo, j], l in [0, 31]
+  const long long g_lo = max(0, j_lo - 1) >> 3;
+  const long long g_hi = (long long)(j + 30) >> 3;
+  const long long ng = g_hi - g_lo + 1;
+  const bool staged = ng * GS <= smem_hw;
+  const uint16_t* base = dirs + (long long)s * G * GS;
+  if (staged) {
+    const uint4* src = reinterpret_cast<const uint4*>(base + g_lo * GS);
+    uint4* dst = reinterpret_cast<uint4*>(sh);
+    const long long n16 = ng * GS / 8;
+    for (long long q = lane; q < n16; q += 32) dst[q] = __ldcg(src + q);
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  uint8_t* out = seg + (long long)s * segstride;
+  int k = 0;
+  while (i > i_stop) {
+    if (j == 0) { out[k++] = 2; --i; continue; }  // border column: vertical (R7)
+    const int ia = i - 1;
+    const int l = (ia % R) / KR, r = ia % KR;
+    const int t = (j - 1) + l;
+    const long long g = t >> 3;
+    const long long off = (g * KR + r) * 32 + l;
+    const uint32_t hw = staged ? sh[off - g_lo * GS] : __ldcg(base + off);
+    const int code = tb_decode<KR>(hw, t & 7, X, Y, Z);
+    out[k++] = (uint8_t)code;
+    i -= (code != 3);
+    j -= (code != 2);
+  }
+  if (s == 0)
+    while (j > 0) { out[k++] = 3; --j; }  // row 0: horizontal (R7)
+  seglen[s] = k;
+}
+
+#ifdef NW_COMMON_KERNELS
+// Exclusive prefix of the segment lengths (top strip first) and the total.
+__global__ void k_tb_offsets(const int* __restrict__ seglen, int S, long long* segoff,
+                             long long* total) {
+  __shared__ long long part[1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (S + nt - 1) / nt;
+  const int lo = min(S, tid * per), hi = min(S, lo + per);
+  long long acc = 0;
+  for (int k = lo; k < hi; ++k) acc += seglen[k];
+  part[tid] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    long long run = 0;
+    for (int k = 0; k < nt; ++k) { const long long v = part[k]; part[k] = run; run += v; }
+    *total = run;
+  }
+  __syncthreads();
+  long long run = part[tid];
+  for (int k = lo; k < hi; ++k) { segoff[k] = run; run += seglen[k]; }
+}
+
+// out[segoff[s] + p] = seg[s][seglen[s] - 1 - p]: forward order, one block per strip.
+__global__ void k_tb_assemble(const uint8_t* __restrict__ seg, long long segstride,
+                              const int* __restrict__ seglen, const long long* __restrict__ segoff,
+                              uint8_t* __restrict__ out) {
+  const int s = blockIdx.x;
+  const int L = seglen[s];
+  const uint8_t* src = seg + (long long)s * segstride;
+  uint8_t* dst = out + segoff[s];
+  for (int p = threadIdx.x; p < L; p += blockDim.x) dst[p] = src[L - 1 - p];
+}
+
+#endif  // NW_COMMON_KERNELS
+
+
 
 struct BatchArgs {
   const uint8_t* codes;    // concatenated codes, padded (PAD before, >= R + PAD after)
@@ -138,7 +251,7 @@ struct BatchArgs {
   int* wbnd;               // [nwarps][2][bstride]
   long long bstride;
   int* whm;                // [nwarps]
-  uint32_t* wdirs;         // [nwarps][dstride] (TRACEBACK)
+  uint16_t* wdirs;         // [nwarps][dstride] (TRACEBACK)
   long long dstride;
   // traceback outputs
   const long long* ops_off;
@@ -170,7 +283,7 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
   int8_t* sprof = smem + (PROFREG ? 0 : wib * (B.K * R));
   int* bnd = B.wbnd + gw * 2 * B.bstride;
-  uint32_t* wd = DIRS ? B.wdirs + gw * B.dstride : nullptr;
+  uint16_t* wd = DIRS ? B.wdirs + gw * B.dstride : nullptr;
   for (;;) {
     int task = 0;
     if (lane == 0) task = atomicAdd(B.ticket, 1);
@@ -197,11 +310,11 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       FillArgs A;
       A.a = B.codes + ao; A.b = B.codes + bo; A.prof = B.prof; A.K = B.K;
       A.m = m; A.n = n; A.nstrips = (m + R - 1) / R; A.nslots = 2;
-      A.bnd = bnd; A.bstride = B.bstride; A.prog = nullptr; A.ticket = nullptr;
+      A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr; A.ebnd = nullptr; A.em = nullptr;
       A.dirs = wd;
-      A.wpl = (long long)((n + 62) / 32) * (32 / (16 / KR));
+      A.wpl = (n + 31 + 7) / 8;  // 8-step groups per strip
       A.hm = B.whm + gw; A.err = B.err;
-      for (int s = 0; s < A.nstrips; ++s) strip_sweep<KR, DIRS, PROFREG, PI, false>(A, s, lane, sprof);
+      for (int s = 0; s < A.nstrips; ++s) strip_sweep<KR, DIRS, PROFREG, PI, false, false>(A, s, lane, sprof);
       __syncwarp();
       hmv = *(volatile int*)(B.whm + gw);
       if (DIRS) {

@@ -7,12 +7,13 @@
 
 namespace nwk {
 
-constexpr int KR_PAIR = 8;   // rows per lane, single-pair kernels
+constexpr int KR_MAX = 8;    // rows per lane: single-pair kernels pick 2, 4 or 8 per shape
+constexpr int R_MAX = 32 * KR_MAX;
 constexpr int KR_BATCH = 8;  // rows per lane, batch kernel
 
 // DIRS = true launchers, one instantiation per tie order PI (nw_inst_<PI>.cu)
 template <int PI>
-void launch_fill_dirs(const FillArgs& A, bool profreg, int grid, size_t smem, cudaStream_t st);
+void launch_fill_dirs(const FillArgs& A, int kr, bool profreg, int grid, size_t smem, cudaStream_t st);
 template <int PI>
 void launch_batch_dirs(const BatchArgs& B, bool profreg, int grid, size_t smem, cudaStream_t st);
 
@@ -32,10 +33,18 @@ void launch_batch_t(const BatchArgs& B, int grid, size_t smem, cudaStream_t st) 
 
 #define NW_DEFINE_DIRS_LAUNCHERS(PI)                                                          \
   template <>                                                                                 \
-  void launch_fill_dirs<PI>(const FillArgs& A, bool profreg, int grid, size_t smem,           \
+  void launch_fill_dirs<PI>(const FillArgs& A, int kr, bool profreg, int grid, size_t smem,   \
                             cudaStream_t st) {                                                \
-    if (profreg) launch_fill_t<KR_PAIR, true, true, PI>(A, grid, smem, st);                   \
-    else launch_fill_t<KR_PAIR, true, false, PI>(A, grid, smem, st);                          \
+    if (kr == 2) {                                                                            \
+      if (profreg) launch_fill_t<2, true, true, PI>(A, grid, smem, st);                       \
+      else launch_fill_t<2, true, false, PI>(A, grid, smem, st);                              \
+    } else if (kr == 4) {                                                                     \
+      if (profreg) launch_fill_t<4, true, true, PI>(A, grid, smem, st);                       \
+      else launch_fill_t<4, true, false, PI>(A, grid, smem, st);                              \
+    } else {                                                                                  \
+      if (profreg) launch_fill_t<8, true, true, PI>(A, grid, smem, st);                       \
+      else launch_fill_t<8, true, false, PI>(A, grid, smem, st);                              \
+    }                                                                                         \
   }                                                                                           \
   template <>                                                                                 \
   void launch_batch_dirs<PI>(const BatchArgs& B, bool profreg, int grid, size_t smem,         \

@@ -89,6 +89,17 @@ def test_empty_and_degenerate(ctx):
     check_pair(ctx, b"A" * 700, b"C" * 300, sc)    # disjoint alphabets
 
 
+@pytest.mark.parametrize("m,n", [(600, 20000), (20000, 600), (3000, 7), (7, 3000)])
+def test_long_thin_and_border_paths(ctx, m, n):
+    """Paths with long horizontal runs inside one strip (unstaged traceback
+    segments) and long vertical runs down column 0 (border moves)."""
+    sc = nwgen.PAPER_DNA
+    check_pair(ctx, b"A" * m, b"C" * n, sc)
+    a, b = _pair(31337 + m, m, n)
+    check_pair(ctx, a, b, sc)
+    check_pair(ctx, a, b, nwgen.Scoring(tie=(3, 2, 1)))
+
+
 def test_golden_worked_grid(ctx):
     sc = nwgen.Scoring(alphabet="ACGTU")
     for tie in ORDERS:
