@@ -245,15 +245,18 @@ class BatchWorkload:
             pairs = nwgen.consecutive_pairs(ss.nseq // 2)
             self.sc = nwgen.PROTEIN_BLOSUM62
             self.flags = nwb.NW_TRACEBACK
+        from paper_2412_21103_b200 import dist as nwdist
+        self.nwdist = nwdist
         lens = ss.lengths()
-        cost = lens[pairs[:, 0]].astype(np.int64) * lens[pairs[:, 1]]
+        cost = nwdist.pair_costs(lens, pairs)
         self.total_cells = int(cost.sum())
-        # cost-balanced shard: LPT deal of pairs (sorted by cost) over ranks
+        self.npairs_total = len(pairs)
+        # cost-balanced shard of the pair list over ranks (reading R18)
         if world > 1:
-            order = np.argsort(-cost, kind="stable")
-            shard = order[rank::world]
-            pairs_r = pairs[np.sort(shard)]
+            self.shard = nwdist.partition_pairs(cost, world)[rank]
+            pairs_r = pairs[self.shard]
         else:
+            self.shard = None
             pairs_r = pairs if workload == "c4" else None
         self.ss = ss
         self.h_pairs = pairs_r
@@ -263,10 +266,7 @@ class BatchWorkload:
         self.d_seqs = torch.from_numpy(ss.residues).cuda()
         self.d_offs = torch.from_numpy(ss.offs).cuda()
         self.d_pairs = None if pairs_r is None else torch.from_numpy(pairs_r).cuda()
-        # padded to the largest shard so the score all-gather has equal-sized parts
-        self.shard_cap = -(-len(pairs) // world)
-        self.d_scores = torch.zeros(max(self.shard_cap, self.npairs), dtype=torch.int32,
-                                    device="cuda")
+        self.d_scores = torch.zeros(max(self.npairs, 1), dtype=torch.int32, device="cuda")
         if self.flags:
             oo = nwb.nw_batch_ops_offsets(ss.offs, pairs_r)
             self.d_ops_off = torch.from_numpy(oo).cuda()
@@ -274,11 +274,7 @@ class BatchWorkload:
             self.d_ops_len = torch.zeros(self.npairs, dtype=torch.int32, device="cuda")
         else:
             self.d_ops_off = self.d_ops = self.d_ops_len = None
-        if world > 1:
-            import torch.distributed as dist
-            self.dist = dist
-            self.gathered = torch.empty(world * self.d_scores.numel(), dtype=torch.int32,
-                                        device="cuda")
+
 
     def step(self):
         self.nwb.nw_align_batch_dev(self.ctx, self.d_seqs, self.d_offs, self.ss.offs, self.d_pairs,
@@ -286,7 +282,8 @@ class BatchWorkload:
                                     self.d_ops_off, self.d_ops, self.d_ops_len)
         if self.world > 1:
             # P:131 "gathered back in the main process": every rank gets every shard's scores
-            self.dist.all_gather_into_tensor(self.gathered, self.d_scores)
+            self.full = self.nwdist.gather_scores(self.d_scores, self.shard, self.npairs_total,
+                                                  self.world)
 
     def step_host(self):
         r = self.nwb.nw_align_batch(self.ctx, self.ss.residues, self.ss.offs, self.h_pairs, self.sc,

@@ -267,15 +267,17 @@ int choose_kr(long long m, long long n, bool dirs) {
   }
   (void)n;
   (void)dirs;
-  if (m >= 32 * 8 * 592) return 8;  // enough strips for every SMSP at KR = 8
-  if (m >= 32 * 4 * 300) return 4;
+  // the largest KR that still gives about one strip per SM (measured on B200:
+  // 20k x 20k best at 4, 80k x 2k at 8, 2k x 80k at 2; profiles/r01_exp_fill.json)
+  for (int k : {8, 4}) if (m >= 32LL * k * 150) return k;
   return 2;
 }
 
-bool dispatch_batch(bool dirs, int pi, bool profreg, const BatchArgs& B, int grid, size_t smem,
-                    cudaStream_t st) {
+bool dispatch_batch(bool dirs, int pi, bool profreg, bool u16, const BatchArgs& B, int grid,
+                    size_t smem, cudaStream_t st) {
   if (!dirs) {
-    if (profreg) launch_batch_t<KR_BATCH, false, true, 123>(B, grid, smem, st);
+    if (u16) launch_batch_t<KR_BATCH, false, true, 123, true>(B, grid, smem, st);
+    else if (profreg) launch_batch_t<KR_BATCH, false, true, 123>(B, grid, smem, st);
     else launch_batch_t<KR_BATCH, false, false, 123>(B, grid, smem, st);
     return true;
   }
@@ -755,8 +757,9 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   if (st) return st;
   st = init_small(c, 4);
   if (st) return st;
-  // codes buffer: PAD | codes | R + PAD
-  const long long lc = PAD + total + R + PAD;
+  // codes buffer: PAD | codes | tail: the sweeps read up to one strip of rows
+  // (512 for the packed sweep) and ~94 columns past a sequence's end
+  const long long lc = PAD + total + 512 + 2 * PAD;
   st = grow(c, c->d_codes, c->codes_cap, (size_t)lc);
   if (st) return st;
   CUDA_TRY(c, cudaMemsetAsync(c->d_codes, 0, (size_t)lc, c->stream));
@@ -831,10 +834,23 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
     return fail(c, NW_E_NOMEM, "batch scratch");
   const int grid = (int)(nwarps / warps_per_cta);
   const int pi = tbk ? pi_code(sc->tie) : 123;
+  // packed 16-bit sweep (score-only DNA-size alphabets) when s' = s - 2g >= 0 and
+  // min(m,n) * max(s') <= 65535 for every pair (bounded by the longest sequence)
+  bool u16 = false;
+  if (!tbk && profreg && !getenv("NW_NO_U16")) {
+    int smin = 1 << 30, smax = -(1 << 30);
+    for (int x = 0; x < sc->K; ++x)
+      for (int y = 0; y < sc->K; ++y) {
+        const int v = score_of(sc, x, y) - 2 * sc->gap;
+        smin = std::min(smin, v);
+        smax = std::max(smax, v);
+      }
+    u16 = smin >= 0 && smax <= 127 && (long long)maxlen * smax <= 65535;
+  }
   bool ok;
   {
     KernelTimer kt(c, 0);
-    ok = dispatch_batch(tbk, pi, profreg, B, grid, smem, c->stream);
+    ok = dispatch_batch(tbk, pi, profreg, u16, B, grid, smem, c->stream);
   }
   if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
   LAUNCHED(c);

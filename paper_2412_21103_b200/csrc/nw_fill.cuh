@@ -177,7 +177,7 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
     uint32_t sel = 0;
     uint2 pw = make_uint2(0, 0);
     if (PROFREG) {
-      sel = bc * 0x1111u | 0x8880u;  // byte bc, sign-replicated into bytes 1..3
+      sel = bc * 0x1111u + 0x8880u;  // byte bc, sign-replicated into bytes 1..3 (bc < 8: no carry)
     } else if (KR == 8) {
       pw = *reinterpret_cast<const uint2*>(C.sprof + bc * R + lane * KR);
     } else if (KR == 4) {

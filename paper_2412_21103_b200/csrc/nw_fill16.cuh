@@ -1,0 +1,158 @@
+// nw_fill16.cuh -- packed u16x2 score-only sweep.
+//
+// Same recurrence as nw_fill.cuh (Eq. 1, in the shifted form
+// H' = H - g(i+j) with H' >= 0), two cells per 32-bit register: lane l owns
+// KR = 2h rows; packed register k holds row k in its low half and row k+h in
+// its high half, and the high ("bottom") half runs one column behind the low
+// ("top") half:
+//
+//   step t, lane l:  low half at column jT = t - 2l + 1,  high half at jB = jT - 1
+//
+// so the two halves of every register are independent cells and one DPX
+// instruction updates both:
+//   up(k)   = packed k-1 of this step (k >= 1); for k = 0 the low half is the
+//             bottom row of lane l-1 (shuffled, one step old) and the high half
+//             is this lane's packed h-1 low half of the previous step
+//   left(k) = packed k of the previous step, diag(k) = up(k) of the previous step
+//   H'      = VIMNMX.U16x2(VIADDMNMX.U16x2(diag, s', left), up)
+// Lanes are therefore skewed by two steps. Valid when s' = s - 2g >= 0 and
+// min(m,n) * max(s') <= 65535 (the host checks; otherwise the int32 sweep runs).
+#pragma once
+#include "nw_fill.cuh"
+
+namespace nwk {
+
+__device__ __forceinline__ uint32_t prmt2(uint32_t x, uint32_t y, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(y), "r"(sel));
+  return d;
+}
+
+struct U16State {
+  uint32_t up0_prev;  // up(0) of the previous step (diag of packed 0)
+  uint32_t send;      // packed h-1 (its high half = this lane's bottom row at jB)
+  uint32_t xT_prev;   // 17 * b code at the previous step's jT (this step's jB)
+  int chunk;          // boundary values, lane q holds column t0+1+q
+};
+
+// One 32-step block (t0 % 32 == 0). MASKED blocks contain a half outside
+// [1, n] for some lane, or the H'(m, n) cell.
+template <int KR, bool MASKED>
+__device__ __forceinline__ void u16_block(U16State& st, uint32_t (&PA)[KR / 2],
+                                          uint32_t (&PB)[KR / 2], uint32_t (&Hp)[KR / 2],
+                                          const FillArgs& A, int lane, int t0, int* bnd_out,
+                                          int hm_lane, int hm_k, int hm_hi, int hm_t) {
+  constexpr int H = KR / 2;
+  const int n = A.n;
+  const uint8_t* bp = A.b + (t0 - 2 * lane);  // b code at jT - 1 for step t0
+  int* op = bnd_out + (t0 - 62);             // lane 31's bottom row column jB = t - 62
+#pragma unroll 8
+  for (int q = 0; q < 32; ++q) {
+    const int t = t0 + q;
+    const uint32_t bT = bp[q];
+    // s' selector: nibbles (bT, bT|8, 4+bB, 12+bB) -> byte bT of PA zero-extended into
+    // the low half, byte bB of PB into the high half (s' >= 0: sign replication = 0x00);
+    // (c | (c|8)<<4) = 17c + 128 and (4+c | (12+c)<<4) = 17c + 196 for c < 4
+    const uint32_t xT = bT * 17u;
+    const uint32_t sel = xT + (st.xT_prev << 8) + (128u + (196u << 8));
+    st.xT_prev = xT;
+    const int recv = __shfl_up_sync(FULL, (int)st.send, 1);
+    const int bval = __shfl_sync(FULL, st.chunk, q);
+    // up(0): low = lane l-1's bottom row at jT (its packed h-1 high half),
+    //        high = own packed h-1 low half from the previous step
+    const uint32_t upsrc = (lane == 0) ? ((uint32_t)bval << 16) : (uint32_t)recv;
+    uint32_t up = prmt2(upsrc, Hp[H - 1], 0x5432u);
+    uint32_t diag = st.up0_prev;
+    st.up0_prev = up;
+    uint32_t mask = 0xffffffffu;
+    int jT = 0;
+    if (MASKED) {  // low half active iff jT >= 1, high half iff jB = jT - 1 >= 1
+      jT = t - 2 * lane + 1;
+      mask = (jT >= 1 ? 0x0000ffffu : 0u) | (jT >= 2 ? 0xffff0000u : 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      const uint32_t sp = prmt2(PA[k], PB[k], sel);
+      const uint32_t left = Hp[k];
+      uint32_t h = __vmaxu2(__viaddmax_u16x2(diag, sp, left), up);
+      if (MASKED) h &= mask;  // border column H'(i, 0) = 0 until each half starts
+      diag = left;
+      up = h;
+      Hp[k] = h;
+    }
+    st.send = Hp[H - 1];
+    if (MASKED) {
+      const int jB = jT - 1;
+      if (lane == 31 && jB >= 1 && jB <= n) op[q] = (int)(st.send >> 16);
+      if (lane == hm_lane && t == hm_t) {
+#pragma unroll
+        for (int k = 0; k < H; ++k)
+          if (k == hm_k) *A.hm = (int)(hm_hi ? (Hp[k] >> 16) : (Hp[k] & 0xffffu));
+      }
+    } else {
+      if (lane == 31) op[q] = (int)(st.send >> 16);
+    }
+  }
+}
+
+// One strip, score-only, packed. Same FillArgs / boundary conventions as
+// strip_sweep<..., MULTIWARP = false> (the batch kernel's per-warp strips).
+template <int KR>
+__device__ __forceinline__ void strip_sweep_u16(const FillArgs& A, int s, int lane) {
+  static_assert(KR % 2 == 0 && KR <= 16, "KR must be even");
+  constexpr int H = KR / 2;
+  constexpr int R = 32 * KR;
+  const int n = A.n;
+  const int ia0 = s * R + lane * KR;
+  // profiles: PA[k] bytes = s'(a_{k}, c), PB[k] bytes = s'(a_{k+h}, c), c < K <= 4
+  uint32_t PA[H], PB[H], Hp[H];
+#pragma unroll
+  for (int k = 0; k < H; ++k) {
+    const int a0 = A.a[ia0 + k], a1 = A.a[ia0 + k + H];
+    uint32_t w0 = 0, w1 = 0;
+    for (int c = 0; c < A.K; ++c) {
+      w0 |= ((uint32_t)(uint8_t)A.prof[a0 * A.K + c]) << (8 * c);
+      w1 |= ((uint32_t)(uint8_t)A.prof[a1 * A.K + c]) << (8 * c);
+    }
+    PA[k] = w0;
+    PB[k] = w1;
+    Hp[k] = 0;
+  }
+  const int* bnd_in = (s > 0) ? static_cast<const int*>(A.bnd) + (size_t)(s % A.nslots) * A.bstride : nullptr;
+  int* bnd_out = static_cast<int*>(A.bnd) + (size_t)((s + 1) % A.nslots) * A.bstride;
+  // where H'(m, n) lives: row rr of this strip -> lane, packed k, half; column n
+  int hm_lane = -1, hm_k = 0, hm_hi = 0, hm_t = 0;
+  if ((A.m - 1) / R == s) {
+    const int rr = (A.m - 1) % R;
+    hm_lane = rr / KR;
+    const int r = rr % KR;
+    hm_hi = r >= H;
+    hm_k = hm_hi ? r - H : r;
+    hm_t = n - 1 + 2 * hm_lane + hm_hi;  // jT = n (low) or jB = n (high)
+  }
+  U16State st;
+  st.up0_prev = 0;
+  st.send = 0;
+  st.xT_prev = 0;
+  st.chunk = 0;
+  // boundary values H'(top-1, jT) for lane 0's columns t0+1 .. t0+32 (lane q: t0+1+q),
+  // fetched one block ahead; strip 0's top row is H'(0, j) = 0
+  int chunk_nxt = 0;
+  if (s > 0) chunk_nxt = (lane + 1 <= n) ? bnd_in[lane + 1] : 0;
+  const int nsteps = n + 63;  // last lane's high half reaches column n at t = n + 62
+  for (int t0 = 0; t0 < nsteps; t0 += 32) {
+    st.chunk = chunk_nxt;
+    if (s > 0) {
+      const int jj = t0 + 33 + lane;
+      chunk_nxt = (jj <= n) ? bnd_in[jj] : 0;
+    }
+    const bool masked = t0 < 64 || t0 + 31 >= n - 1;
+    if (masked)
+      u16_block<KR, true>(st, PA, PB, Hp, A, lane, t0, bnd_out, hm_lane, hm_k, hm_hi, hm_t);
+    else
+      u16_block<KR, false>(st, PA, PB, Hp, A, lane, t0, bnd_out, hm_lane, hm_k, hm_hi, hm_t);
+  }
+  __syncwarp();
+}
+
+}  // namespace nwk

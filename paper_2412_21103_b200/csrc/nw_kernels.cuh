@@ -11,6 +11,7 @@
 //               optional per-pair traceback by the same warp
 #pragma once
 #include "nw_fill.cuh"
+#include "nw_fill16.cuh"
 
 namespace nwk {
 
@@ -274,7 +275,9 @@ __device__ __forceinline__ void unrank_pair(long long k, int N, int& p, int& q) 
   q = (int)(k - off(pp) + pp + 1);
 }
 
-template <int KR, bool DIRS, bool PROFREG, int PI>
+// U16 (score-only, K <= 4, bounded scores): the packed half-row sweep of
+// nw_fill16.cuh with KR16 rows per lane instead of the int32 strip_sweep.
+template <int KR, bool DIRS, bool PROFREG, int PI, bool U16 = false, int KR16 = 16>
 __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
   constexpr int R = 32 * KR;
   extern __shared__ __align__(16) int8_t smem[];
@@ -309,12 +312,18 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
     if (m > 0 && n > 0) {
       FillArgs A;
       A.a = B.codes + ao; A.b = B.codes + bo; A.prof = B.prof; A.K = B.K;
-      A.m = m; A.n = n; A.nstrips = (m + R - 1) / R; A.nslots = 2;
+      constexpr int RS = U16 ? 32 * KR16 : R;  // strip height of the sweep in use
+      A.m = m; A.n = n; A.nstrips = (m + RS - 1) / RS; A.nslots = 2;
       A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr; A.ebnd = nullptr; A.em = nullptr;
       A.dirs = wd;
       A.wpl = (n + 31 + 7) / 8;  // 8-step groups per strip
       A.hm = B.whm + gw; A.err = B.err;
-      for (int s = 0; s < A.nstrips; ++s) strip_sweep<KR, DIRS, PROFREG, PI, false, false>(A, s, lane, sprof);
+      if constexpr (U16) {
+        for (int s = 0; s < A.nstrips; ++s) strip_sweep_u16<KR16>(A, s, lane);
+      } else {
+        for (int s = 0; s < A.nstrips; ++s)
+          strip_sweep<KR, DIRS, PROFREG, PI, false, false>(A, s, lane, sprof);
+      }
       __syncwarp();
       hmv = *(volatile int*)(B.whm + gw);
       if (DIRS) {

@@ -24,9 +24,9 @@ void launch_fill_t(const FillArgs& A, int grid, size_t smem, cudaStream_t st) {
   k<<<grid, 32, smem, st>>>(A);
 }
 
-template <int KR, bool DIRS, bool PROFREG, int PI>
+template <int KR, bool DIRS, bool PROFREG, int PI, bool U16 = false>
 void launch_batch_t(const BatchArgs& B, int grid, size_t smem, cudaStream_t st) {
-  auto k = k_batch<KR, DIRS, PROFREG, PI>;
+  auto k = k_batch<KR, DIRS, PROFREG, PI, U16>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<grid, 128, smem, st>>>(B);
 }

@@ -182,6 +182,30 @@ def test_batch_all_pairs_dna(ctx):
     assert got.tolist() == want.tolist()
 
 
+@pytest.mark.parametrize("lo,hi,sc", [
+    (0, 700, nwgen.Scoring(match=2, mismatch=-5, gap=-2)),   # s - 2g < 0: int32 sweep
+    (1, 3000, nwgen.Scoring(match=0, mismatch=-1, gap=-1)),  # edit-distance scoring, packed
+    (5000, 9000, nwgen.PAPER_DNA),                           # long rows, packed (H' <= 27000)
+])
+def test_batch_score_paths(ctx, lo, hi, sc):
+    ss = nwgen.random_set(34 + lo, 7, lo, hi)
+    pairs = nwgen.all_pairs(ss.nseq)
+    want = oracle.batch_score(ss.residues, ss.offs, pairs, sc)
+    got = nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc)
+    assert got.tolist() == want.tolist()
+    got2 = nwb.nw_align_batch(ctx, ss.residues, ss.offs, pairs[:, ::-1].copy(), sc)
+    assert got2.tolist() == want.tolist()
+
+
+def test_batch_packed_bound_fallback(ctx):
+    """maxlen * max(s') > 65535 must take the int32 sweep (bit-exact either way)."""
+    ss = nwgen.random_set(35, 3, 30000, 30500)
+    pairs = nwgen.all_pairs(ss.nseq)
+    want = oracle.batch_score(ss.residues, ss.offs, pairs, nwgen.PAPER_DNA)
+    got = nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, nwgen.PAPER_DNA)
+    assert got.tolist() == want.tolist()
+
+
 def test_batch_explicit_pairs_traceback_protein(ctx):
     ss = nwgen.random_set(32, 60, 0, 600, nwgen.PROTEIN)
     rng = np.random.Generator(np.random.PCG64(9))
