@@ -289,7 +289,8 @@ class BatchWorkload:
         r = self.nwb.nw_align_batch(self.ctx, self.ss.residues, self.ss.offs, self.h_pairs, self.sc,
                                     self.flags)
         if self.flags:
-            return r[0].nbytes + sum(len(p) for p in r[1])
+            scores, ops, ops_off, ops_len = r
+            return scores.nbytes + ops.nbytes + ops_len.nbytes
         return r.nbytes
 
     @property

@@ -148,6 +148,17 @@ nw_status nw_align_batch_dev(nw_ctx *ctx, const uint8_t *d_seqs, const int64_t *
 nw_status nw_batch_ops_offsets(const int64_t *h_offs, int32_t nseq, const int32_t *h_pairs,
                                int64_t npairs, int64_t *ops_off);
 
+/* ---- column-block wavefront (giant pair across ranks) ----
+ * Score-only H(m,n) computed as the multi-GPU pipeline computes it: columns cut
+ * into blocks of block_cols (0 = automatic), block b owned by rank b % ranks,
+ * strips handed down within a rank and each strip's right boundary column handed
+ * to the next rank as tagged 64-bit entries. Here all `ranks` are virtual ranks
+ * on this context's device (one launch, all warps resident); the result equals
+ * nw_score_only's. Host pointers, synchronous. DNA-size alphabets (K <= 4). */
+nw_status nw_score_only_cblock(nw_ctx *ctx, const uint8_t *a, int64_t m, const uint8_t *b,
+                               int64_t n, const nw_scoring *sc, int32_t ranks,
+                               int32_t block_cols, int64_t *score);
+
 /* Wait for the context's stream and report any deferred device-side error
  * (alphabet violations, watchdog) raised by earlier _dev calls. */
 nw_status nw_ctx_sync(nw_ctx *ctx);

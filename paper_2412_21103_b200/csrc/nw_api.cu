@@ -715,6 +715,72 @@ nw_status nw_traceback_dev(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops, int64_t c
   return NW_OK;
 }
 
+nw_status nw_score_only_cblock(nw_ctx* c, const uint8_t* a, int64_t m, const uint8_t* b,
+                               int64_t n, const nw_scoring* sc, int32_t ranks,
+                               int32_t block_cols, int64_t* score) {
+  if (!c) return NW_E_INVAL;
+  if ((m > 0 && !a) || (n > 0 && !b) || !score) return fail(c, NW_E_INVAL, "NULL argument");
+  nw_status st = check_scoring(c, sc);
+  if (st) return st;
+  st = check_bounds(c, sc, m, n);
+  if (st) return st;
+  if (sc->K > 4) return fail(c, NW_E_INVAL, "column-block path supports K <= 4");
+  if (ranks < 1 || ranks > 64) return fail(c, NW_E_INVAL, "ranks %d outside [1,64]", ranks);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  st = upload_tables(c, sc);
+  if (st) return st;
+  constexpr int KR = 8, R = 32 * KR;
+  const long long S = std::max<long long>((m + R - 1) / R, 1);
+  int W = block_cols > 0 ? block_cols : (int)std::max<long long>(256, (n + 4 * ranks - 1) / (4 * ranks));
+  const long long nblocks = std::max<long long>((n + W - 1) / W, 1);
+  const long long la = pad16(PAD + m + R_MAX + PAD), lb = pad16(PAD + n + R_MAX + PAD);
+  st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
+  if (st) return st;
+  const long long bstride = bnd_stride(n);
+  const long long rstride = S * (R + 1);
+  const size_t b_bnd = sizeof(unsigned long long) * (size_t)ranks * 2 * bstride;
+  const size_t b_recv = sizeof(unsigned long long) * (size_t)ranks * 2 * rstride;
+  void* buf = nullptr;
+  CUDA_TRY(c, cudaMallocAsync(&buf, b_bnd + b_recv, c->stream));
+  ZeroRanges zr{{c->d_codes, buf, nullptr, nullptr},
+                {la + lb, (long long)((b_bnd + b_recv + 15) & ~size_t(15)), 0, 0}};
+  st = init_small(c, 4 + ranks, zr);
+  if (st) { cudaFreeAsync(buf, c->stream); return st; }
+  uint8_t *ca, *cb;
+  st = stage_pair(c, a, m, b, n, true, &ca, &cb);
+  if (st) { cudaFreeAsync(buf, c->stream); return st; }
+  if (m > 0 && n > 0) {
+    CBlockArgs A;
+    A.a = ca; A.b = cb; A.prof = c->d_prof; A.K = sc->K; A.m = (int)m; A.n = (int)n;
+    A.W = W; A.G = ranks; A.S = (int)S; A.nblocks = (int)nblocks;
+    A.bnd = static_cast<unsigned long long*>(buf);
+    A.bstride = bstride;
+    A.recv = reinterpret_cast<unsigned long long*>(static_cast<char*>(buf) + b_bnd);
+    A.rstride = rstride;
+    A.ticket = c->d_ints + 4;
+    A.hm = c->d_ints + 2;
+    A.err = c->d_ints + 1;
+    A.rank0 = 0;
+    A.nranks_here = ranks;
+    // every virtual rank's warps must be resident at once (they wait on each other)
+    const int grid = (int)std::min<long long>((long long)c->sm_count * 8, S * ranks);
+    const int grid_r = std::max(ranks, grid - grid % ranks);
+    {
+      KernelTimer kt(c, 0);
+      k_fill_cblock<KR><<<grid_r, 32, 0, c->stream>>>(A);
+    }
+    LAUNCHED(c);
+    CUDA_TRY(c, cudaGetLastError());
+  }
+  k_finish_score<<<1, 1, 0, c->stream>>>(c->d_ints + 2, (long long)sc->gap * (m + n), c->d_score,
+                                         (m == 0 || n == 0) ? 1 : 0);
+  LAUNCHED(c);
+  CUDA_TRY(c, cudaMemcpyAsync(score, c->d_score, sizeof(long long), cudaMemcpyDeviceToHost,
+                              c->stream));
+  cudaFreeAsync(buf, c->stream);
+  return check_deferred(c);
+}
+
 nw_status nw_batch_ops_offsets(const int64_t* h_offs, int32_t nseq, const int32_t* h_pairs,
                                int64_t npairs, int64_t* ops_off) {
   if (!h_offs || !ops_off || nseq < 0 || npairs < 0) return NW_E_INVAL;

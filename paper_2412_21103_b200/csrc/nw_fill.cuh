@@ -246,12 +246,15 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
       st.esend = st.El[KR - 1];
     }
     if (lane == 31 && (!MASKED || (j >= 1 && j <= n))) {
-      if (MULTIWARP)
-        st_relaxed_u64(static_cast<unsigned long long*>(C.bnd_out) + j,
-                       ((unsigned long long)(unsigned)(C.s + 1) << 32) | (unsigned)st.send);
-      else
-        static_cast<int*>(C.bnd_out)[j] = st.send;
-      if (TBE) C.ebnd_out[j] = st.esend;
+      // lane 31's column is j = t - 30: stores step through the group's base pointers
+      if (MULTIWARP) {
+        unsigned long long v;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "r"(st.send), "r"(C.s + 1));  // (tag << 32) | H'
+        st_relaxed_u64(static_cast<unsigned long long*>(C.bnd_out) + (t0 - 30) + q, v);
+      } else {
+        static_cast<int*>(C.bnd_out)[(t0 - 30) + q] = st.send;
+      }
+      if (TBE) C.ebnd_out[(t0 - 30) + q] = st.esend;
     }
     if (MASKED && lane == C.hm_lane && t == C.hm_t) {
 #pragma unroll

@@ -12,6 +12,7 @@
 #pragma once
 #include "nw_fill.cuh"
 #include "nw_fill16.cuh"
+#include "nw_cblock.cuh"
 
 namespace nwk {
 
@@ -114,7 +115,9 @@ __device__ long long tb_walk(const uint16_t* dirs, long long G, int m, int n, in
   while (i > 0 && j > 0) {
     int kk;
     const long long idx = tb_index<KR>(G, i, j, kk);
-    const int code = tb_decode<KR>(__ldcg(dirs + idx), kk, X, Y, Z);
+    // L1-cached: consecutive steps mostly stay in one 128-byte line (rows r, r+1 of a
+    // group); the lines were written by this warp before __syncwarp, so L1 holds no stale copy
+    const int code = tb_decode<KR>(__ldca(dirs + idx), kk, X, Y, Z);
     rev[k++] = (uint8_t)code;
     i -= (code != 3);
     j -= (code != 2);

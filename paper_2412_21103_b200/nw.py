@@ -71,6 +71,8 @@ def lib() -> ctypes.CDLL:
         "nw_align_batch_dev": ([vp, vp, vp, vp, i32, vp, vp, i64, P(_Scoring), u32, vp, vp, vp,
                                 vp], ctypes.c_int),
         "nw_batch_ops_offsets": ([vp, i32, vp, i64, vp], ctypes.c_int),
+        "nw_score_only_cblock": ([vp, vp, i64, vp, i64, P(_Scoring), i32, i32, P(i64)],
+                                 ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -83,7 +85,8 @@ def lib() -> ctypes.CDLL:
 EXPORTED = ("nw_ctx_create", "nw_ctx_destroy", "nw_strerror", "nw_last_error", "nw_last_bad_pos",
             "nw_ctx_sync", "nw_ctx_launches", "nw_ctx_set_timing", "nw_ctx_kernel_time", "nw_score_only", "nw_score_only_dev",
             "nw_align_pair", "nw_align_pair_dev", "nw_traceback", "nw_traceback_dev",
-            "nw_tb_free", "nw_align_batch", "nw_align_batch_dev", "nw_batch_ops_offsets")
+            "nw_tb_free", "nw_align_batch", "nw_align_batch_dev", "nw_batch_ops_offsets",
+            "nw_score_only_cblock")
 
 
 def _scoring(sc) -> tuple[_Scoring, object]:
@@ -252,8 +255,15 @@ def nw_batch_ops_offsets(offs: np.ndarray, pairs: np.ndarray | None) -> np.ndarr
     return out
 
 
+def batch_paths(ops: np.ndarray, ops_off: np.ndarray, ops_len: np.ndarray) -> list:
+    """Per-pair forward op arrays from nw_align_batch's flat traceback output."""
+    return [ops[ops_off[k]:ops_off[k] + ops_len[k]] for k in range(len(ops_len))]
+
+
 def nw_align_batch(ctx: Context, seqs, offs, pairs, sc, flags: int = NW_SCORE_ONLY):
-    """Host batch. Returns scores (int32[npairs]) or (scores, list of op arrays)."""
+    """Host batch. Returns scores (int32[npairs]); with NW_TRACEBACK returns
+    (scores, ops, ops_off, ops_len): pair k's path is ops[ops_off[k]:ops_off[k]+ops_len[k]]
+    (see batch_paths)."""
     seqs = _host_bytes(seqs)
     offs = np.ascontiguousarray(offs, dtype=np.int64)
     nseq = len(offs) - 1
@@ -277,8 +287,7 @@ def nw_align_batch(ctx: Context, seqs, offs, pairs, sc, flags: int = NW_SCORE_ON
                                     _ptr(ops), _ptr(ops_len)))
     if not tbk:
         return scores
-    paths = [ops[ops_off[k]:ops_off[k] + ops_len[k]].copy() for k in range(npairs)]
-    return scores, paths
+    return scores, ops, ops_off, ops_len[:npairs]
 
 
 def nw_align_batch_dev(ctx: Context, d_seqs, d_offs, h_offs, d_pairs, h_pairs, npairs: int, sc,
@@ -292,3 +301,13 @@ def nw_align_batch_dev(ctx: Context, d_seqs, d_offs, h_offs, d_pairs, h_pairs, n
                                         len(h_offs) - 1, _ptr(d_pairs), _ptr(h_pairs), npairs,
                                         ctypes.byref(s), flags, _ptr(d_scores), _ptr(d_ops_off),
                                         _ptr(d_ops), _ptr(d_ops_len)))
+
+
+def nw_score_only_cblock(ctx: Context, a, b, sc, ranks: int, block_cols: int = 0) -> int:
+    """H(m, n) through the column-block wavefront over `ranks` virtual ranks (a10)."""
+    a, b = _host_bytes(a), _host_bytes(b)
+    s, keep = _scoring(sc)
+    out = ctypes.c_int64()
+    ctx._check(lib().nw_score_only_cblock(ctx.handle, _ptr(a), len(a), _ptr(b), len(b),
+                                          ctypes.byref(s), ranks, block_cols, ctypes.byref(out)))
+    return out.value

@@ -213,7 +213,8 @@ def test_batch_explicit_pairs_traceback_protein(ctx):
     for tie in [(1, 2, 3), (3, 1, 2)]:
         sc = nwgen.Scoring(match=0, mismatch=0, gap=-5, alphabet=nwgen.PROTEIN,
                            subst=nwgen.BLOSUM62, tie=tie)
-        scores, paths = nwb.nw_align_batch(ctx, ss.residues, ss.offs, pairs, sc, nwb.NW_TRACEBACK)
+        scores, *flat = nwb.nw_align_batch(ctx, ss.residues, ss.offs, pairs, sc, nwb.NW_TRACEBACK)
+        paths = nwb.batch_paths(*flat)
         for k, (p, q) in enumerate(pairs):
             ws, wops = oracle.align(ss.seq(p), ss.seq(q), sc)
             assert scores[k] == ws, k
@@ -223,7 +224,8 @@ def test_batch_explicit_pairs_traceback_protein(ctx):
 def test_batch_traceback_dna_all_pairs(ctx):
     ss = nwgen.random_set(33, 25, 1, 400)
     sc = nwgen.PAPER_DNA
-    scores, paths = nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc, nwb.NW_TRACEBACK)
+    scores, *flat = nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc, nwb.NW_TRACEBACK)
+    paths = nwb.batch_paths(*flat)
     for k, (p, q) in enumerate(nwgen.all_pairs(ss.nseq)):
         ws, wops = oracle.align(ss.seq(p), ss.seq(q), sc)
         assert scores[k] == ws and paths[k].tolist() == wops.tolist()
@@ -250,7 +252,8 @@ def test_c4_full_size_sampled(ctx):
     ss = nwgen.config_c4()
     pairs = nwgen.consecutive_pairs(100_000)
     sc = nwgen.PROTEIN_BLOSUM62
-    scores, paths = nwb.nw_align_batch(ctx, ss.residues, ss.offs, pairs, sc, nwb.NW_TRACEBACK)
+    scores, *flat = nwb.nw_align_batch(ctx, ss.residues, ss.offs, pairs, sc, nwb.NW_TRACEBACK)
+    paths = nwb.batch_paths(*flat)
     rng = np.random.Generator(np.random.PCG64(2))
     for k in np.concatenate([rng.integers(0, len(pairs), 60), [0, len(pairs) - 1]]):
         p, q = pairs[k]
@@ -274,3 +277,24 @@ def test_score_only_prefix_and_closed_forms_c5(ctx):
     sc = nwgen.Scoring(match=0, mismatch=-1, gap=-1)
     qa, qb = a[:3000], b[:2900]
     assert nwb.nw_score_only(ctx, qa, qb, sc) == -myers_edit_distance(qa, qb)
+
+
+# ---------------------------------------------------------------- column blocks (a10)
+
+@pytest.mark.parametrize("m,n", [(1, 1), (300, 500), (1000, 5000), (3000, 700), (513, 2049)])
+@pytest.mark.parametrize("ranks,w", [(1, 0), (2, 64), (3, 1000), (8, 0), (5, 257)])
+def test_cblock_virtual_ranks(ctx, m, n, ranks, w):
+    """Column-block wavefront across virtual ranks == oracle score (SURVEY §8(e) C5 path)."""
+    a, b = _pair(7000 + m + n, m, n)
+    sc = nwgen.PAPER_DNA
+    assert nwb.nw_score_only_cblock(ctx, a, b, sc, ranks, w) == oracle.score(a, b, sc)
+
+
+def test_cblock_c5_prefix_and_closed_forms(ctx):
+    a, b = nwgen.config_c5()
+    pa, pb = a[:30000], b[:30000]
+    sc = nwgen.PAPER_DNA
+    assert nwb.nw_score_only_cblock(ctx, pa, pb, sc, 8, 1024) == oracle.score(pa, pb, sc)
+    n = 1_000_000
+    assert nwb.nw_score_only_cblock(ctx, a, a, sc, 8, 0) == n
+    assert nwb.nw_score_only_cblock(ctx, a, b, sc, 4, 0) == nwb.nw_score_only(ctx, a, b, sc)
