@@ -238,7 +238,13 @@ void launch_score(const FillArgs& A, bool profreg, int grid, size_t smem, cudaSt
 }
 
 bool dispatch_fill(bool dirs, int pi, int kr, bool profreg, const FillArgs& A, int grid,
-                   size_t smem, cudaStream_t st) {
+                   size_t smem, cudaStream_t st, bool d16 = false) {
+  if (!dirs && d16) {  // packed difference form, KR rows per lane (2 per register)
+    if (kr == 16) launch_fill_t<16, false, true, 123, true>(A, grid, smem, st);
+    else if (kr == 8) launch_fill_t<8, false, true, 123, true>(A, grid, smem, st);
+    else launch_fill_t<4, false, true, 123, true>(A, grid, smem, st);
+    return true;
+  }
   if (!dirs) {
     if (kr == 2) launch_score<2>(A, profreg, grid, smem, st);
     else if (kr == 4) launch_score<4>(A, profreg, grid, smem, st);
@@ -254,6 +260,16 @@ bool dispatch_fill(bool dirs, int pi, int kr, bool profreg, const FillArgs& A, i
     case 321: launch_fill_dirs<321>(A, kr, profreg, grid, smem, st); return true;
   }
   return false;
+}
+
+// Packed difference form (nw_fill_d16.cuh) applies to score-only DNA-size
+// alphabets with s - 2g >= 0 for every symbol pair.
+bool d16_ok(const nw_scoring* sc) {
+  if (sc->K > 4 || getenv("NW_NO_D16")) return false;
+  for (int x = 0; x < sc->K; ++x)
+    for (int y = 0; y < sc->K; ++y)
+      if (score_of(sc, x, y) - 2 * sc->gap < 0) return false;
+  return true;
 }
 
 // Rows per lane for a single pair: the strip count m/(32 KR)
@@ -273,10 +289,11 @@ int choose_kr(long long m, long long n, bool dirs) {
   return 2;
 }
 
-bool dispatch_batch(bool dirs, int pi, bool profreg, bool u16, const BatchArgs& B, int grid,
-                    size_t smem, cudaStream_t st) {
+bool dispatch_batch(bool dirs, int pi, bool profreg, bool u16, bool d16, const BatchArgs& B,
+                    int grid, size_t smem, cudaStream_t st) {
   if (!dirs) {
-    if (u16) launch_batch_t<KR_BATCH, false, true, 123, true>(B, grid, smem, st);
+    if (u16) launch_batch_t<KR_BATCH, false, true, 123, 1>(B, grid, smem, st);
+    else if (d16) launch_batch_t<KR_BATCH, false, true, 123, 2>(B, grid, smem, st);
     else if (profreg) launch_batch_t<KR_BATCH, false, true, 123>(B, grid, smem, st);
     else launch_batch_t<KR_BATCH, false, false, 123>(B, grid, smem, st);
     return true;
@@ -351,6 +368,7 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     A.hm = hm; A.em = dirs ? tb->em : em; A.err = errf;
     const bool profreg = sc->K <= 4;
     const size_t smem = profreg ? 0 : (size_t)sc->K * R;
+    const bool d16 = !dirs && kr == 16;
     // persistent grid: one warp per CTA, at most the resident capacity
     int per_sm = 16;
     int grid = std::min<long long>(nstrips, (long long)c->sm_count * per_sm);
@@ -358,7 +376,7 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     bool ok;
     {
       KernelTimer kt(c, 0);
-      ok = dispatch_fill(dirs, pi, kr, profreg, A, grid, smem, c->stream);
+      ok = dispatch_fill(dirs, pi, kr, profreg, A, grid, smem, c->stream, d16);
     }
     if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
     LAUNCHED(c);
@@ -463,7 +481,12 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
   // workspace: padded code buffers and the tagged 2-slot boundary ring
   constexpr long long R = R_MAX;
   const long long la = pad16(PAD + m + R + PAD), lb = pad16(PAD + n + R + PAD);
-  const int kr = choose_kr(m, n, want_dirs);
+  int kr = choose_kr(m, n, want_dirs);
+  // packed difference form (two rows per register) for tall score-only pairs: it
+  // halves the ALU work per cell but doubles the lane skew, so it only pays when
+  // there are enough 512-row strips to fill the GPU (measured: 1M^2 2.4 -> 5.9
+  // TCUPS; 20k^2 1.44 -> 2.14 ms, slower)
+  if (!want_dirs && d16_ok(sc) && m >= 32LL * 16 * 150) kr = 16;
   st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
   if (st) return st;
   const long long bbytes = (long long)sizeof(unsigned long long) * 2 * bnd_stride(n);
@@ -902,21 +925,18 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   const int pi = tbk ? pi_code(sc->tie) : 123;
   // packed 16-bit sweep (score-only DNA-size alphabets) when s' = s - 2g >= 0 and
   // min(m,n) * max(s') <= 65535 for every pair (bounded by the longest sequence)
-  bool u16 = false;
-  if (!tbk && profreg && !getenv("NW_NO_U16")) {
-    int smin = 1 << 30, smax = -(1 << 30);
-    for (int x = 0; x < sc->K; ++x)
-      for (int y = 0; y < sc->K; ++y) {
-        const int v = score_of(sc, x, y) - 2 * sc->gap;
-        smin = std::min(smin, v);
-        smax = std::max(smax, v);
-      }
-    u16 = smin >= 0 && smax <= 127 && (long long)maxlen * smax <= 65535;
-  }
+  // packed score-only sweeps: the H' form when every H' fits 16 bits (measured
+  // faster on C3), else the difference form (any length); both need s - 2g >= 0
+  const bool packed = !tbk && profreg && d16_ok(sc);
+  int smax = 0;
+  for (int x = 0; x < sc->K; ++x)
+    for (int y = 0; y < sc->K; ++y) smax = std::max(smax, score_of(sc, x, y) - 2 * sc->gap);
+  const bool u16 = packed && (long long)maxlen * smax <= 65535;
+  const bool d16 = packed && !u16;
   bool ok;
   {
     KernelTimer kt(c, 0);
-    ok = dispatch_batch(tbk, pi, profreg, u16, B, grid, smem, c->stream);
+    ok = dispatch_batch(tbk, pi, profreg, u16, d16, B, grid, smem, c->stream);
   }
   if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
   LAUNCHED(c);

@@ -39,6 +39,9 @@ namespace nwk {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int PAD = 64;  // code buffers carry PAD readable bytes before and after
+#ifndef NW_POLL_SLEEP_NS
+#define NW_POLL_SLEEP_NS 0
+#endif
 
 struct FillArgs {
   const uint8_t* a;    // row codes, a[-PAD .. m+PAD) readable
@@ -146,14 +149,17 @@ __device__ __forceinline__ int chunk_verify(const StripCtx& C, int c0, unsigned 
   bool ok = !need || (unsigned)(v >> 32) == tag;
   if (__all_sync(FULL, ok)) return (int)(unsigned)v;
   const unsigned long long* p = static_cast<const unsigned long long*>(C.bnd_in) + jj;
+  // re-poll without sleeping: the waiting warp is usually alone on its SM
+  // sub-partition (one strip per warp), and a sleep adds its whole granularity
+  // to every strip-to-strip hand-off (NW_POLL_SLEEP_NS > 0 restores backoff)
   for (long long it = 0;; ++it) {
-    __nanosleep(20);
+    if (NW_POLL_SLEEP_NS > 0) __nanosleep(NW_POLL_SLEEP_NS);
     if (!ok) {
       v = ld_relaxed_u64(p);
       ok = (unsigned)(v >> 32) == tag;
     }
     if (__all_sync(FULL, ok)) break;
-    if (it > (1ll << 26)) {  // watchdog: report and stop waiting (results invalid)
+    if (it > (1ll << 28)) {  // watchdog: report and stop waiting (results invalid)
       if (C.lane == 0) atomicExch(C.err, 8);
       break;
     }

@@ -13,6 +13,7 @@
 #include "nw_fill.cuh"
 #include "nw_fill16.cuh"
 #include "nw_cblock.cuh"
+#include "nw_fill_d16.cuh"
 
 namespace nwk {
 
@@ -73,7 +74,9 @@ __global__ void k_encode(const uint8_t* __restrict__ in, long long len,
 
 // One pair, one strip per warp at a time; strips handed out in order by an
 // atomic ticket so every awaited producer is already resident (no deadlock).
-template <int KR, bool DIRS, bool PROFREG, int PI>
+// D16 (score-only, K <= 4, s - 2g >= 0): the packed difference-form sweep of
+// nw_fill_d16.cuh (KR rows per lane, two per register) instead of strip_sweep.
+template <int KR, bool DIRS, bool PROFREG, int PI, bool D16 = false>
 __global__ void __launch_bounds__(32) k_fill_pair(FillArgs A) {
   extern __shared__ __align__(16) int8_t smem[];
   const int lane = threadIdx.x & 31;
@@ -82,7 +85,8 @@ __global__ void __launch_bounds__(32) k_fill_pair(FillArgs A) {
     if (lane == 0) s = atomicAdd(A.ticket, 1);
     s = __shfl_sync(FULL, s, 0);
     if (s >= A.nstrips) break;
-    strip_sweep<KR, DIRS, PROFREG, PI, true, DIRS>(A, s, lane, smem);
+    if constexpr (D16) strip_sweep_d16<KR, true>(A, s, lane);
+    else strip_sweep<KR, DIRS, PROFREG, PI, true, DIRS>(A, s, lane, smem);
   }
 }
 
@@ -278,9 +282,10 @@ __device__ __forceinline__ void unrank_pair(long long k, int N, int& p, int& q) 
   q = (int)(k - off(pp) + pp + 1);
 }
 
-// U16 (score-only, K <= 4, bounded scores): the packed half-row sweep of
-// nw_fill16.cuh with KR16 rows per lane instead of the int32 strip_sweep.
-template <int KR, bool DIRS, bool PROFREG, int PI, bool U16 = false, int KR16 = 16>
+// PACKED (score-only, K <= 4, s - 2g >= 0), KR16 rows per lane, two per register:
+// 1 = the H' half-row sweep of nw_fill16.cuh (every H' < 2^16),
+// 2 = the difference-form sweep of nw_fill_d16.cuh (any length).
+template <int KR, bool DIRS, bool PROFREG, int PI, int PACKED = 0, int KR16 = 16>
 __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
   constexpr int R = 32 * KR;
   extern __shared__ __align__(16) int8_t smem[];
@@ -315,14 +320,18 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
     if (m > 0 && n > 0) {
       FillArgs A;
       A.a = B.codes + ao; A.b = B.codes + bo; A.prof = B.prof; A.K = B.K;
-      constexpr int RS = U16 ? 32 * KR16 : R;  // strip height of the sweep in use
+      constexpr int RS = PACKED ? 32 * KR16 : R;  // strip height of the sweep in use
       A.m = m; A.n = n; A.nstrips = (m + RS - 1) / RS; A.nslots = 2;
       A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr; A.ebnd = nullptr; A.em = nullptr;
       A.dirs = wd;
       A.wpl = (n + 31 + 7) / 8;  // 8-step groups per strip
       A.hm = B.whm + gw; A.err = B.err;
-      if constexpr (U16) {
+      if constexpr (PACKED == 1) {
         for (int s = 0; s < A.nstrips; ++s) strip_sweep_u16<KR16>(A, s, lane);
+      } else if constexpr (PACKED == 2) {
+        if (lane == 0) *A.hm = 0;  // the difference-form sweep accumulates sum U(i, n)
+        __syncwarp();
+        for (int s = 0; s < A.nstrips; ++s) strip_sweep_d16<KR16, false>(A, s, lane);
       } else {
         for (int s = 0; s < A.nstrips; ++s)
           strip_sweep<KR, DIRS, PROFREG, PI, false, false>(A, s, lane, sprof);

@@ -8,7 +8,7 @@
 namespace nwk {
 
 constexpr int KR_MAX = 8;    // rows per lane: single-pair kernels pick 2, 4 or 8 per shape
-constexpr int R_MAX = 32 * KR_MAX;
+constexpr int R_MAX = 32 * 16;  // tallest strip of any sweep (packed KR = 16): code padding
 constexpr int KR_BATCH = 8;  // rows per lane, batch kernel
 
 // DIRS = true launchers, one instantiation per tie order PI (nw_inst_<PI>.cu)
@@ -17,16 +17,16 @@ void launch_fill_dirs(const FillArgs& A, int kr, bool profreg, int grid, size_t 
 template <int PI>
 void launch_batch_dirs(const BatchArgs& B, bool profreg, int grid, size_t smem, cudaStream_t st);
 
-template <int KR, bool DIRS, bool PROFREG, int PI>
+template <int KR, bool DIRS, bool PROFREG, int PI, bool D16 = false>
 void launch_fill_t(const FillArgs& A, int grid, size_t smem, cudaStream_t st) {
-  auto k = k_fill_pair<KR, DIRS, PROFREG, PI>;
+  auto k = k_fill_pair<KR, DIRS, PROFREG, PI, D16>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<grid, 32, smem, st>>>(A);
 }
 
-template <int KR, bool DIRS, bool PROFREG, int PI, bool U16 = false>
+template <int KR, bool DIRS, bool PROFREG, int PI, int PACKED = 0>
 void launch_batch_t(const BatchArgs& B, int grid, size_t smem, cudaStream_t st) {
-  auto k = k_batch<KR, DIRS, PROFREG, PI, U16>;
+  auto k = k_batch<KR, DIRS, PROFREG, PI, PACKED>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<grid, 128, smem, st>>>(B);
 }

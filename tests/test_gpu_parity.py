@@ -298,3 +298,11 @@ def test_cblock_c5_prefix_and_closed_forms(ctx):
     n = 1_000_000
     assert nwb.nw_score_only_cblock(ctx, a, a, sc, 8, 0) == n
     assert nwb.nw_score_only_cblock(ctx, a, b, sc, 4, 0) == nwb.nw_score_only(ctx, a, b, sc)
+
+
+@pytest.mark.parametrize("m,n", [(100_000, 3000), (80_000, 5), (77_000, 1)])
+def test_score_only_tall_difference_form(ctx, m, n):
+    """Tall score-only pairs take the packed difference-form sweep (nw_fill_d16.cuh)."""
+    a, b = _pair(8000 + n, m, n)
+    for sc in (nwgen.PAPER_DNA, nwgen.Scoring(match=2, mismatch=-1, gap=-3)):
+        assert nwb.nw_score_only(ctx, a, b, sc) == oracle.score(a, b, sc)
