@@ -159,6 +159,20 @@ nw_status nw_score_only_cblock(nw_ctx *ctx, const uint8_t *a, int64_t m, const u
                                int64_t n, const nw_scoring *sc, int32_t ranks,
                                int32_t block_cols, int64_t *score);
 
+/* One real rank of the same pipeline (one process per GPU). recv_self: this rank's
+ * receive buffer of nw_cblock_recv_bytes(m) bytes, device memory the previous rank
+ * can write (e.g. a symmetric-memory / CUDA-IPC peer mapping); recv_next: the next
+ * rank's receive buffer as mapped on this device. Every rank's recv_self must be
+ * zeroed, and that zeroing complete on all ranks, before any rank calls this.
+ * d_a, d_b, d_score device pointers; async on ctx's stream. *d_score receives
+ * H(m,n) on the rank owning the last column block and 0 elsewhere (sum across
+ * ranks = the score). */
+int64_t nw_cblock_recv_bytes(int64_t m);
+nw_status nw_score_only_cblock_rank_dev(nw_ctx *ctx, const uint8_t *d_a, int64_t m,
+                                        const uint8_t *d_b, int64_t n, const nw_scoring *sc,
+                                        int32_t rank, int32_t ranks, int32_t block_cols,
+                                        void *recv_self, void *recv_next, int64_t *d_score);
+
 /* Wait for the context's stream and report any deferred device-side error
  * (alphabet violations, watchdog) raised by earlier _dev calls. */
 nw_status nw_ctx_sync(nw_ctx *ctx);

@@ -738,70 +738,161 @@ nw_status nw_traceback_dev(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops, int64_t c
   return NW_OK;
 }
 
-nw_status nw_score_only_cblock(nw_ctx* c, const uint8_t* a, int64_t m, const uint8_t* b,
-                               int64_t n, const nw_scoring* sc, int32_t ranks,
-                               int32_t block_cols, int64_t* score) {
-  if (!c) return NW_E_INVAL;
-  if ((m > 0 && !a) || (n > 0 && !b) || !score) return fail(c, NW_E_INVAL, "NULL argument");
+}  // extern "C"
+
+namespace {
+
+constexpr int CB_KR = 8, CB_R = 32 * CB_KR;
+
+long long cblock_strips(long long m) { return std::max<long long>((m + CB_R - 1) / CB_R, 1); }
+
+// Shared body of the column-block entry points: ranks [rank0, rank0 + nhere) run
+// in this launch; recv_tab (device, G entries) points at every rank's receive
+// buffer (virtual ranks: all local; a real rank: its own and the next rank's).
+nw_status cblock_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb, long long n,
+                      const nw_scoring* sc, int G, int W, int rank0, int nhere,
+                      unsigned long long* const* recv_tab, long long* d_score, bool owner_adds_gap) {
+  const long long S = cblock_strips(m);
+  const long long nblocks = std::max<long long>((n + W - 1) / W, 1);
+  const long long bstride = bnd_stride(n);
+  const size_t b_bnd = sizeof(unsigned long long) * (size_t)nhere * 2 * bstride;
+  void* ring = nullptr;
+  CUDA_TRY(c, cudaMallocAsync(&ring, b_bnd + 16, c->stream));
+  ZeroRanges zr{{ring, nullptr, nullptr, nullptr}, {(long long)((b_bnd + 15) & ~size_t(15)), 0, 0, 0}};
+  nw_status st = init_small(c, 4 + nhere, zr);
+  if (st) { cudaFreeAsync(ring, c->stream); return st; }
+  const int last_owner = (int)((nblocks - 1) % G);
+  if (m > 0 && n > 0) {
+    CBlockArgs A;
+    A.a = ca; A.b = cb; A.prof = c->d_prof; A.K = sc->K; A.m = (int)m; A.n = (int)n;
+    A.W = W; A.G = G; A.S = (int)S; A.nblocks = (int)nblocks;
+    A.bnd = static_cast<unsigned long long*>(ring);
+    A.bstride = bstride;
+    A.recv_tab = recv_tab;
+    A.rstride = S * (CB_R + 1);
+    A.ticket = c->d_ints + 4;
+    A.hm = c->d_ints + 2;
+    A.err = c->d_ints + 1;
+    A.rank0 = rank0;
+    A.nranks_here = nhere;
+    // every rank's warps must be resident together (they wait on each other);
+    // NW_CBLOCK_WARPS_PER_SM caps this launch's share of the GPU
+    int per_sm = 8;
+    if (const char* e = getenv("NW_CBLOCK_WARPS_PER_SM")) per_sm = std::max(1, atoi(e));
+    const int grid = (int)std::min<long long>((long long)c->sm_count * per_sm, S * nhere);
+    const int grid_r = std::max(nhere, grid - grid % nhere);
+    {
+      KernelTimer kt(c, 0);
+      k_fill_cblock<CB_KR><<<grid_r, 32, 0, c->stream>>>(A);
+    }
+    LAUNCHED(c);
+    CUDA_TRY(c, cudaGetLastError());
+  }
+  const bool owner = rank0 <= last_owner && last_owner < rank0 + nhere;
+  // the owner of the last block reports H(m,n); other real ranks report 0
+  const long long gmn = owner || !owner_adds_gap ? (long long)sc->gap * (m + n) : 0;
+  k_finish_score<<<1, 1, 0, c->stream>>>(c->d_ints + 2, gmn, d_score, (m == 0 || n == 0) ? 1 : 0);
+  LAUNCHED(c);
+  cudaFreeAsync(ring, c->stream);
+  CUDA_TRY(c, cudaGetLastError());
+  return NW_OK;
+}
+
+int cblock_width(long long n, int G, int block_cols) {
+  if (block_cols > 0) return block_cols;
+  return (int)std::max<long long>(256, (n + 4LL * G - 1) / (4LL * G));
+}
+
+nw_status cblock_check(nw_ctx* c, long long m, long long n, const nw_scoring* sc, int G) {
   nw_status st = check_scoring(c, sc);
   if (st) return st;
   st = check_bounds(c, sc, m, n);
   if (st) return st;
   if (sc->K > 4) return fail(c, NW_E_INVAL, "column-block path supports K <= 4");
-  if (ranks < 1 || ranks > 64) return fail(c, NW_E_INVAL, "ranks %d outside [1,64]", ranks);
+  if (G < 1 || G > 64) return fail(c, NW_E_INVAL, "ranks %d outside [1,64]", G);
+  if (cblock_strips(m) >= (1 << 20)) return fail(c, NW_E_OVERFLOW, "too many strips for the tags");
+  return NW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t nw_cblock_recv_bytes(int64_t m) {
+  return (int64_t)sizeof(unsigned long long) * 2 * cblock_strips(m) * (CB_R + 1);
+}
+
+nw_status nw_score_only_cblock(nw_ctx* c, const uint8_t* a, int64_t m, const uint8_t* b,
+                               int64_t n, const nw_scoring* sc, int32_t ranks,
+                               int32_t block_cols, int64_t* score) {
+  if (!c) return NW_E_INVAL;
+  if ((m > 0 && !a) || (n > 0 && !b) || !score) return fail(c, NW_E_INVAL, "NULL argument");
+  nw_status st = cblock_check(c, m, n, sc, ranks);
+  if (st) return st;
   CUDA_TRY(c, cudaSetDevice(c->device));
   st = upload_tables(c, sc);
   if (st) return st;
-  constexpr int KR = 8, R = 32 * KR;
-  const long long S = std::max<long long>((m + R - 1) / R, 1);
-  int W = block_cols > 0 ? block_cols : (int)std::max<long long>(256, (n + 4 * ranks - 1) / (4 * ranks));
-  const long long nblocks = std::max<long long>((n + W - 1) / W, 1);
   const long long la = pad16(PAD + m + R_MAX + PAD), lb = pad16(PAD + n + R_MAX + PAD);
   st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
   if (st) return st;
-  const long long bstride = bnd_stride(n);
-  const long long rstride = S * (R + 1);
-  const size_t b_bnd = sizeof(unsigned long long) * (size_t)ranks * 2 * bstride;
-  const size_t b_recv = sizeof(unsigned long long) * (size_t)ranks * 2 * rstride;
-  void* buf = nullptr;
-  CUDA_TRY(c, cudaMallocAsync(&buf, b_bnd + b_recv, c->stream));
-  ZeroRanges zr{{c->d_codes, buf, nullptr, nullptr},
-                {la + lb, (long long)((b_bnd + b_recv + 15) & ~size_t(15)), 0, 0}};
-  st = init_small(c, 4 + ranks, zr);
+  // virtual ranks: all receive buffers + the pointer table in one allocation
+  const size_t b_recv = (size_t)ranks * (size_t)nw_cblock_recv_bytes(m);
+  const size_t b_tab = sizeof(void*) * (size_t)ranks;
+  char* buf = nullptr;
+  CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&buf), b_recv + b_tab + 16, c->stream));
+  std::vector<unsigned long long*> tab(ranks);
+  for (int r = 0; r < ranks; ++r)
+    tab[r] = reinterpret_cast<unsigned long long*>(buf + (size_t)r * nw_cblock_recv_bytes(m));
+  CUDA_TRY(c, cudaMemcpyAsync(buf + b_recv, tab.data(), b_tab, cudaMemcpyHostToDevice, c->stream));
+  ZeroRanges zr{{c->d_codes, buf, nullptr, nullptr}, {la + lb, (long long)((b_recv + 15) & ~size_t(15)), 0, 0}};
+  st = init_small(c, 4, zr);
   if (st) { cudaFreeAsync(buf, c->stream); return st; }
   uint8_t *ca, *cb;
   st = stage_pair(c, a, m, b, n, true, &ca, &cb);
   if (st) { cudaFreeAsync(buf, c->stream); return st; }
-  if (m > 0 && n > 0) {
-    CBlockArgs A;
-    A.a = ca; A.b = cb; A.prof = c->d_prof; A.K = sc->K; A.m = (int)m; A.n = (int)n;
-    A.W = W; A.G = ranks; A.S = (int)S; A.nblocks = (int)nblocks;
-    A.bnd = static_cast<unsigned long long*>(buf);
-    A.bstride = bstride;
-    A.recv = reinterpret_cast<unsigned long long*>(static_cast<char*>(buf) + b_bnd);
-    A.rstride = rstride;
-    A.ticket = c->d_ints + 4;
-    A.hm = c->d_ints + 2;
-    A.err = c->d_ints + 1;
-    A.rank0 = 0;
-    A.nranks_here = ranks;
-    // every virtual rank's warps must be resident at once (they wait on each other)
-    const int grid = (int)std::min<long long>((long long)c->sm_count * 8, S * ranks);
-    const int grid_r = std::max(ranks, grid - grid % ranks);
-    {
-      KernelTimer kt(c, 0);
-      k_fill_cblock<KR><<<grid_r, 32, 0, c->stream>>>(A);
-    }
-    LAUNCHED(c);
-    CUDA_TRY(c, cudaGetLastError());
-  }
-  k_finish_score<<<1, 1, 0, c->stream>>>(c->d_ints + 2, (long long)sc->gap * (m + n), c->d_score,
-                                         (m == 0 || n == 0) ? 1 : 0);
-  LAUNCHED(c);
+  st = cblock_core(c, ca, m, cb, n, sc, ranks, cblock_width(n, ranks, block_cols), 0, ranks,
+                   reinterpret_cast<unsigned long long* const*>(buf + b_recv), c->d_score, false);
+  if (st) { cudaFreeAsync(buf, c->stream); return st; }
   CUDA_TRY(c, cudaMemcpyAsync(score, c->d_score, sizeof(long long), cudaMemcpyDeviceToHost,
                               c->stream));
   cudaFreeAsync(buf, c->stream);
   return check_deferred(c);
+}
+
+nw_status nw_score_only_cblock_rank_dev(nw_ctx* c, const uint8_t* d_a, int64_t m,
+                                        const uint8_t* d_b, int64_t n, const nw_scoring* sc,
+                                        int32_t rank, int32_t ranks, int32_t block_cols,
+                                        void* recv_self, void* recv_next, int64_t* d_score) {
+  if (!c) return NW_E_INVAL;
+  if ((m > 0 && !d_a) || (n > 0 && !d_b) || !d_score || !recv_self || (ranks > 1 && !recv_next))
+    return fail(c, NW_E_INVAL, "NULL argument");
+  nw_status st = cblock_check(c, m, n, sc, ranks);
+  if (st) return st;
+  if (rank < 0 || rank >= ranks) return fail(c, NW_E_INVAL, "rank %d outside [0,%d)", rank, ranks);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  st = upload_tables(c, sc);
+  if (st) return st;
+  const long long la = pad16(PAD + m + R_MAX + PAD), lb = pad16(PAD + n + R_MAX + PAD);
+  st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
+  if (st) return st;
+  // pointer table: own and next rank's receive buffers (the rest are never read)
+  std::vector<unsigned long long*> tab(ranks, nullptr);
+  tab[rank] = static_cast<unsigned long long*>(recv_self);
+  tab[(rank + 1) % ranks] = static_cast<unsigned long long*>(ranks > 1 ? recv_next : recv_self);
+  unsigned long long** d_tab = nullptr;
+  CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&d_tab), sizeof(void*) * ranks, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(d_tab, tab.data(), sizeof(void*) * ranks, cudaMemcpyHostToDevice,
+                              c->stream));
+  ZeroRanges zr{{c->d_codes, nullptr, nullptr, nullptr}, {la + lb, 0, 0, 0}};
+  st = init_small(c, 4, zr);
+  if (st) { cudaFreeAsync(d_tab, c->stream); return st; }
+  uint8_t *ca, *cb;
+  st = stage_pair(c, d_a, m, d_b, n, false, &ca, &cb);
+  if (st) { cudaFreeAsync(d_tab, c->stream); return st; }
+  st = cblock_core(c, ca, m, cb, n, sc, ranks, cblock_width(n, ranks, block_cols), rank, 1,
+                   d_tab, reinterpret_cast<long long*>(d_score), true);
+  cudaFreeAsync(d_tab, c->stream);
+  return st;
 }
 
 nw_status nw_batch_ops_offsets(const int64_t* h_offs, int32_t nseq, const int32_t* h_pairs,

@@ -34,8 +34,10 @@ struct CBlockArgs {
   // per-rank state (indexed by rank for virtual ranks; real ranks pass their own at index 0)
   unsigned long long* bnd;   // [ranks][2][n + 1 + 64] tagged top/bottom rows (column-indexed)
   long long bstride;
-  unsigned long long* recv;  // [ranks][2][S][R + 1] tagged left columns (block-slot k % 2)
-  long long rstride;         // entries per (rank, slot) = S * (R + 1)
+  unsigned long long* const* recv_tab;  // [G]: rank r's receive buffer [2][S][R + 1] (tagged
+                                        // left columns, block-slot k % 2); peer pointers for
+                                        // real ranks (only own and next are dereferenced)
+  long long rstride;         // entries per slot = S * (R + 1)
   int* ticket;               // [ranks]
   int* hm;                   // H'(m, n)
   int* err;
@@ -54,7 +56,7 @@ __global__ void __launch_bounds__(32) k_fill_cblock(CBlockArgs A) {
   const int kmax = (A.nblocks - rank + G - 1) / G;  // blocks k*G + rank < nblocks
   const long long ntask = (long long)kmax * A.S;
   unsigned long long* bnd = A.bnd + (size_t)lr * 2 * A.bstride;
-  unsigned long long* recv_me = A.recv + (size_t)rank * 2 * A.rstride;
+  const unsigned long long* recv_me = A.recv_tab[rank];
   for (;;) {
     long long task = 0;
     if (lane == 0) task = atomicAdd(A.ticket + lr, 1);
@@ -117,7 +119,7 @@ __global__ void __launch_bounds__(32) k_fill_cblock(CBlockArgs A) {
     if (blk + 1 < A.nblocks) {
       const int rn = (blk + 1) % G;
       const int kn = (blk + 1) / G;
-      rnext = A.recv + (size_t)rn * 2 * A.rstride + (size_t)(kn & 1) * A.rstride + (size_t)s * (R + 1);
+      rnext = A.recv_tab[rn] + (size_t)(kn & 1) * A.rstride + (size_t)s * (R + 1);
       rtag = ((unsigned)(kn & 0xfff) << 20) | (unsigned)(s + 1);
     }
     const int hm_here = (A.m - 1) / R == s && c1 == A.n;

@@ -62,3 +62,28 @@ def gather_scores(local_scores, local_idx: np.ndarray, npairs: int, world: int, 
         keep = i_ >= 0
         full[i_[keep]] = s_[keep]
     return full
+
+
+def cblock_score(ctx, d_a, d_b, sc, group=None, block_cols: int = 0) -> int:
+    """Score of one giant pair with the column-block pipeline across the ranks of
+    `group` (one process per GPU). Receive buffers are
+    symmetric memory, so each rank writes its right boundary columns straight
+    into the next rank's buffer over NVLink; one all-reduce returns H(m, n).
+    Not exercised on more than one GPU in this round (tests cover the same
+    kernel with ranks on concurrent streams of one GPU)."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+    from . import nw as _nw
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    nbytes = _nw.nw_cblock_recv_bytes(d_a.numel())
+    buf = symm.empty(nbytes, dtype=torch.uint8, device=d_a.device)
+    hdl = symm.rendezvous(buf, group if group is not None else dist.group.WORLD)
+    nxt = hdl.get_buffer((rank + 1) % world, [nbytes], torch.uint8)
+    buf.zero_()
+    torch.cuda.synchronize()
+    dist.barrier(group)  # every receive buffer is zero before anyone writes
+    part = torch.zeros(1, dtype=torch.int64, device=d_a.device)
+    _nw.nw_score_only_cblock_rank_dev(ctx, d_a, d_b, sc, rank, world, block_cols, buf, nxt, part)
+    dist.all_reduce(part, group=group)
+    return int(part.item())

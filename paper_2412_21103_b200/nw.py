@@ -73,6 +73,9 @@ def lib() -> ctypes.CDLL:
         "nw_batch_ops_offsets": ([vp, i32, vp, i64, vp], ctypes.c_int),
         "nw_score_only_cblock": ([vp, vp, i64, vp, i64, P(_Scoring), i32, i32, P(i64)],
                                  ctypes.c_int),
+        "nw_cblock_recv_bytes": ([i64], i64),
+        "nw_score_only_cblock_rank_dev": ([vp, vp, i64, vp, i64, P(_Scoring), i32, i32, i32, vp,
+                                           vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -86,7 +89,7 @@ EXPORTED = ("nw_ctx_create", "nw_ctx_destroy", "nw_strerror", "nw_last_error", "
             "nw_ctx_sync", "nw_ctx_launches", "nw_ctx_set_timing", "nw_ctx_kernel_time", "nw_score_only", "nw_score_only_dev",
             "nw_align_pair", "nw_align_pair_dev", "nw_traceback", "nw_traceback_dev",
             "nw_tb_free", "nw_align_batch", "nw_align_batch_dev", "nw_batch_ops_offsets",
-            "nw_score_only_cblock")
+            "nw_score_only_cblock", "nw_cblock_recv_bytes", "nw_score_only_cblock_rank_dev")
 
 
 def _scoring(sc) -> tuple[_Scoring, object]:
@@ -311,3 +314,19 @@ def nw_score_only_cblock(ctx: Context, a, b, sc, ranks: int, block_cols: int = 0
     ctx._check(lib().nw_score_only_cblock(ctx.handle, _ptr(a), len(a), _ptr(b), len(b),
                                           ctypes.byref(s), ranks, block_cols, ctypes.byref(out)))
     return out.value
+
+
+def nw_cblock_recv_bytes(m: int) -> int:
+    """Bytes of one rank's receive buffer for the column-block pipeline."""
+    return int(lib().nw_cblock_recv_bytes(m))
+
+
+def nw_score_only_cblock_rank_dev(ctx: Context, d_a, d_b, sc, rank: int, ranks: int,
+                                  block_cols: int, recv_self, recv_next, d_score) -> None:
+    """One rank of the column-block pipeline (see include/nw.h). Async."""
+    s, keep = _scoring(sc)
+    nxt = None if recv_next is None else _ptr(recv_next)
+    ctx._check(lib().nw_score_only_cblock_rank_dev(ctx.handle, _ptr(d_a), d_a.numel(), _ptr(d_b),
+                                                   d_b.numel(), ctypes.byref(s), rank, ranks,
+                                                   block_cols, _ptr(recv_self), nxt,
+                                                   _ptr(d_score)))

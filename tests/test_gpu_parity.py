@@ -306,3 +306,30 @@ def test_score_only_tall_difference_form(ctx, m, n):
     a, b = _pair(8000 + n, m, n)
     for sc in (nwgen.PAPER_DNA, nwgen.Scoring(match=2, mismatch=-1, gap=-3)):
         assert nwb.nw_score_only(ctx, a, b, sc) == oracle.score(a, b, sc)
+
+
+@pytest.mark.parametrize("G,w", [(2, 0), (3, 700)])
+def test_cblock_rank_api_concurrent_streams(ctx, monkeypatch, G, w):
+    """The per-rank (real multi-GPU) entry point, with the G ranks as concurrent
+    launches on G streams of one GPU and plain device buffers as 'peer' memory."""
+    import torch
+    monkeypatch.setenv("NW_CBLOCK_WARPS_PER_SM", "4")
+    m, n = 5000, 9000
+    a, b = _pair(9100 + G, m, n)
+    sc = nwgen.PAPER_DNA
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    ctxs = [nwb.Context(0, s.cuda_stream) for s in streams]
+    da = torch.frombuffer(bytearray(a), dtype=torch.uint8).cuda()
+    db = torch.frombuffer(bytearray(b), dtype=torch.uint8).cuda()
+    nbytes = nwb.nw_cblock_recv_bytes(m)
+    bufs = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(G)]
+    parts = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(G)]
+    torch.cuda.synchronize()
+    for r in range(G):
+        nwb.nw_score_only_cblock_rank_dev(ctxs[r], da, db, sc, r, G, w, bufs[r], bufs[(r + 1) % G],
+                                          parts[r])
+    for c in ctxs:
+        c.sync()
+    assert sum(int(p.item()) for p in parts) == oracle.score(a, b, sc)
+    for c in ctxs:
+        c.close()
