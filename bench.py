@@ -404,7 +404,9 @@ def run_ours(args):
     out = {
         "metric": "GCUPS (cell updates/s)", "value": value, "unit": "GCUPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong" if (wl == "c5" and world > 1) else "weak", "vs_baseline": None, "dtype": "int32",
+        "higher_is_better": True, "scaling": "strong" if (wl == "c5" and world > 1) else "weak", "vs_baseline": None,
+        # arithmetic of the fill kernel in use: int32 strips, or two 16-bit cells per register
+        "dtype": "int32" if wl in ("c1", "c2") else "u16x2",
         "data": "synthetic (nwgen seeded, SURVEY.md §8(d) recipe)",
         "config": {"workload": WORKLOADS[wl], "cells_per_step": cells_all,
                    "parallelism": (f"replicas{world}" if wl in ("c1", "c2") or (wl == "c5" and world == 1)

@@ -289,8 +289,8 @@ int choose_kr(long long m, long long n, bool dirs) {
   return 2;
 }
 
-bool dispatch_batch(bool dirs, int pi, bool profreg, bool u16, bool d16, const BatchArgs& B,
-                    int grid, size_t smem, cudaStream_t st) {
+bool dispatch_batch(bool dirs, int pi, bool profreg, bool u16, bool d16, int packed_kr,
+                    const BatchArgs& B, int grid, size_t smem, cudaStream_t st) {
   if (!dirs) {
     if (u16) launch_batch_t<KR_BATCH, false, true, 123, 1>(B, grid, smem, st);
     else if (d16) launch_batch_t<KR_BATCH, false, true, 123, 2>(B, grid, smem, st);
@@ -299,12 +299,12 @@ bool dispatch_batch(bool dirs, int pi, bool profreg, bool u16, bool d16, const B
     return true;
   }
   switch (pi) {
-    case 123: launch_batch_dirs<123>(B, profreg, grid, smem, st); return true;
-    case 132: launch_batch_dirs<132>(B, profreg, grid, smem, st); return true;
-    case 213: launch_batch_dirs<213>(B, profreg, grid, smem, st); return true;
-    case 231: launch_batch_dirs<231>(B, profreg, grid, smem, st); return true;
-    case 312: launch_batch_dirs<312>(B, profreg, grid, smem, st); return true;
-    case 321: launch_batch_dirs<321>(B, profreg, grid, smem, st); return true;
+    case 123: launch_batch_dirs<123>(B, profreg, d16 ? packed_kr : 0, grid, smem, st); return true;
+    case 132: launch_batch_dirs<132>(B, profreg, d16 ? packed_kr : 0, grid, smem, st); return true;
+    case 213: launch_batch_dirs<213>(B, profreg, d16 ? packed_kr : 0, grid, smem, st); return true;
+    case 231: launch_batch_dirs<231>(B, profreg, d16 ? packed_kr : 0, grid, smem, st); return true;
+    case 312: launch_batch_dirs<312>(B, profreg, d16 ? packed_kr : 0, grid, smem, st); return true;
+    case 321: launch_batch_dirs<321>(B, profreg, d16 ? packed_kr : 0, grid, smem, st); return true;
   }
   return false;
 }
@@ -972,12 +972,46 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   // per-warp scratch
   const int warps_per_cta = 4;
   const bool profreg = sc->K <= 4;
-  const size_t smem = profreg ? 0 : (size_t)warps_per_cta * sc->K * R;
+  // packed score-only sweeps: the H' form when every H' fits 16 bits (measured
+  // faster on C3), else the difference form (any length); both need s - 2g >= 0
+  const bool packed = !tbk && profreg && d16_ok(sc);
+  int smax = 0;
+  for (int x = 0; x < sc->K; ++x)
+    for (int y = 0; y < sc->K; ++y) smax = std::max(smax, score_of(sc, x, y) - 2 * sc->gap);
+  const bool u16 = packed && (long long)maxlen * smax <= 65535;
+  bool d16 = packed && !u16;
+  if (tbk && !getenv("NW_NO_D16")) {  // traceback: difference form with decision flags
+    int smin = 1 << 30;
+    for (int x = 0; x < sc->K; ++x)
+      for (int y = 0; y < sc->K; ++y) smin = std::min(smin, score_of(sc, x, y) - 2 * sc->gap);
+    d16 = smin >= 0;
+  }
+  const bool packed_sweep = u16 || d16;  // two rows per register
+  // packed traceback strips: 16 rows per lane, or 8 when most pairs are short
+  // (a 512-row strip over a 300-row pair idles 40% of the lanes); NW_BATCH_KR16 overrides
+  int packed_kr = 16;
+  if (tbk && d16) {
+    std::vector<long long> rl;
+    rl.reserve(std::min<long long>(npairs, 4096));
+    for (long long k = 0; k < npairs && k < 4096; ++k) {
+      const int p = h_pairs ? h_pairs[2 * k] : (int)(k % std::max(nseq, 1));
+      rl.push_back(h_offs[p + 1] - h_offs[p]);
+    }
+    std::nth_element(rl.begin(), rl.begin() + rl.size() / 2, rl.end());
+    if (!rl.empty() && rl[rl.size() / 2] <= 768) packed_kr = 8;
+    if (const char* e = getenv("NW_BATCH_KR16")) packed_kr = atoi(e) == 8 ? 8 : 16;
+  }
+  const long long RS = packed_sweep ? 32 * (tbk && d16 ? packed_kr : 16) : R;
+  const size_t smem = profreg ? 0 : (size_t)warps_per_cta * sc->K * RS;
   int ctas_per_sm = 4;
   const long long nwarps = (long long)c->sm_count * ctas_per_sm * warps_per_cta;
   const long long bstride = maxlen + 1 + 64;
-  const long long wpl = (maxlen + 31 + 7) / 8;  // 8-step groups per strip
-  const long long dstride = tbk ? ((maxlen + R - 1) / R) * wpl * KR_BATCH * 32 : 0;
+  // direction scratch per warp, in halfwords: int32 sweep = halfword per (group,
+  // row, lane); packed sweep = 32-bit word per (group, packed row, lane)
+  const long long wpl = (maxlen + (packed_sweep ? 63 : 31) + 7) / 8;  // 8-step groups per strip
+  const long long dstride = !tbk ? 0
+      : packed_sweep ? ((maxlen + RS - 1) / RS) * wpl * (RS / 64) * 32 * 2
+                     : ((maxlen + R - 1) / R) * wpl * KR_BATCH * 32;
   const size_t bytes_bnd = sizeof(int) * (size_t)(nwarps * 2 * bstride);
   const size_t bytes_hm = sizeof(int) * (size_t)nwarps;
   const size_t bytes_dirs = sizeof(uint16_t) * (size_t)(nwarps * dstride);
@@ -1016,18 +1050,11 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   const int pi = tbk ? pi_code(sc->tie) : 123;
   // packed 16-bit sweep (score-only DNA-size alphabets) when s' = s - 2g >= 0 and
   // min(m,n) * max(s') <= 65535 for every pair (bounded by the longest sequence)
-  // packed score-only sweeps: the H' form when every H' fits 16 bits (measured
-  // faster on C3), else the difference form (any length); both need s - 2g >= 0
-  const bool packed = !tbk && profreg && d16_ok(sc);
-  int smax = 0;
-  for (int x = 0; x < sc->K; ++x)
-    for (int y = 0; y < sc->K; ++y) smax = std::max(smax, score_of(sc, x, y) - 2 * sc->gap);
-  const bool u16 = packed && (long long)maxlen * smax <= 65535;
-  const bool d16 = packed && !u16;
+
   bool ok;
   {
     KernelTimer kt(c, 0);
-    ok = dispatch_batch(tbk, pi, profreg, u16, d16, B, grid, smem, c->stream);
+    ok = dispatch_batch(tbk, pi, profreg, u16, d16, packed_kr, B, grid, smem, c->stream);
   }
   if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
   LAUNCHED(c);

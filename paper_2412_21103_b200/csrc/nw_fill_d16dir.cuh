@@ -1,0 +1,219 @@
+// nw_fill_d16dir.cuh -- difference-form packed sweep WITH decision bits, for the
+// batch kernel's traceback mode.
+//
+// Difference form of Eq. 1 as in nw_fill_d16.cuh (Z = max(s-2g, V_up, U_left),
+// U = Z - V_up, V = Z - U_left), two cells per register (rows k and k+h of a
+// lane, the high half one column behind). The P:90 decision needs no extra
+// comparisons: each candidate is maximal exactly when its difference to Z is 0,
+//     D maximal <=> Z - (s-2g) == 0,   U maximal <=> U == 0,   L maximal <=> V == 0,
+// so the bits for the tie order pi = (X, Y, Z) are [q_X == 0], [q_Y == 0], tested
+// for both halves at once by VIADD.16x2(q, 0xffff'ffff) (the top bit of a half is
+// set iff that half was 0; every q < 2^15). Per packed register and 8 steps the
+// flags go to one 32-bit word (halves sharing a PRMT-gathered byte each):
+//   byte 0: X flags of the low cell, byte 1: X of the high cell,
+//   byte 2: Y flags of the low cell, byte 3: Y of the high cell,  step q at bit q.
+// Word index ((s*G + g)*H + k)*32 + lane, G = 8-step groups per strip.
+#pragma once
+#include "nw_fill_d16.cuh"
+
+namespace nwk {
+
+template <int KR>
+struct D16DirState {
+  uint32_t Up[KR / 2];
+  uint32_t PA[KR / 2], PB[KR / 2];  // register profile (PROFREG)
+  uint32_t acc[KR / 2];             // flags of the current 8-step group
+  uint32_t vlast;
+  uint32_t xT_prev, bc_prev, bc_nxt;
+  int usum;
+};
+
+template <int KR, bool PROFREG, int PI, bool MASKED>
+__device__ __forceinline__ void d16dir_group(D16DirState<KR>& st, const FillArgs& A, int lane,
+                                             int t0, const int* bnd_in, int* bnd_out,
+                                             uint32_t* dir_base, const int8_t* sprof,
+                                             int rows_lo, int rows_hi, int chunk) {
+  constexpr int H = KR / 2;
+  constexpr int R = 32 * KR;
+  using T = Tie<PI>;
+  const int n = A.n;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int t = t0 + q;
+    const int jT = t - 2 * lane + 1;
+    const uint32_t bT = st.bc_nxt;
+    st.bc_nxt = __ldg(A.b + jT);
+    uint32_t sel = 0;
+    uint2 lo8 = make_uint2(0, 0), hi8 = make_uint2(0, 0);
+    if (PROFREG) {
+      const uint32_t xT = bT * 17u;
+      sel = xT + (st.xT_prev << 8) + (128u + (196u << 8));
+      st.xT_prev = xT;
+    } else {
+      // s' of the lane's low rows for b_jT and of its high rows for b_jB (previous code)
+      if constexpr (H == 8) {
+        lo8 = *reinterpret_cast<const uint2*>(sprof + bT * R + lane * KR);
+        hi8 = *reinterpret_cast<const uint2*>(sprof + st.bc_prev * R + lane * KR + H);
+      } else {
+        static_assert(H == 4, "packed traceback sweep: 8 or 16 rows per lane");
+        lo8.x = *reinterpret_cast<const uint32_t*>(sprof + bT * R + lane * KR);
+        hi8.x = *reinterpret_cast<const uint32_t*>(sprof + st.bc_prev * R + lane * KR + H);
+      }
+      st.bc_prev = bT;
+    }
+    const int recv = __shfl_up_sync(FULL, (int)st.vlast, 1);
+    const int bval = __shfl_sync(FULL, chunk, (t & 31));
+    const uint32_t upsrc = (lane == 0) ? ((uint32_t)bval << 16) : (uint32_t)recv;
+    uint32_t vup = prmt2(upsrc, st.vlast, 0x5432u);
+    uint32_t mask = 0xffffffffu;
+    if (MASKED) mask = (jT >= 1 ? 0x0000ffffu : 0u) | (jT >= 2 ? 0xffff0000u : 0u);
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      uint32_t sp;
+      if (PROFREG) {
+        sp = prmt2(st.PA[k], st.PB[k], sel);
+      } else {
+        // byte k of lo8 into the low half, byte k of hi8 into the high half (zero-extended)
+        const uint32_t b = (uint32_t)(k & 3);
+        const uint32_t s2 = b | ((b | 8u) << 4) | ((4u + b) << 8) | ((12u + b) << 12);
+        sp = prmt2(k < 4 ? lo8.x : lo8.y, k < 4 ? hi8.x : hi8.y, s2);
+      }
+      const uint32_t ul = st.Up[k];
+      const uint32_t z = __vimax3_u16x2(sp, vup, ul);
+      uint32_t un = z - vup;
+      const uint32_t vn = z - ul;
+      const uint32_t dd = z - sp;
+      // q_X, q_Y in {D: dd, U: un, L: vn}; flag = [q == 0] per half (top bit of each half)
+      const uint32_t qX = T::X == 1 ? dd : (T::X == 2 ? un : vn);
+      const uint32_t qY = T::Y == 1 ? dd : (T::Y == 2 ? un : vn);
+      const uint32_t fX = __vadd2(qX, 0xffffffffu);
+      const uint32_t fY = __vadd2(qY, 0xffffffffu);
+      const uint32_t tk = prmt2(fX, fY, 0x7531u);  // bytes: X.lo, X.hi, Y.lo, Y.hi (flag = bit 7)
+      st.acc[k] = ((st.acc[k] >> 1) & 0x7f7f7f7fu) | (tk & 0x80808080u);
+      if (MASKED) un &= mask;  // U(i, 0) = 0 until each half reaches column 1
+      st.Up[k] = un;
+      vup = vn;
+    }
+    st.vlast = vup;
+    const int jB = jT - 1;
+    if (lane == 31 && (!MASKED || (jB >= 1 && jB <= n))) bnd_out[(t0 - 62) + q] = (int)(vup >> 16);
+    if (MASKED) {
+      if (jT == n) {
+#pragma unroll
+        for (int k = 0; k < H; ++k)
+          if (k < rows_lo) st.usum += (int)(st.Up[k] & 0xffffu);
+      }
+      if (jB == n) {
+#pragma unroll
+        for (int k = 0; k < H; ++k)
+          if (k < rows_hi) st.usum += (int)(st.Up[k] >> 16);
+      }
+    }
+  }
+  uint32_t* d = dir_base + (long long)(t0 >> 3) * (H * 32);
+#pragma unroll
+  for (int k = 0; k < H; ++k) d[k * 32] = st.acc[k];
+}
+
+// One strip of one pair inside the batch kernel (single warp, sequential strips).
+// Adds sum U(i, n) of this strip to *A.hm.
+template <int KR, bool PROFREG, int PI>
+__device__ __forceinline__ void strip_sweep_d16dir(const FillArgs& A, int s, int lane,
+                                                   int8_t* sprof) {
+  constexpr int H = KR / 2;
+  constexpr int R = 32 * KR;
+  const int n = A.n;
+  const int ia0 = s * R + lane * KR;
+  D16DirState<KR> st;
+  if (PROFREG) {
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      const int a0 = A.a[ia0 + k], a1 = A.a[ia0 + k + H];
+      uint32_t w0 = 0, w1 = 0;
+      for (int c = 0; c < A.K; ++c) {
+        w0 |= ((uint32_t)(uint8_t)A.prof[a0 * A.K + c]) << (8 * c);
+        w1 |= ((uint32_t)(uint8_t)A.prof[a1 * A.K + c]) << (8 * c);
+      }
+      st.PA[k] = w0;
+      st.PB[k] = w1;
+    }
+  } else {
+    for (int c = 0; c < A.K; ++c) {
+#pragma unroll
+      for (int r = 0; r < KR; ++r) sprof[c * R + lane * KR + r] = A.prof[A.a[ia0 + r] * A.K + c];
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int k = 0; k < H; ++k) {
+    st.Up[k] = 0;
+    st.acc[k] = 0;
+  }
+  const int rows_lo = max(0, min(H, A.m - ia0));
+  const int rows_hi = max(0, min(H, A.m - ia0 - H));
+  st.vlast = 0;
+  st.xT_prev = 0;
+  st.bc_prev = 0;
+  st.usum = 0;
+  st.bc_nxt = __ldg(A.b - 2 * lane);
+  const int* bnd_in = (s > 0) ? static_cast<const int*>(A.bnd) + (size_t)(s % A.nslots) * A.bstride : nullptr;
+  int* bnd_out = static_cast<int*>(A.bnd) + (size_t)((s + 1) % A.nslots) * A.bstride;
+  uint32_t* dir_base = reinterpret_cast<uint32_t*>(A.dirs) + (long long)s * A.wpl * (H * 32) + lane;
+  const int ngrp = (n + 63 + 7) / 8;
+  int chunk = 0;
+#pragma unroll 1
+  for (int g = 0; g < ngrp; ++g) {
+    const int t0 = g * 8;
+    if ((t0 & 31) == 0) {  // boundary V values for lane 0's columns t0+1 .. t0+32
+      const int jj = t0 + 1 + lane;
+      chunk = (s > 0 && jj <= n) ? bnd_in[jj] : 0;
+    }
+    const bool masked = t0 < 64 || t0 + 7 >= n - 1;
+    if (masked)
+      d16dir_group<KR, PROFREG, PI, true>(st, A, lane, t0, bnd_in, bnd_out, dir_base, sprof,
+                                          rows_lo, rows_hi, chunk);
+    else
+      d16dir_group<KR, PROFREG, PI, false>(st, A, lane, t0, bnd_in, bnd_out, dir_base, sprof,
+                                           rows_lo, rows_hi, chunk);
+  }
+  int tot = st.usum;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
+  if (lane == 0) *A.hm += tot;
+  __syncwarp();
+}
+
+// Decode the decision flags of interior cell (i, j) (1-based) -> P:90 code.
+template <int KR>
+__device__ __forceinline__ int tb_code_d16(const uint32_t* dirs, long long G, int i, int j,
+                                           int X, int Y, int Z) {
+  constexpr int H = KR / 2, R = 32 * KR;
+  const int ia = i - 1;
+  const int s = ia / R, rr = ia % R, l = rr / KR, r = rr % KR;
+  const int hi = r >= H;
+  const int k = hi ? r - H : r;
+  const int t = hi ? j + 2 * l : j - 1 + 2 * l;
+  const uint32_t w = __ldca(dirs + (((long long)s * G + (t >> 3)) * H + k) * 32 + l);
+  const int q = t & 7;
+  const uint32_t fx = (w >> (8 * hi + q)) & 1u, fy = (w >> (16 + 8 * hi + q)) & 1u;
+  return fx ? X : (fy ? Y : Z);
+}
+
+// Walk from (m, n) to (0, 0) over the packed flags; rev[k] = k-th code from the end.
+template <int KR>
+__device__ long long tb_walk_d16(const uint32_t* dirs, long long G, int m, int n, int X, int Y,
+                                 int Z, uint8_t* rev) {
+  int i = m, j = n;
+  long long k = 0;
+  while (i > 0 && j > 0) {
+    const int code = tb_code_d16<KR>(dirs, G, i, j, X, Y, Z);
+    rev[k++] = (uint8_t)code;
+    i -= (code != 3);
+    j -= (code != 2);
+  }
+  while (i > 0) { rev[k++] = 2; --i; }
+  while (j > 0) { rev[k++] = 3; --j; }
+  return k;
+}
+
+}  // namespace nwk

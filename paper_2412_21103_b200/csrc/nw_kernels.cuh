@@ -14,6 +14,7 @@
 #include "nw_fill16.cuh"
 #include "nw_cblock.cuh"
 #include "nw_fill_d16.cuh"
+#include "nw_fill_d16dir.cuh"
 
 namespace nwk {
 
@@ -282,9 +283,10 @@ __device__ __forceinline__ void unrank_pair(long long k, int N, int& p, int& q) 
   q = (int)(k - off(pp) + pp + 1);
 }
 
-// PACKED (score-only, K <= 4, s - 2g >= 0), KR16 rows per lane, two per register:
-// 1 = the H' half-row sweep of nw_fill16.cuh (every H' < 2^16),
-// 2 = the difference-form sweep of nw_fill_d16.cuh (any length).
+// PACKED (s - 2g >= 0), KR16 rows per lane, two per register:
+// 1 = the H' half-row sweep of nw_fill16.cuh (score-only, K <= 4, every H' < 2^16),
+// 2 = the difference-form sweep of nw_fill_d16.cuh (score-only, K <= 4, any length),
+// 3 = the difference-form sweep with decision flags of nw_fill_d16dir.cuh (DIRS).
 template <int KR, bool DIRS, bool PROFREG, int PI, int PACKED = 0, int KR16 = 16>
 __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
   constexpr int R = 32 * KR;
@@ -292,7 +294,8 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
-  int8_t* sprof = smem + (PROFREG ? 0 : wib * (B.K * R));
+  constexpr int RSP = PACKED ? 32 * KR16 : R;  // strip height (shared-profile rows)
+  int8_t* sprof = smem + (PROFREG ? 0 : wib * (B.K * RSP));
   int* bnd = B.wbnd + gw * 2 * B.bstride;
   uint16_t* wd = DIRS ? B.wdirs + gw * B.dstride : nullptr;
   for (;;) {
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       A.m = m; A.n = n; A.nstrips = (m + RS - 1) / RS; A.nslots = 2;
       A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr; A.ebnd = nullptr; A.em = nullptr;
       A.dirs = wd;
-      A.wpl = (n + 31 + 7) / 8;  // 8-step groups per strip
+      A.wpl = PACKED ? (n + 63 + 7) / 8 : (n + 31 + 7) / 8;  // 8-step groups per strip
       A.hm = B.whm + gw; A.err = B.err;
       if constexpr (PACKED == 1) {
         for (int s = 0; s < A.nstrips; ++s) strip_sweep_u16<KR16>(A, s, lane);
@@ -332,6 +335,10 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
         if (lane == 0) *A.hm = 0;  // the difference-form sweep accumulates sum U(i, n)
         __syncwarp();
         for (int s = 0; s < A.nstrips; ++s) strip_sweep_d16<KR16, false>(A, s, lane);
+      } else if constexpr (PACKED == 3) {
+        if (lane == 0) *A.hm = 0;
+        __syncwarp();
+        for (int s = 0; s < A.nstrips; ++s) strip_sweep_d16dir<KR16, PROFREG, PI>(A, s, lane, sprof);
       } else {
         for (int s = 0; s < A.nstrips; ++s)
           strip_sweep<KR, DIRS, PROFREG, PI, false, false>(A, s, lane, sprof);
@@ -341,7 +348,12 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       if (DIRS) {
         uint8_t* o = B.ops + B.ops_off[outk];
         long long L = 0;
-        if (lane == 0) L = tb_walk<KR>(wd, A.wpl, m, n, B.X, B.Y, B.Z, o);
+        if (lane == 0) {
+          if constexpr (PACKED == 3)
+            L = tb_walk_d16<KR16>(reinterpret_cast<const uint32_t*>(wd), A.wpl, m, n, B.X, B.Y, B.Z, o);
+          else
+            L = tb_walk<KR>(wd, A.wpl, m, n, B.X, B.Y, B.Z, o);
+        }
         L = __shfl_sync(FULL, L, 0);
         __syncwarp();
         // reverse in place: o[0..L) holds the codes last-first

@@ -15,7 +15,8 @@ constexpr int KR_BATCH = 8;  // rows per lane, batch kernel
 template <int PI>
 void launch_fill_dirs(const FillArgs& A, int kr, bool profreg, int grid, size_t smem, cudaStream_t st);
 template <int PI>
-void launch_batch_dirs(const BatchArgs& B, bool profreg, int grid, size_t smem, cudaStream_t st);
+void launch_batch_dirs(const BatchArgs& B, bool profreg, int packed_kr, int grid, size_t smem,
+                       cudaStream_t st);
 
 template <int KR, bool DIRS, bool PROFREG, int PI, bool D16 = false>
 void launch_fill_t(const FillArgs& A, int grid, size_t smem, cudaStream_t st) {
@@ -24,9 +25,9 @@ void launch_fill_t(const FillArgs& A, int grid, size_t smem, cudaStream_t st) {
   k<<<grid, 32, smem, st>>>(A);
 }
 
-template <int KR, bool DIRS, bool PROFREG, int PI, int PACKED = 0>
+template <int KR, bool DIRS, bool PROFREG, int PI, int PACKED = 0, int KR16 = 16>
 void launch_batch_t(const BatchArgs& B, int grid, size_t smem, cudaStream_t st) {
-  auto k = k_batch<KR, DIRS, PROFREG, PI, PACKED>;
+  auto k = k_batch<KR, DIRS, PROFREG, PI, PACKED, KR16>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<grid, 128, smem, st>>>(B);
 }
@@ -47,10 +48,18 @@ void launch_batch_t(const BatchArgs& B, int grid, size_t smem, cudaStream_t st) 
     }                                                                                         \
   }                                                                                           \
   template <>                                                                                 \
-  void launch_batch_dirs<PI>(const BatchArgs& B, bool profreg, int grid, size_t smem,         \
-                             cudaStream_t st) {                                               \
-    if (profreg) launch_batch_t<KR_BATCH, true, true, PI>(B, grid, smem, st);                 \
-    else launch_batch_t<KR_BATCH, true, false, PI>(B, grid, smem, st);                        \
+  void launch_batch_dirs<PI>(const BatchArgs& B, bool profreg, int packed_kr, int grid,      \
+                             size_t smem, cudaStream_t st) {                                  \
+    if (packed_kr == 16) {                                                                    \
+      if (profreg) launch_batch_t<KR_BATCH, true, true, PI, 3, 16>(B, grid, smem, st);        \
+      else launch_batch_t<KR_BATCH, true, false, PI, 3, 16>(B, grid, smem, st);               \
+    } else if (packed_kr == 8) {                                                              \
+      if (profreg) launch_batch_t<KR_BATCH, true, true, PI, 3, 8>(B, grid, smem, st);         \
+      else launch_batch_t<KR_BATCH, true, false, PI, 3, 8>(B, grid, smem, st);                \
+    } else {                                                                                  \
+      if (profreg) launch_batch_t<KR_BATCH, true, true, PI>(B, grid, smem, st);               \
+      else launch_batch_t<KR_BATCH, true, false, PI>(B, grid, smem, st);                      \
+    }                                                                                         \
   }
 
 }  // namespace nwk

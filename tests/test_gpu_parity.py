@@ -333,3 +333,25 @@ def test_cblock_rank_api_concurrent_streams(ctx, monkeypatch, G, w):
     assert sum(int(p.item()) for p in parts) == oracle.score(a, b, sc)
     for c in ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("tie", ORDERS)
+@pytest.mark.parametrize("scname", ["dna", "fallback", "protein"])
+def test_batch_traceback_paths_all_orders(ctx, tie, scname):
+    """Batch traceback: packed difference-form flags (s - 2g >= 0) and the int32
+    fallback (s - 2g < 0), every tie order, ragged lengths across strip edges."""
+    if scname == "protein":
+        ss = nwgen.random_set(40 + sum(tie), 16, 1, 1100, nwgen.PROTEIN)
+        sc = nwgen.Scoring(match=0, mismatch=0, gap=-5, alphabet=nwgen.PROTEIN,
+                           subst=nwgen.BLOSUM62, tie=tie)
+    else:
+        ss = nwgen.random_set(50 + sum(tie), 14, 0, 1100)
+        sc = nwgen.Scoring(tie=tie) if scname == "dna" else nwgen.Scoring(match=2, mismatch=-4,
+                                                                        gap=-1, tie=tie)
+    rng = np.random.Generator(np.random.PCG64(sum(tie)))
+    pairs = rng.integers(0, ss.nseq, size=(40, 2)).astype(np.int32)
+    scores, *flat = nwb.nw_align_batch(ctx, ss.residues, ss.offs, pairs, sc, nwb.NW_TRACEBACK)
+    paths = nwb.batch_paths(*flat)
+    for k, (p, q) in enumerate(pairs):
+        ws, wops = oracle.align(ss.seq(p), ss.seq(q), sc)
+        assert scores[k] == ws and paths[k].tolist() == wops.tolist(), (k, len(ss.seq(p)), len(ss.seq(q)))
