@@ -1002,7 +1002,10 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
     if (const char* e = getenv("NW_BATCH_KR16")) packed_kr = atoi(e) == 8 ? 8 : 16;
   }
   const long long RS = packed_sweep ? 32 * (tbk && d16 ? packed_kr : 16) : R;
-  const size_t smem = profreg ? 0 : (size_t)warps_per_cta * sc->K * RS;
+  const size_t smem_prof = profreg ? 0 : (((size_t)warps_per_cta * sc->K * RS + 15) & ~size_t(15));
+  // packed traceback: per-warp window of NG_WIN groups x (RS/64) packed rows x 32 lanes words
+  const size_t smem_win = (tbk && d16) ? (size_t)warps_per_cta * NG_WIN * (RS / 64) * 32 * 4 : 0;
+  const size_t smem = smem_prof + smem_win;
   int ctas_per_sm = 4;
   const long long nwarps = (long long)c->sm_count * ctas_per_sm * warps_per_cta;
   const long long bstride = maxlen + 1 + 64;
@@ -1041,6 +1044,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   B.ops_off = d_ops_off;
   B.ops = d_ops;
   B.ops_len = d_ops_len;
+  B.win_off = (int)smem_prof;
   B.X = sc->tie[0];
   B.Y = sc->tie[1];
   B.Z = sc->tie[2];

@@ -268,7 +268,10 @@ struct BatchArgs {
   int* ops_len;
   int X, Y, Z;
   int* err;
+  int win_off;             // byte offset of the per-warp traceback windows in dynamic smem
 };
+
+constexpr int NG_WIN = 16;  // 8-step groups per staged traceback window (packed layout)
 
 // flat rank-space index k -> (p', q'), p' < q', lexicographic over N items
 __device__ __forceinline__ void unrank_pair(long long k, int N, int& p, int& q) {
@@ -348,13 +351,15 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       if (DIRS) {
         uint8_t* o = B.ops + B.ops_off[outk];
         long long L = 0;
-        if (lane == 0) {
-          if constexpr (PACKED == 3)
-            L = tb_walk_d16<KR16>(reinterpret_cast<const uint32_t*>(wd), A.wpl, m, n, B.X, B.Y, B.Z, o);
-          else
-            L = tb_walk<KR>(wd, A.wpl, m, n, B.X, B.Y, B.Z, o);
+        if constexpr (PACKED == 3) {
+          // all lanes: staged windows of decision words (NG_WIN groups per window)
+          uint32_t* win = reinterpret_cast<uint32_t*>(smem + B.win_off) + wib * (NG_WIN * (KR16 / 2) * 32);
+          L = tb_walk_d16_win<KR16, NG_WIN>(reinterpret_cast<const uint32_t*>(wd), A.wpl, m, n, B.X,
+                                            B.Y, B.Z, o, win, lane);
+        } else {
+          if (lane == 0) L = tb_walk<KR>(wd, A.wpl, m, n, B.X, B.Y, B.Z, o);
+          L = __shfl_sync(FULL, L, 0);
         }
-        L = __shfl_sync(FULL, L, 0);
         __syncwarp();
         // reverse in place: o[0..L) holds the codes last-first
         for (long long a0 = lane; a0 < L / 2; a0 += 32) {
