@@ -38,7 +38,7 @@ struct nw_ctx {
   uint8_t* d_lut = nullptr;     // 256
   int8_t* d_prof = nullptr;     // 64*64
   long long* d_bad = nullptr;   // 1 (+ spare)
-  int* d_ints = nullptr;        // small ints: [0] ticket [1] err [2] hm [3] em
+  int* d_ints = nullptr;        // small ints: [0] ticket [1] err [2] hm [5] slow traceback strips
   size_t ints_cap = 0;
   uint8_t* d_codes = nullptr;   // encoded inputs
   size_t codes_cap = 0;
@@ -69,11 +69,10 @@ struct nw_tb {
   void* mem;          // one device allocation holding everything below
   uint16_t* dirs;     // [S][wpl][KR][32] decision-bit halfwords (nw_fill.cuh)
   long long wpl;      // 8-step groups per strip
-  int* ebnd;          // [S][n+1] exit columns of each strip's bottom row
+  int* spec;          // [S-1][nq] + 1: exits of sampled entries (k_tb_spec)
   int* cs;            // [S] entry column per strip (traceback)
   int* seglen;        // [S]
   long long* segoff;  // [S]
-  int* em;            // E(m, n): exit column of the path's start (written by the fill)
   uint8_t* seg;       // [S][segstride] reversed per-strip path segments
   long long segstride;
   int m, n, S;
@@ -221,6 +220,19 @@ int pi_code(const uint8_t tie[3]) { return tie[0] * 100 + tie[1] * 10 + tie[2]; 
 
 long long pad16(long long x) { return (x + 15) & ~15ll; }
 
+int env_int(const char* name, int dflt, int lo) {
+  const char* e = getenv(name);
+  const int k = e ? atoi(e) : 0;
+  return k >= lo ? k : dflt;
+}
+// Sampled strip exits: spacing of the samples in columns and
+// samples per strip (a multiple of 32), overridable for experiments.
+int tb_lstep() {  // log2 of the spacing (NW_TB_STEP rounds down to a power of two)
+  static int v = [] { int k = env_int("NW_TB_STEP", 4, 1), l = 0; while ((2 << l) <= k) ++l; return l; }();
+  return v;
+}
+int tb_band() { static int v = (env_int("NW_TB_BAND", 256, 32) + 31) / 32 * 32; return v; }
+
 // Entries per boundary-ring slot (columns 0..n plus the sweep's overhang), 16-byte multiple.
 long long bnd_stride(long long n) { return (n + 1 + 64 + 1) & ~1ll; }
 
@@ -355,7 +367,6 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
   int* ticket = c->d_ints;
   int* errf = c->d_ints + 1;
   int* hm = c->d_ints + 2;
-  int* em = c->d_ints + 3;
   const long long gmn = (long long)sc->gap * (m + n);
   if (m > 0 && n > 0) {
     FillArgs A;
@@ -364,8 +375,7 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     A.bnd = c->d_bnd; A.bstride = bnd_stride(n); A.ticket = ticket;
     A.dirs = dirs ? tb->dirs : nullptr;
     A.wpl = dirs ? tb->wpl : 0;
-    A.ebnd = dirs ? tb->ebnd : nullptr;
-    A.hm = hm; A.em = dirs ? tb->em : em; A.err = errf;
+    A.hm = hm; A.err = errf;
     const bool profreg = sc->K <= 4;
     const size_t smem = profreg ? 0 : (size_t)sc->K * R;
     const bool d16 = !dirs && kr == 16;
@@ -442,11 +452,11 @@ nw_status new_tb(nw_ctx* c, long long m, long long n, const nw_scoring* sc, int 
   tb->segstride = pad16(R + n + 1);
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t b_dirs = al((size_t)S * tb->wpl * kr * 32 * sizeof(uint16_t));
-  const size_t b_ebnd = al((size_t)S * (n + 1) * sizeof(int));
+  const size_t b_spec = al((size_t)S * tb_band() * sizeof(int));
   const size_t b_cs = al((size_t)S * sizeof(int)), b_len = b_cs;
-  const size_t b_off = al((size_t)S * sizeof(long long)), b_em = al(sizeof(int));
+  const size_t b_off = al((size_t)S * sizeof(long long));
   const size_t b_seg = al((size_t)S * tb->segstride);
-  const size_t bytes = b_dirs + b_ebnd + b_cs + b_len + b_off + b_em + b_seg;
+  const size_t bytes = b_dirs + b_spec + b_cs + b_len + b_off + b_seg;
   if (m > 0 && n > 0) {
     cudaError_t e = cudaMallocAsync(&tb->mem, bytes, c->stream);
     if (e != cudaSuccess) {
@@ -455,11 +465,10 @@ nw_status new_tb(nw_ctx* c, long long m, long long n, const nw_scoring* sc, int 
     }
     char* p = static_cast<char*>(tb->mem);
     tb->dirs = reinterpret_cast<uint16_t*>(p); p += b_dirs;
-    tb->ebnd = reinterpret_cast<int*>(p); p += b_ebnd;
+    tb->spec = reinterpret_cast<int*>(p); p += b_spec;
     tb->cs = reinterpret_cast<int*>(p); p += b_cs;
     tb->seglen = reinterpret_cast<int*>(p); p += b_len;
     tb->segoff = reinterpret_cast<long long*>(p); p += b_off;
-    tb->em = reinterpret_cast<int*>(p); p += b_em;
     tb->seg = reinterpret_cast<uint8_t*>(p);
   }
   *out = tb;
@@ -492,10 +501,10 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
   const long long bbytes = (long long)sizeof(unsigned long long) * 2 * bnd_stride(n);
   st = grow(c, c->d_bnd, c->bnd_cap, (size_t)bbytes);
   if (st) return st;
-  // one launch zeroes ticket/err/hm/em, the bad-position flag, the code
+  // one launch zeroes ticket/err/hm, the bad-position flag, the code
   // buffers (their padding must hold valid codes) and the boundary ring (tags)
   ZeroRanges zr{{c->d_codes, c->d_bnd, nullptr, nullptr}, {la + lb, bbytes, 0, 0}};
-  st = init_small(c, 4, zr);
+  st = init_small(c, 8, zr);  // [0] ticket [1] err [2] hm [5] slow traceback strips
   if (st) return st;
   uint8_t *ca, *cb;
   st = stage_pair(c, a, m, b, n, host, &ca, &cb);
@@ -673,8 +682,36 @@ static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops) {
   {
     KernelTimer kt(c, 1);
     const int S = tb->S;
-    k_tb_chain<<<1, 32, 0, c->stream>>>(tb->ebnd, tb->n, S, tb->em, tb->cs);
-    LAUNCHED(c);
+    // strip entries: sampled exit walks in a band around the diagonal (in
+    // parallel), then the bottom-up chain over the brackets
+    const int kr = tb->kr, R = 32 * kr;
+    nwk::TbBand B;
+    B.m = tb->m; B.n = tb->n; B.lstep = tb_lstep(); B.step = 1 << B.lstep; B.nb = tb_band();
+    B.ratio = (float)tb->n / (float)tb->m;
+    B.nq = (tb->n + B.step - 1) / B.step + 1;
+    const int left_cols = R + 128;  // > one strip's drift on a near-diagonal path
+    const int gw_bytes = (kr * 16 + 1) * 4;
+    if (S >= 2) {
+      auto kspec = kr == 2 ? k_tb_spec<2> : (kr == 4 ? k_tb_spec<4> : k_tb_spec<8>);
+      const size_t win = (size_t)((32 * B.step + left_cols + 40) / 8 + 2) * gw_bytes;
+      cudaFuncSetAttribute(kspec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win);
+      kspec<<<(S - 1) * (B.nb / 32), 32, win, c->stream>>>(tb->dirs, tb->wpl, B, tb->tie[0],
+                                                          tb->tie[1], tb->tie[2], tb->spec, left_cols);
+      LAUNCHED(c);
+    }
+    {
+      auto kchain = kr == 2 ? k_tb_chain<2> : (kr == 4 ? k_tb_chain<4> : k_tb_chain<8>);
+      // exact walks: windows of ~96 KB of decision bits left of the entry
+      const int win_groups = 96 * 1024 / gw_bytes;
+      const int left_exact = (win_groups - 6) * 8;
+      const int CH = std::max(1, std::min(S, (int)(64 * 1024 / (B.nb * 4))));
+      const size_t smem = (size_t)CH * B.nb * 4 + (size_t)win_groups * gw_bytes;
+      cudaFuncSetAttribute(kchain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kchain<<<1, 1024, smem, c->stream>>>(tb->dirs, tb->wpl, B, S, tb->tie[0], tb->tie[1],
+                                           tb->tie[2], tb->spec, tb->cs, c->d_ints + 5, CH,
+                                           left_exact);
+      LAUNCHED(c);
+    }
     const int smem_bytes = 96 * 1024;
     auto kseg = tb->kr == 2 ? k_tb_segments<2> : (tb->kr == 4 ? k_tb_segments<4> : k_tb_segments<8>);
     cudaFuncSetAttribute(kseg, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
@@ -709,6 +746,11 @@ nw_status nw_traceback(nw_ctx* c, const nw_tb* tb, uint8_t* ops, int64_t cap, in
   long long hl = 0;
   CUDA_TRY(c, cudaMemcpyAsync(&hl, c->d_len, sizeof hl, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (getenv("NW_TB_DEBUG")) {
+    int slow = 0;
+    cudaMemcpy(&slow, c->d_ints + 5, sizeof slow, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "nw_traceback: %d strips, %d walked exactly (unresolved brackets)\n", tb->S, slow);
+  }
   *len = hl;
   if (cap < hl) {
     cudaFreeAsync(d_ops, c->stream);

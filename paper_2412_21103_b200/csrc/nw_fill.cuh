@@ -26,12 +26,6 @@
 // first maximal candidate in pi. Each lane packs one row's bits of 8 steps into
 // a halfword: group g = t/8, halfword index ((s*G + g)*KR + r)*32 + lane, step
 // k = t%8 at bits (15-2k, 14-2k) = (nbX, nbY); every store is 64 contiguous bytes.
-//
-// TBE (traceback exits): every cell also carries E(i,j), the
-// column at which the traceback path from (i,j) first reaches the strip's top
-// boundary row: E = E(predecessor chosen by the decision bits), E(top, j) = j,
-// E(i, 0) = 0. The bottom row's E values let the traceback split into
-// independent per-strip walks.
 #pragma once
 #include <cstdint>
 
@@ -56,9 +50,7 @@ struct FillArgs {
   int* ticket;         // strip dispenser (MULTIWARP)
   uint16_t* dirs;      // [nstrips][wpl][KR][32] decision-bit halfwords (DIRS)
   long long wpl;       // 8-step groups per strip
-  int* ebnd;           // [nstrips][n+1] exit columns E of each strip's bottom row (TBE)
   int* hm;             // H'(m, n) output
-  int* em;             // E(m, n) output (TBE)
   int* err;            // watchdog flag (NW_E_DEADLOCK)
 };
 
@@ -96,11 +88,10 @@ __device__ __forceinline__ int pick(int cD, int cU, int cL) {
 template <int KR>
 struct LaneState {
   int Hl[KR];        // H'(row r, previous column)
-  int El[KR];        // E(row r, previous column) (TBE)
   uint32_t P[KR];    // register profile (PROFREG): byte c = s(a_r, c) - 2g
   uint32_t acc[KR];  // decision bits of row r for the current 8-step group (DIRS)
-  int diag, ediag;   // H'(top-1, j-1), E(top-1, j-1)
-  int send, esend;   // H'(bottom, j), E(bottom, j): sent to lane+1
+  int diag;          // H'(top-1, j-1)
+  int send;          // H'(bottom, j): sent to lane+1
   int chunk_cur, chunk_nxt;  // boundary values for 8 columns (lane q < 8 holds column t0+1+q)
   uint32_t bc_nxt;   // prefetched column code for the next step
 };
@@ -112,10 +103,8 @@ struct StripCtx {
   const void* bnd_in;               // boundary row read (strip s-1's bottom), null for s == 0
   void* bnd_out;                    // boundary row written (this strip's bottom)
   uint16_t* dir_base;               // this lane's decision-bit halfwords
-  int* ebnd_out;                    // this strip's bottom-row exits (TBE)
   int* err;
   int* hm;
-  int* em;
   int n, s, lane;
   int hm_lane, hm_r, hm_t;  // where H'(m, n) lives in this strip (hm_lane < 0: not here)
 };
@@ -169,7 +158,7 @@ __device__ __forceinline__ int chunk_verify(const StripCtx& C, int c0, unsigned 
 
 // One 8-step group of the sweep starting at t0 (t0 % 8 == 0): lane column j = t - lane + 1.
 // MASKED groups contain columns outside [1, n] for some lane (or the H'(m,n) cell).
-template <int KR, bool DIRS, bool PROFREG, int PI, bool MULTIWARP, bool TBE, bool MASKED>
+template <int KR, bool DIRS, bool PROFREG, int PI, bool MULTIWARP, bool MASKED>
 __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C, int t0) {
   constexpr int R = 32 * KR;
   using T = Tie<PI>;
@@ -196,19 +185,13 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
     const int recv = __shfl_up_sync(FULL, st.send, 1);
     const int bval = __shfl_sync(FULL, st.chunk_cur, q);  // strip 0: chunks hold H'(0, j) = 0
     const int up = (lane == 0) ? bval : recv;
-    int eup = 0;
-    if (TBE) {
-      const int erecv = __shfl_up_sync(FULL, st.esend, 1);
-      eup = (lane == 0) ? j : erecv;  // E(top boundary row, j) = j
-    }
-    int hd = st.diag, hu = up, ed = st.ediag, eu = eup;
+    int hd = st.diag, hu = up;
 #pragma unroll
     for (int r = 0; r < KR; ++r) {
       const int S = cell_score<KR, PROFREG>(st, r, sel, pw);
       const int cD = hd + S, cU = hu, cL = st.Hl[r];
       // the up candidate arrives last (vertical chain): fold diag and left first
       int h = max(max(cD, cL), cU);
-      int e = 0;
       if (DIRS) {
         const int cX = pick<T::X>(cD, cU, cL);
         const int cY = pick<T::Y>(cD, cU, cL);
@@ -216,41 +199,14 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
         const int dY = cY - h;  // 0 iff Y is maximal, else < 0  (bit nbY = sign)
         st.acc[r] = __funnelshift_l((uint32_t)dX, st.acc[r], 1);
         st.acc[r] = __funnelshift_l((uint32_t)dY, st.acc[r], 1);
-        if (TBE) {
-          // E follows the chosen predecessor: X if dX == 0, else Y if dY == 0, else Z.
-          // Written so that the up value eu (the vertical chain) enters one select.
-          const bool isX = dX >= 0, isY = dY >= 0;
-          const int el = st.El[r];
-          if (T::X == 2) {
-            e = isX ? eu : (isY ? pick<T::Y>(ed, eu, el) : pick<T::Z>(ed, eu, el));
-          } else if (T::Y == 2) {
-            const int o = isX ? pick<T::X>(ed, eu, el) : pick<T::Z>(ed, eu, el);
-            e = (!isX && isY) ? eu : o;
-          } else {
-            const int o = isX ? pick<T::X>(ed, eu, el) : pick<T::Y>(ed, eu, el);
-            e = (!isX && !isY) ? eu : o;
-          }
-        }
       }
-      if (MASKED) {  // border column H'(i, 0) = 0, E(i, 0) = 0 until the lane starts
-        h = (j >= 1) ? h : 0;
-        if (TBE) e = (j >= 1) ? e : 0;
-      }
+      if (MASKED) h = (j >= 1) ? h : 0;  // border column H'(i, 0) = 0 until the lane starts
       hd = st.Hl[r];
       hu = h;
       st.Hl[r] = h;
-      if (TBE) {
-        ed = st.El[r];
-        eu = e;
-        st.El[r] = e;
-      }
     }
     st.diag = MASKED ? ((j >= 1) ? up : 0) : up;
     st.send = st.Hl[KR - 1];
-    if (TBE) {
-      st.ediag = MASKED ? ((j >= 1) ? eup : 0) : eup;
-      st.esend = st.El[KR - 1];
-    }
     if (lane == 31 && (!MASKED || (j >= 1 && j <= n))) {
       // lane 31's column is j = t - 30: stores step through the group's base pointers
       if (MULTIWARP) {
@@ -260,15 +216,11 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
       } else {
         static_cast<int*>(C.bnd_out)[(t0 - 30) + q] = st.send;
       }
-      if (TBE) C.ebnd_out[(t0 - 30) + q] = st.esend;
     }
     if (MASKED && lane == C.hm_lane && t == C.hm_t) {
 #pragma unroll
       for (int r = 0; r < KR; ++r)
-        if (r == C.hm_r) {
-          *C.hm = st.Hl[r];
-          if (TBE) *C.em = st.El[r];
-        }
+        if (r == C.hm_r) *C.hm = st.Hl[r];
     }
   }
   if (DIRS) {  // group g = t0/8: halfword (g, r, lane), step k at bits (15-2k, 14-2k) = (nbX, nbY)
@@ -282,7 +234,7 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
 // PROFREG: K <= 4, the lane's KR profile words live in registers and each
 // cell's score is one PRMT; otherwise the profile column for b_j is read from
 // shared memory (sprof, K x R bytes per warp).
-template <int KR, bool DIRS, bool PROFREG, int PI, bool MULTIWARP, bool TBE>
+template <int KR, bool DIRS, bool PROFREG, int PI, bool MULTIWARP>
 __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, int8_t* sprof) {
   constexpr int R = 32 * KR;
   const int n = A.n;
@@ -308,11 +260,10 @@ __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, 
 #pragma unroll
   for (int r = 0; r < KR; ++r) {
     st.Hl[r] = 0;
-    st.El[r] = 0;
     st.acc[r] = 0;
   }
-  st.diag = st.ediag = 0;
-  st.send = st.esend = 0;
+  st.diag = 0;
+  st.send = 0;
   st.chunk_cur = st.chunk_nxt = 0;
   StripCtx C;
   C.b = A.b;
@@ -322,10 +273,8 @@ __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, 
   C.bnd_in = (s > 0) ? bnd + esz * (size_t)((s % A.nslots) * A.bstride) : nullptr;
   C.bnd_out = bnd + esz * (size_t)(((s + 1) % A.nslots) * A.bstride);
   C.dir_base = DIRS ? A.dirs + (long long)s * A.wpl * (KR * 32) + lane : nullptr;
-  C.ebnd_out = TBE ? A.ebnd + (long long)s * (n + 1) : nullptr;
   C.err = A.err;
   C.hm = A.hm;
-  C.em = A.em;
   C.n = n;
   C.s = s;
   C.lane = lane;
@@ -345,8 +294,8 @@ __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, 
     unsigned long long raw = 0;
     if (more) raw = chunk_issue<MULTIWARP>(C, t0 + 8);
     const bool masked = t0 < 31 || t0 + 7 >= n - 1;
-    if (masked) sweep_group<KR, DIRS, PROFREG, PI, MULTIWARP, TBE, true>(st, C, t0);
-    else sweep_group<KR, DIRS, PROFREG, PI, MULTIWARP, TBE, false>(st, C, t0);
+    if (masked) sweep_group<KR, DIRS, PROFREG, PI, MULTIWARP, true>(st, C, t0);
+    else sweep_group<KR, DIRS, PROFREG, PI, MULTIWARP, false>(st, C, t0);
     if (more) st.chunk_nxt = chunk_verify<MULTIWARP>(C, t0 + 8, raw);
   }
   __syncwarp();

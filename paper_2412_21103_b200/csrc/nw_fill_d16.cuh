@@ -137,10 +137,8 @@ __device__ __forceinline__ void strip_sweep_d16(const FillArgs& A, int s, int la
   C.bnd_in = (s > 0) ? bnd + esz * (size_t)((s % A.nslots) * A.bstride) : nullptr;
   C.bnd_out = bnd + esz * (size_t)(((s + 1) % A.nslots) * A.bstride);
   C.dir_base = nullptr;
-  C.ebnd_out = nullptr;
   C.err = A.err;
   C.hm = A.hm;
-  C.em = nullptr;
   C.n = n;
   C.s = s;
   C.lane = lane;

@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(32) k_fill_pair(FillArgs A) {
     s = __shfl_sync(FULL, s, 0);
     if (s >= A.nstrips) break;
     if constexpr (D16) strip_sweep_d16<KR, true>(A, s, lane);
-    else strip_sweep<KR, DIRS, PROFREG, PI, true, DIRS>(A, s, lane, smem);
+    else strip_sweep<KR, DIRS, PROFREG, PI, true>(A, s, lane, smem);
   }
 }
 
@@ -132,27 +132,221 @@ __device__ long long tb_walk(const uint16_t* dirs, long long G, int m, int n, in
   return k;
 }
 
-#ifdef NW_COMMON_KERNELS
 // ---- single-pair traceback split at strip boundaries ----
 // cs[s] = column where the path enters strip s: at row m for the last strip
-// (cs[S-1] = n), else on strip s's bottom row R*(s+1). Exits chain through the
-// fill's E values: cs[S-2] = E(m, n), cs[s-1] = ebnd[s][cs[s]].
-__global__ void k_tb_chain(const int* __restrict__ ebnd, int n, int S, const int* em, int* cs) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int c = n;
-  cs[S - 1] = c;
-  if (S >= 2) {
-    c = *em;
-    cs[S - 2] = c;
-    for (int s = S - 2; s >= 1; --s) {
-      // column 0 is the left border: a path there stays there (E(i, 0) = 0)
-      c = (c == 0) ? 0 : __ldcg(ebnd + (long long)s * (n + 1) + c);
-      cs[s - 1] = c;
+// (cs[S-1] = n), else on strip s's bottom row R*(s+1). The fill stores only the
+// decision bits; the entries are recovered after it in two launches:
+//   k_tb_spec   exits of sampled entries in a band around the diagonal, in parallel
+//   k_tb_chain  the bottom-up chain: cs[s-1] = exit of strip s from cs[s], read off
+//               the samples whenever the two samples bracketing cs[s] agree,
+//               else walked exactly.
+// Traceback paths cannot cross (each cell has one predecessor, moves are unit
+// up/left/diagonal), so exits are monotone in the entry column and a path that
+// enters between two sampled entries with the same exit leaves there too.
+
+// Walk strip s's decision bits from (i, j) until the path reaches row i_stop; the
+// column there is the strip's exit. Column 0 is the border (the path goes straight up).
+template <int KR>
+__device__ __forceinline__ int strip_exit_walk(const uint16_t* __restrict__ dirs, long long G,
+                                               int i, int j, int i_stop, int X, int Y, int Z) {
+  constexpr int LKR = KR == 2 ? 1 : (KR == 4 ? 2 : 3), R = 32 * KR;
+  const uint16_t* base = dirs + (long long)((i - 1) / R) * G * (KR * 32);  // one strip
+  while (i > i_stop && j > 0) {
+    const int ia = i - 1;
+    const int l = (ia >> LKR) & 31, r = ia & (KR - 1);
+    const int t = j - 1 + l;
+    // L1-cached: consecutive steps mostly stay in one 128-byte line
+    const uint32_t f = (uint32_t)__ldca(base + ((long long)(t >> 3) * KR + r) * 32 + l) >>
+                       (14 - 2 * (t & 7));
+    const int code = !(f & 2u) ? X : (!(f & 1u) ? Y : Z);
+    i -= (code != 3);
+    j -= (code != 2);
+  }
+  return i > i_stop ? 0 : j;
+}
+
+// Sample q of strip s enters at column min(q*step, n) of row R*(s+1); strip s
+// holds samples q0(s) .. q0(s)+nb-1, centred on the column the diagonal of the
+// (m+1)x(n+1) grid crosses that row at.
+struct TbBand {
+  int m, n, step, lstep, nb, nq;  // step = 1 << lstep; nq = ceil(n/step) + 1 samples per row
+  float ratio;                    // n / m
+  __device__ int q0(int s, int R) const {
+    const int cc = __float2int_rd(__fmul_rn((float)(R * (s + 1)), ratio));
+    const int q = (cc >> lstep) - nb / 2;
+    const int qmax = nq > nb ? nq - nb : 0;
+    return q < 0 ? 0 : (q > qmax ? qmax : q);
+  }
+  __host__ __device__ int col(int q) const { return q * step < n ? q * step : n; }
+};
+
+// Copy ng decision groups of one strip (GS halfwords each) into shared memory,
+// group g at word g * (GS/2 + 1): the pad puts the same (r, l) of consecutive
+// groups in consecutive banks. Threads tid of nth cooperate.
+template <int KR>
+__device__ __forceinline__ void stage_groups(const uint16_t* __restrict__ src_hw, int ng,
+                                             uint32_t* w32, int tid, int nth) {
+  constexpr int GS = KR * 32, GW = GS / 2 + 1, U4 = GS / 8;
+  const uint4* src = reinterpret_cast<const uint4*>(src_hw);
+  const int n16 = ng * U4;
+  int w = tid;
+  for (; w + 7 * nth < n16; w += 8 * nth) {  // 8 loads in flight per thread
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + w + u * nth);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      uint32_t* d = w32 + ((w + u * nth) / U4) * GW + ((w + u * nth) % U4) * 4;
+      d[0] = v[u].x; d[1] = v[u].y; d[2] = v[u].z; d[3] = v[u].w;
     }
+  }
+  for (; w < n16; w += nth) {
+    const uint4 v = __ldcg(src + w);
+    uint32_t* d = w32 + (w / U4) * GW + (w % U4) * 4;
+    d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
   }
 }
 
-#endif  // NW_COMMON_KERNELS
+// Walk strip s (decision bits at base) from (i, j) up to row i_stop through the
+// staged groups g_lo .. g_lo+ng-1. Returns false, with (i, j) where it stopped,
+// when the path leaves the window.
+template <int KR>
+__device__ __forceinline__ bool walk_window(const uint32_t* w32, int g_lo, int ng, int& i, int& j,
+                                            int i_stop, int X, int Y, int Z) {
+  constexpr int LKR = KR == 2 ? 1 : (KR == 4 ? 2 : 3), GW = KR * 16 + 1;
+  while (i > i_stop && j > 0) {
+    const int ia = i - 1;
+    const int l = (ia >> LKR) & 31, r = ia & (KR - 1);
+    const int t = j - 1 + l;
+    const int g = (t >> 3) - g_lo;
+    if ((unsigned)g >= (unsigned)ng) return false;
+    const int x = r * 32 + l;  // halfword within the group
+    const uint32_t f = w32[g * GW + (x >> 1)] >> ((x & 1) * 16 + 14 - 2 * (t & 7));
+    const int code = !(f & 2u) ? X : (!(f & 1u) ? Y : Z);
+    i -= (code != 3);
+    j -= (code != 2);
+  }
+  return true;
+}
+
+// spec[s*nb + k] = exit column of strip s (s < S-1) entered at sample q0(s)+k, or
+// -1 when that walk leaves its window (entries far off the path walk long gaps;
+// the chain then walks the strip exactly). One warp per 32 samples: the warp
+// stages its samples' columns plus left_cols to their left and each lane walks one.
+template <int KR>
+__global__ void __launch_bounds__(32) k_tb_spec(const uint16_t* __restrict__ dirs, long long G,
+                                               TbBand B, int X, int Y, int Z, int* spec,
+                                               int left_cols) {
+  constexpr int R = 32 * KR, GS = KR * 32;
+  extern __shared__ __align__(16) uint32_t w32[];
+  const int lane = threadIdx.x;
+  const int tiles = B.nb / 32;
+  const int s = blockIdx.x / tiles, tile = blockIdx.x % tiles;
+  const int qt = B.q0(s, R) + tile * 32;  // first sample of this warp
+  if (qt >= B.nq) return;
+  const int c_hi = B.col(min(qt + 31, B.nq - 1));
+  const int c_lo = max(0, B.col(qt) - left_cols);
+  const int g_lo = max(0, c_lo - 1) >> 3;  // groups of t = j - 1 + l, j in [c_lo, c_hi]
+  const int ng = (int)min((long long)((c_hi + 30) >> 3), G - 1) - g_lo + 1;
+  const uint16_t* base = dirs + (long long)s * G * GS;
+  stage_groups<KR>(base + (long long)g_lo * GS, ng, w32, lane, 32);
+  __syncwarp();
+  const int q = qt + lane;
+  if (q >= B.nq) return;
+  int i = R * (s + 1), j = B.col(q);
+  const bool in = walk_window<KR>(w32, g_lo, ng, i, j, R * s, X, Y, Z);
+  spec[(long long)s * B.nb + tile * 32 + lane] = (!in) ? -1 : (i == R * s ? j : 0);
+}
+
+// The chain, one CTA of 1024 threads: all threads stage CH strips' samples in
+// shared memory, then warp 0 chains through them. A strip whose bracket is
+// unresolved (or outside the band) is walked exactly: warp 0 posts the strip and
+// entry e, the whole CTA stages the strip's decision bits for columns
+// [e - left_cols, e], and thread 0 walks them; a path that leaves the window on
+// the left (a long gap) gets the next window staged, from where it stopped. The
+// last strip (entered at (m, n)) is always walked exactly.
+template <int KR>
+__global__ void __launch_bounds__(1024) k_tb_chain(const uint16_t* __restrict__ dirs, long long G,
+                                                   TbBand B, int S, int X, int Y, int Z,
+                                                   const int* __restrict__ spec, int* cs,
+                                                   int* nslow, int CH, int left_cols) {
+  constexpr int R = 32 * KR, GS = KR * 32;
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ int cmd[4];  // {0 = chunk done | 1 = walk, strip, entry}; walk state (i, j, done)
+  int* spc = reinterpret_cast<int*>(sm);
+  uint32_t* w32 = sm + (long long)CH * B.nb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nth = blockDim.x;
+  // Exact exit of strip s entered at row i0, column cmd[2]; every thread calls it
+  // after the barrier that published cmd. Returns the exit (all threads).
+  auto exact = [&](int s, int i0) -> int {
+    const int i_stop = R * s;
+    int i = i0, j = cmd[2];
+    __syncthreads();  // cmd[2..3] are rewritten below
+    while (i > i_stop && j > 0) {
+      const int c_lo = max(0, j - left_cols);
+      const int g_lo = max(0, c_lo - 1) >> 3;  // groups of t = j' - 1 + l, j' in [c_lo, j]
+      const int ng = (int)min((long long)((j + 30) >> 3), G - 1) - g_lo + 1;
+      stage_groups<KR>(dirs + ((long long)s * G + g_lo) * GS, ng, w32, tid, nth);
+      __syncthreads();
+      if (tid == 0) {
+        walk_window<KR>(w32, g_lo, ng, i, j, i_stop, X, Y, Z);
+        cmd[2] = i; cmd[3] = j;
+      }
+      __syncthreads();
+      i = cmd[2]; j = cmd[3];
+      __syncthreads();
+    }
+    return (i > i_stop) ? 0 : j;  // j == 0: the path reached the left border and stays there
+  };
+  int e = B.n, slow = 1;
+  if (tid == 0) { cs[S - 1] = e; cmd[2] = e; }
+  __syncthreads();
+  if (S >= 2) {
+    e = exact(S - 1, B.m);
+    if (tid == 0) cs[S - 2] = e;
+  }
+  for (int s_hi = S - 2; s_hi >= 1; s_hi -= CH) {
+    const int s_lo = max(1, s_hi - CH + 1);
+    {
+      const int4* src = reinterpret_cast<const int4*>(spec + (long long)s_lo * B.nb);
+      int4* dst = reinterpret_cast<int4*>(spc);
+      const int n16 = (s_hi - s_lo + 1) * B.nb / 4;
+      for (int w = tid; w < n16; w += blockDim.x) dst[w] = __ldcg(src + w);
+    }
+    __syncthreads();
+    int s = s_hi;
+    for (;;) {
+      if (warp == 0) {  // chain through resolved brackets; stop at an unresolved one
+        for (; s >= s_lo; --s) {
+          const int q0 = B.q0(s, R);
+          const int qa = e >> B.lstep;
+          const int ka = qa - q0;
+          const bool on = B.col(qa) == e;  // e is a sample itself
+          int x = -1;
+          if (ka >= 0 && ka < B.nb && (on || (ka + 1 < B.nb && qa + 1 < B.nq))) {
+            const int* row = spc + (s - s_lo) * B.nb;
+            const int xa = row[ka], xb = on ? xa : row[ka + 1];
+            if (xa == xb) x = xa;  // -1 stays -1: a sample left its window
+          }
+          if (x < 0) break;
+          e = x;
+          if (lane == 0) cs[s - 1] = e;
+        }
+        if (lane == 0) { cmd[0] = s >= s_lo; cmd[1] = s; cmd[2] = e; }
+      }
+      __syncthreads();
+      if (!cmd[0]) break;
+      s = cmd[1];
+      e = exact(s, R * (s + 1));
+      ++slow;
+      if (tid == 0) cs[s - 1] = e;
+      --s;
+    }
+    e = cmd[2];  // every thread carries the chain's entry into the next chunk
+    __syncthreads();
+  }
+  if (tid == 0) *nslow = slow;
+}
 
 // One warp per strip: walk from the strip's entry to its top boundary row (the
 // last row of the strip above), codes written last-first into seg + s*segstride.
@@ -328,7 +522,7 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       A.a = B.codes + ao; A.b = B.codes + bo; A.prof = B.prof; A.K = B.K;
       constexpr int RS = PACKED ? 32 * KR16 : R;  // strip height of the sweep in use
       A.m = m; A.n = n; A.nstrips = (m + RS - 1) / RS; A.nslots = 2;
-      A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr; A.ebnd = nullptr; A.em = nullptr;
+      A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr;
       A.dirs = wd;
       A.wpl = PACKED ? (n + 63 + 7) / 8 : (n + 31 + 7) / 8;  // 8-step groups per strip
       A.hm = B.whm + gw; A.err = B.err;
@@ -344,7 +538,7 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
         for (int s = 0; s < A.nstrips; ++s) strip_sweep_d16dir<KR16, PROFREG, PI>(A, s, lane, sprof);
       } else {
         for (int s = 0; s < A.nstrips; ++s)
-          strip_sweep<KR, DIRS, PROFREG, PI, false, false>(A, s, lane, sprof);
+          strip_sweep<KR, DIRS, PROFREG, PI, false>(A, s, lane, sprof);
       }
       __syncwarp();
       hmv = *(volatile int*)(B.whm + gw);
