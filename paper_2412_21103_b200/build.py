@@ -13,11 +13,14 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libnw_b200.so")
-BUILD = os.path.join(HERE, "_build")
+# NW_BUILD_VARIANT=<name> + NW_NVCC_DEFS="-DX=Y ...": an experiment build in _build_<name>/
+_VAR = os.environ.get("NW_BUILD_VARIANT", "")
+OUT = os.path.join(HERE, f"libnw_b200_{_VAR}.so" if _VAR else "libnw_b200.so")
+BUILD = os.path.join(HERE, f"_build_{_VAR}" if _VAR else "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
+         *os.environ.get("NW_NVCC_DEFS", "").split()]
 
 
 def _sources():

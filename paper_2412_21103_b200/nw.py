@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnw_b200.so")
+LIB_PATH = os.environ.get("NW_LIB_PATH") or os.path.join(_HERE, "libnw_b200.so")  # experiments only
 
 NW_OK, NW_E_INVAL, NW_E_ALPHABET, NW_E_OVERFLOW, NW_E_NOMEM, NW_E_CUDA, NW_E_TRUNC, \
     NW_E_STATE, NW_E_DEADLOCK, NW_E_COMM = range(10)
