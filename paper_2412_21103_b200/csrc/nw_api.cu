@@ -72,7 +72,6 @@ struct nw_tb {
   int* spec;          // [S-1][nq] + 1: exits of sampled entries (k_tb_spec)
   int* cs;            // [S] entry column per strip (traceback)
   int* seglen;        // [S]
-  long long* segoff;  // [S]
   uint8_t* seg;       // [S][segstride] reversed per-strip path segments
   long long segstride;
   int m, n, S;
@@ -293,12 +292,24 @@ int choose_kr(long long m, long long n, bool dirs) {
     const int k = atoi(env);
     if (k == 2 || k == 4 || k == 8) return k;
   }
-  (void)n;
   (void)dirs;
-  // the largest KR that still gives about one strip per SM (measured on B200:
-  // 20k x 20k best at 4, 80k x 2k at 8, 2k x 80k at 2; profiles/r01_exp_fill.json)
-  for (int k : {8, 4}) if (m >= 32LL * k * 150) return k;
-  return 2;
+  // Tall pairs (>= ~150 strips at KR = 8): the largest KR, the lag is amortised
+  // (80k x 2k best at 8, profiles/r01_exp_fill.json). Otherwise the wavefront
+  // model of DESIGN.md §3.2: time ~ c(KR) (n + 31) + L(KR) (S - 1) cycles, with
+  // the measured step cost c and strip-to-strip lag L (tools/exp_lag.py: c = 75,
+  // 97.5, 150 and L = 9450, 9650, 12450 cycles at KR = 2, 4, 8): C2 -> 4,
+  // C1 (1k x 1k) -> 4, 2k x 80k -> 2.
+  if (m >= 32LL * 8 * 150) return 8;
+  const int ks[3] = {2, 4, 8};
+  const double c[3] = {75.0, 97.5, 150.0}, L[3] = {9450.0, 9650.0, 12450.0};
+  int best = 2;
+  double tbest = 1e300;
+  for (int i = 0; i < 3; ++i) {
+    const double S = (double)((m + 32 * ks[i] - 1) / (32 * ks[i]));
+    const double t = c[i] * (double)(n + 31) + L[i] * (S - 1.0);
+    if (t < tbest) { tbest = t; best = ks[i]; }
+  }
+  return best;
 }
 
 bool dispatch_batch(bool dirs, int pi, bool profreg, bool u16, bool d16, int packed_kr,
@@ -454,9 +465,8 @@ nw_status new_tb(nw_ctx* c, long long m, long long n, const nw_scoring* sc, int 
   const size_t b_dirs = al((size_t)S * tb->wpl * kr * 32 * sizeof(uint16_t));
   const size_t b_spec = al((size_t)S * tb_band() * sizeof(int));
   const size_t b_cs = al((size_t)S * sizeof(int)), b_len = b_cs;
-  const size_t b_off = al((size_t)S * sizeof(long long));
   const size_t b_seg = al((size_t)S * tb->segstride);
-  const size_t bytes = b_dirs + b_spec + b_cs + b_len + b_off + b_seg;
+  const size_t bytes = b_dirs + b_spec + b_cs + b_len + b_seg;
   if (m > 0 && n > 0) {
     cudaError_t e = cudaMallocAsync(&tb->mem, bytes, c->stream);
     if (e != cudaSuccess) {
@@ -468,7 +478,6 @@ nw_status new_tb(nw_ctx* c, long long m, long long n, const nw_scoring* sc, int 
     tb->spec = reinterpret_cast<int*>(p); p += b_spec;
     tb->cs = reinterpret_cast<int*>(p); p += b_cs;
     tb->seglen = reinterpret_cast<int*>(p); p += b_len;
-    tb->segoff = reinterpret_cast<long long*>(p); p += b_off;
     tb->seg = reinterpret_cast<uint8_t*>(p);
   }
   *out = tb;
@@ -719,9 +728,7 @@ static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops) {
                                            tb->tie[1], tb->tie[2], tb->cs, tb->seg, tb->segstride,
                                            tb->seglen, smem_bytes / 2);
     LAUNCHED(c);
-    k_tb_offsets<<<1, 1024, 0, c->stream>>>(tb->seglen, S, tb->segoff, c->d_len);
-    LAUNCHED(c);
-    k_tb_assemble<<<S, 256, 0, c->stream>>>(tb->seg, tb->segstride, tb->seglen, tb->segoff, d_ops);
+    k_tb_assemble<<<S, 256, 0, c->stream>>>(tb->seg, tb->segstride, tb->seglen, d_ops, c->d_len);
     LAUNCHED(c);
   }
   CUDA_TRY(c, cudaGetLastError());

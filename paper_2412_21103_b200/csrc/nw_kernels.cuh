@@ -5,7 +5,7 @@
 //   k_fill_pair one pair, many warps: strips chained by tagged boundary entries
 //   k_tb_chain  traceback exits: entry column of every strip (one thread)
 //   k_tb_segments per-strip backtracking of Sec. 2.4, all strips at once
-//   k_tb_offsets / k_tb_assemble  segment offsets, forward-order codes
+//   k_tb_assemble  segment offsets + forward-order codes
 //   (the batch kernel walks each pair with tb_walk inside the same warp)
 //   k_batch     many pairs: one warp per pair, strips in sequence,
 //               optional per-pair traceback by the same warp
@@ -401,36 +401,29 @@ __global__ void __launch_bounds__(32) k_tb_segments(const uint16_t* __restrict__
 }
 
 #ifdef NW_COMMON_KERNELS
-// Exclusive prefix of the segment lengths (top strip first) and the total.
-__global__ void k_tb_offsets(const int* __restrict__ seglen, int S, long long* segoff,
-                             long long* total) {
-  __shared__ long long part[1024];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int per = (S + nt - 1) / nt;
-  const int lo = min(S, tid * per), hi = min(S, lo + per);
+// out[off_s + p] = seg[s][seglen[s] - 1 - p]: forward order, one block per strip;
+// off_s = sum of seglen[0 .. s) (the strips above come first), summed by the
+// block itself; the last block also writes the total length.
+__global__ void __launch_bounds__(256) k_tb_assemble(const uint8_t* __restrict__ seg,
+                                                     long long segstride,
+                                                     const int* __restrict__ seglen,
+                                                     uint8_t* __restrict__ out, long long* total) {
+  __shared__ long long wsum[8];
+  const int s = blockIdx.x, tid = threadIdx.x;
   long long acc = 0;
-  for (int k = lo; k < hi; ++k) acc += seglen[k];
-  part[tid] = acc;
+  for (int k = tid; k < s; k += blockDim.x) acc += seglen[k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((tid & 31) == 0) wsum[tid >> 5] = acc;
   __syncthreads();
-  if (tid == 0) {
-    long long run = 0;
-    for (int k = 0; k < nt; ++k) { const long long v = part[k]; part[k] = run; run += v; }
-    *total = run;
-  }
-  __syncthreads();
-  long long run = part[tid];
-  for (int k = lo; k < hi; ++k) { segoff[k] = run; run += seglen[k]; }
-}
-
-// out[segoff[s] + p] = seg[s][seglen[s] - 1 - p]: forward order, one block per strip.
-__global__ void k_tb_assemble(const uint8_t* __restrict__ seg, long long segstride,
-                              const int* __restrict__ seglen, const long long* __restrict__ segoff,
-                              uint8_t* __restrict__ out) {
-  const int s = blockIdx.x;
+  long long off = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) off += wsum[w];
   const int L = seglen[s];
+  if (s == gridDim.x - 1 && tid == 0) *total = off + L;
   const uint8_t* src = seg + (long long)s * segstride;
-  uint8_t* dst = out + segoff[s];
-  for (int p = threadIdx.x; p < L; p += blockDim.x) dst[p] = src[L - 1 - p];
+  uint8_t* dst = out + off;
+  for (int p = tid; p < L; p += blockDim.x) dst[p] = src[L - 1 - p];
 }
 
 #endif  // NW_COMMON_KERNELS
