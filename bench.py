@@ -49,6 +49,8 @@ WORKLOADS = {
     "c3": "C3: all-pairs of 2,048 DNA sequences of 500-2,000 bp (2,096,128 pairs), score-only",
     "c4": "C4: 100,000 protein pairs of 100-1,000 residues, BLOSUM62, g=-5, score + traceback",
     "c5": "C5: single DNA pair 1,000,000 x 1,000,000, score-only (linear memory)",
+    "msa": "center-star MSA of the C3 set (2,048 DNA sequences of 500-2,000 bp): all-pairs "
+           "scores, center, 2,047 alignments with traceback, union-gap merge (SURVEY.md 8(f) NEXT #1)",
 }
 
 
@@ -180,6 +182,19 @@ def cpu_oracle_sample(workload: str, budget_s: float = 15.0):
         dt = time.perf_counter() - t0
         return {"value": cells / dt / 1e9, "unit": "GCUPS", "cores": 1, "kind": "oracle",
                 "sample": f"{k + 1} C4 pairs ({cells:.3e} cells), fill + traceback, 1 core, {dt:.2f} s"}
+    if workload == "msa":
+        from oracle import msa as omsa
+        ss = nwgen.config_c3()
+        nsub = 48
+        seqs = [ss.seq(k) for k in range(nsub)]
+        lens = np.array([len(x) for x in seqs], dtype=np.int64)
+        t0 = time.perf_counter()
+        c, rows = omsa.msa(seqs, nwgen.PAPER_DNA)
+        dt = time.perf_counter() - t0
+        cells = int((np.sum(lens) ** 2 - np.sum(lens ** 2)) // 2 + lens[c] * (lens.sum() - lens[c]))
+        return {"value": cells / dt / 1e9, "unit": "GCUPS", "cores": 1, "kind": "oracle",
+                "sample": f"center-star MSA of the first {nsub} C3 sequences ({cells:.3e} cells: "
+                          f"all pairs + center alignments), 1 core, {dt:.2f} s"}
     raise ValueError(workload)
 
 
@@ -305,6 +320,39 @@ class BatchWorkload:
             0 if self.h_pairs is None else self.h_pairs.nbytes)
 
 
+class MsaWorkload:
+    """Center-star MSA of the C3 set (NEXT #1): one nw_msa_center_star_dev call per step."""
+
+    def __init__(self, ctx, torch, workload: str, rank: int):
+        import paper_2412_21103_b200 as nwb
+        self.nwb, self.ctx, self.torch = nwb, ctx, torch
+        self.ss = nwgen.config_c3()
+        self.sc = nwgen.PAPER_DNA
+        self.d_seqs = torch.from_numpy(self.ss.residues).cuda()
+        self.d_offs = torch.from_numpy(self.ss.offs).cuda()
+        lens = self.ss.lengths().astype(np.int64)
+        h = nwb.nw_msa_center_star_dev(ctx, self.d_seqs, self.d_offs, self.ss.offs, self.sc)
+        self.center, self.width = h.center, h.width
+        h.free()
+        self.cells_pairs = int((lens.sum() ** 2 - (lens ** 2).sum()) // 2)
+        self.cells_center = int(lens[self.center] * (lens.sum() - lens[self.center]))
+        self.cells = self.total_cells = self.cells_pairs + self.cells_center
+
+    def step(self):
+        self.nwb.nw_msa_center_star_dev(self.ctx, self.d_seqs, self.d_offs, self.ss.offs,
+                                        self.sc).free()
+
+    def step_host(self):
+        h = self.nwb.nw_msa_center_star(self.ctx, self.ss.residues, self.ss.offs, self.sc)
+        rows = h.rows_array()
+        h.free()
+        return rows.nbytes
+
+    @property
+    def h2d_bytes(self):
+        return self.ss.residues.nbytes + self.ss.offs.nbytes
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
@@ -318,6 +366,8 @@ def run_ours(args):
     wl = args.workload
     if wl in ("c1", "c2", "c5"):
         W = PairWorkload(ctx, torch, wl, rank)
+    elif wl == "msa":
+        W = MsaWorkload(ctx, torch, wl, rank)
     else:
         W = BatchWorkload(ctx, torch, wl, rank, world)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
@@ -360,8 +410,8 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    if wl in ("c1", "c2") or (wl == "c5" and world == 1):
-        cells_all = W.cells * world  # replicas: every rank aligns its own pair
+    if wl in ("c1", "c2", "msa") or (wl == "c5" and world == 1):
+        cells_all = W.cells * world  # replicas: every rank aligns its own pair / set
     elif wl == "c5":
         cells_all = W.cells          # one pair pipelined across the ranks
     else:
@@ -370,7 +420,7 @@ def run_ours(args):
     # ---- e2e through the host-pointer ABI
     torch.cuda.synchronize()
     barrier()
-    e2e_steps = max(1, min(args.steps, 5 if wl in ("c3", "c4") else args.steps))
+    e2e_steps = max(1, min(args.steps, 5 if wl in ("c3", "c4", "msa") else args.steps))
     d2h = 0
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
@@ -389,6 +439,12 @@ def run_ours(args):
     ops = OPS_PER_CELL[mode]
     cells_per_launch = W.cells
     achieved = cells_per_launch * ops / (fill_avg_ms / 1e3) / 1e12 if fill_n else None
+    if wl == "msa":  # two batch launches per step: all pairs score-only, center pairs + dirs
+        ops = f"{OPS_PER_CELL['score']} (all pairs) / {OPS_PER_CELL['dirs']} (center alignments)"
+        fill_step_ms = fill_ms / max(args.steps, 1)
+        achieved = (W.cells_pairs * OPS_PER_CELL["score"] + W.cells_center * OPS_PER_CELL["dirs"]) / (
+            fill_step_ms / 1e3) / 1e12 if fill_n else None
+        fill_avg_ms = fill_step_ms
     peak = ALU_ISSUE_LANES_PER_CLK_PER_SM * SM_COUNT * SM_MAX_MHZ * 1e6 / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{wl}.json")
@@ -397,6 +453,7 @@ def run_ours(args):
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (int32 lane-ops)",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "kernel": "k_fill_pair" if wl in ("c1", "c2", "c5") else "k_batch",
+                **({"kernel_ms_is": "both k_batch launches of one step"} if wl == "msa" else {}),
                 "ops_per_cell": ops, "kernel_ms_per_launch": fill_avg_ms,
                 "kernel_share_of_step": (fill_ms / total_ms) if total_ms else None,
                 "traceback_ms_per_step": tb_ms / max(args.steps, 1),
@@ -407,9 +464,10 @@ def run_ours(args):
         "higher_is_better": True, "scaling": "strong" if (wl == "c5" and world > 1) else "weak", "vs_baseline": None,
         # arithmetic of the fill kernel in use: int32 strips, or two 16-bit cells per register
         "dtype": "int32" if wl in ("c1", "c2") else "u16x2",
+        **({"msa": {"center": W.center, "width": W.width}} if wl == "msa" else {}),
         "data": "synthetic (nwgen seeded, SURVEY.md §8(d) recipe)",
         "config": {"workload": WORKLOADS[wl], "cells_per_step": cells_all,
-                   "parallelism": (f"replicas{world}" if wl in ("c1", "c2") or (wl == "c5" and world == 1)
+                   "parallelism": (f"replicas{world}" if wl in ("c1", "c2", "msa") or (wl == "c5" and world == 1)
                                    else f"column-blocks{world}" if wl == "c5" else f"pairs-sharded{world}"),
                    "l2": "flushed between steps (256 MB write)"},
         "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roofline,

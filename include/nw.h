@@ -173,6 +173,32 @@ nw_status nw_score_only_cblock_rank_dev(nw_ctx *ctx, const uint8_t *d_a, int64_t
                                         int32_t rank, int32_t ranks, int32_t block_cols,
                                         void *recv_self, void *recv_next, int64_t *d_score);
 
+/* ---- center-star multiple alignment ----
+ * The paper's use of the batch path: scores of all n(n-1)/2 pairs (Eq. 2), the
+ * center = argmax_p sum_{q != p} score(p, q) (lowest index on ties), every other
+ * sequence k aligned to it (center on the rows, canonical traceback of sc->tie),
+ * and the "once a gap, always a gap" merge: before center residue r the MSA has
+ * G(r) = max_k g_k(r) gap columns (g_k(r) = gaps alignment k opens there), each
+ * row's inserted residues left-aligned in them (R20-R23, §3.10).
+ * seqs/offs as nw_align_batch (nseq >= 2, else NW_E_INVAL). Synchronous; on
+ * success *out owns device rows [nseq][width] (input order, '-' = gap). Errors as
+ * nw_align_batch; *out is NULL on error. */
+typedef struct nw_msa nw_msa;
+nw_status nw_msa_center_star(nw_ctx *ctx, const uint8_t *seqs, const int64_t *offs, int32_t nseq,
+                             const nw_scoring *sc, nw_msa **out);
+/* Device inputs (d_seqs, d_offs on ctx's device; h_offs the host copy of d_offs). */
+nw_status nw_msa_center_star_dev(nw_ctx *ctx, const uint8_t *d_seqs, const int64_t *d_offs,
+                                 const int64_t *h_offs, int32_t nseq, const nw_scoring *sc,
+                                 nw_msa **out);
+/* Center index and number of columns. */
+nw_status nw_msa_info(const nw_msa *msa, int32_t *center, int64_t *width);
+/* Copy the rows to host memory: row p at rows + p*row_stride (row_stride >= width,
+ * else NW_E_TRUNC). Synchronous. */
+nw_status nw_msa_rows(nw_ctx *ctx, const nw_msa *msa, uint8_t *rows, int64_t row_stride);
+/* Device pointer to the rows ([nseq][width], owned by msa). */
+const uint8_t *nw_msa_rows_dev(const nw_msa *msa);
+void nw_msa_free(nw_msa *msa);
+
 /* Wait for the context's stream and report any deferred device-side error
  * (alphabet violations, watchdog) raised by earlier _dev calls. */
 nw_status nw_ctx_sync(nw_ctx *ctx);

@@ -17,6 +17,7 @@
 #include "../../include/nw.h"
 #define NW_COMMON_KERNELS 1
 #include "nw_launch.cuh"
+#include "nw_msa.cuh"
 
 using namespace nwk;
 
@@ -62,6 +63,13 @@ struct nw_ctx {
   bool have_tables = false;
   uint8_t lut_h[256];
   int8_t prof_h[64 * 64];
+};
+
+struct nw_msa {
+  nw_ctx* ctx;
+  int nseq = 0, center = 0;
+  long long W = 0;           // MSA columns
+  uint8_t* d_rows = nullptr; // [nseq][W] gapped rows ('-' = gap), input order
 };
 
 struct nw_tb {
@@ -1212,6 +1220,191 @@ nw_status nw_align_batch_dev(nw_ctx* c, const uint8_t* d_seqs, const int64_t* d_
   return batch_core(c, d_seqs, false, reinterpret_cast<const long long*>(d_offs), ho, nseq, d_pairs,
                     h_pairs, npairs, sc, flags, d_scores, reinterpret_cast<const long long*>(d_ops_off),
                     d_ops, d_ops_len);
+}
+
+}  // extern "C"
+
+namespace {
+
+// Center-star MSA (R20-R23): all-pairs scores -> center ->
+// alignments (center, k) with traceback -> union-gap merge, all on the device;
+// the host reads back the center index and the width (two synchronisations).
+nw_status msa_core(nw_ctx* c, const uint8_t* d_seqs, const long long* d_offs,
+                   const long long* h_offs, int nseq, const nw_scoring* sc, nw_msa** out) {
+  const long long P = (long long)nseq * (nseq - 1) / 2;
+  const int nal = nseq - 1;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  // phase 1: scores of every pair, row sums, center
+  char* w1 = nullptr;
+  const size_t b_sc = al(sizeof(int) * P), b_rs = al(sizeof(long long) * nseq);
+  CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&w1), b_sc + b_rs + 256, c->stream));
+  int* d_sc = reinterpret_cast<int*>(w1);
+  long long* d_rs = reinterpret_cast<long long*>(w1 + b_sc);
+  int* d_center = reinterpret_cast<int*>(w1 + b_sc + b_rs);
+  nw_status st = batch_core(c, d_seqs, false, d_offs, h_offs, nseq, nullptr, nullptr, P, sc,
+                            NW_SCORE_ONLY, d_sc, nullptr, nullptr, nullptr);
+  if (st) { cudaFreeAsync(w1, c->stream); return st; }
+  k_msa_rowsum<<<nseq, 256, 0, c->stream>>>(d_sc, nseq, d_rs);
+  LAUNCHED(c);
+  k_msa_argmax<<<1, 1024, 0, c->stream>>>(d_rs, nseq, d_center);
+  LAUNCHED(c);
+  int center = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&center, d_center, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  cudaFreeAsync(w1, c->stream);
+  st = check_deferred(c);
+  if (st) return st;
+  // phase 2: alignments (center, k), k != center, with traceback
+  std::vector<int> hp(2 * (size_t)nal), other(nal);
+  for (int k = 0, a = 0; k < nseq; ++k)
+    if (k != center) { hp[2 * a] = center; hp[2 * a + 1] = k; other[a] = k; ++a; }
+  std::vector<long long> oo((size_t)nal + 1);
+  if (nw_batch_ops_offsets(reinterpret_cast<const int64_t*>(h_offs), nseq, hp.data(), nal,
+                           reinterpret_cast<int64_t*>(oo.data())))
+    return fail(c, NW_E_INVAL, "msa ops offsets");
+  const int lc = (int)(h_offs[center + 1] - h_offs[center]);
+  const size_t b_p = al(sizeof(int) * 2 * nal), b_o = al(sizeof(int) * nal),
+               b_oo = al(sizeof(long long) * (nal + 1)), b_ops = al((size_t)oo[nal] + 16),
+               b_ol = al(sizeof(int) * nal), b_s2 = al(sizeof(int) * nal),
+               b_G = al(sizeof(int) * (lc + 1)), b_B = al(sizeof(long long) * (lc + 1)),
+               b_W = al(sizeof(long long));
+  char* w2 = nullptr;
+  CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&w2),
+                              b_p + b_o + b_oo + b_ops + b_ol + b_s2 + b_G + b_B + b_W, c->stream));
+  char* q = w2;
+  int* d_pairs = reinterpret_cast<int*>(q); q += b_p;
+  int* d_other = reinterpret_cast<int*>(q); q += b_o;
+  long long* d_oo = reinterpret_cast<long long*>(q); q += b_oo;
+  uint8_t* d_ops = reinterpret_cast<uint8_t*>(q); q += b_ops;
+  int* d_ol = reinterpret_cast<int*>(q); q += b_ol;
+  int* d_s2 = reinterpret_cast<int*>(q); q += b_s2;
+  int* d_G = reinterpret_cast<int*>(q); q += b_G;
+  long long* d_B = reinterpret_cast<long long*>(q); q += b_B;
+  long long* d_W = reinterpret_cast<long long*>(q);
+  auto bail = [&](nw_status e) { cudaFreeAsync(w2, c->stream); return e; };
+  if (nal > 0) {
+    CUDA_TRY(c, cudaMemcpyAsync(d_pairs, hp.data(), sizeof(int) * 2 * nal, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(d_other, other.data(), sizeof(int) * nal, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(d_oo, oo.data(), sizeof(long long) * (nal + 1), cudaMemcpyHostToDevice, c->stream));
+    st = batch_core(c, d_seqs, false, d_offs, h_offs, nseq, d_pairs, hp.data(), nal, sc,
+                    NW_TRACEBACK, d_s2, d_oo, d_ops, d_ol);
+    if (st) return bail(st);
+  }
+  // phase 3: union gapping G(r), block starts B(r), width
+  CUDA_TRY(c, cudaMemsetAsync(d_G, 0, sizeof(int) * (lc + 1), c->stream));
+  if (nal > 0) {
+    k_msa_gaps<<<(nal + 3) / 4, 128, 0, c->stream>>>(d_ops, d_oo, d_ol, nal, lc, d_G);
+    LAUNCHED(c);
+  }
+  k_msa_scan<<<1, 1024, 0, c->stream>>>(d_G, lc, d_B, d_W);
+  LAUNCHED(c);
+  long long W = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&W, d_W, sizeof W, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  // phase 4: rows
+  nw_msa* h = new (std::nothrow) nw_msa;
+  if (!h) return bail(fail(c, NW_E_NOMEM, "msa handle"));
+  h->ctx = c; h->nseq = nseq; h->center = center; h->W = W;
+  if (W > 0 && (size_t)nseq * (size_t)W > 0) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&h->d_rows), (size_t)nseq * W, c->stream);
+    if (e != cudaSuccess) {
+      delete h;
+      return bail(fail(c, NW_E_NOMEM, "msa rows of %lld bytes: %s", (long long)nseq * W, cudaGetErrorString(e)));
+    }
+    CUDA_TRY(c, cudaMemsetAsync(h->d_rows, '-', (size_t)nseq * W, c->stream));
+    if (lc > 0) {
+      k_msa_center<<<(lc + 255) / 256, 256, 0, c->stream>>>(d_seqs + h_offs[center], lc, d_G, d_B,
+                                                            h->d_rows + (long long)center * W);
+      LAUNCHED(c);
+    }
+    if (nal > 0) {
+      k_msa_rows<<<(nal + 3) / 4, 128, 0, c->stream>>>(d_ops, d_oo, d_ol, d_other, d_seqs, d_offs,
+                                                      nal, d_G, d_B, h->d_rows, W);
+      LAUNCHED(c);
+    }
+  }
+  cudaFreeAsync(w2, c->stream);
+  CUDA_TRY(c, cudaGetLastError());
+  *out = h;
+  return NW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+nw_status nw_msa_center_star(nw_ctx* c, const uint8_t* seqs, const int64_t* offs, int32_t nseq,
+                             const nw_scoring* sc, nw_msa** out) {
+  if (!c) return NW_E_INVAL;
+  if (!out || !offs) return fail(c, NW_E_INVAL, "NULL argument");
+  *out = nullptr;
+  if (nseq < 2) return fail(c, NW_E_INVAL, "center star needs nseq >= 2 (S:295)");
+  const long long* h_offs = reinterpret_cast<const long long*>(offs);
+  const long long P = (long long)nseq * (nseq - 1) / 2;
+  nw_status st = batch_check(c, h_offs, nseq, nullptr, P, sc, 0);
+  if (st) return st;
+  if (h_offs[nseq] > 0 && !seqs) return fail(c, NW_E_INVAL, "NULL argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  st = upload_tables(c, sc);
+  if (st) return st;
+  const long long total = h_offs[nseq];
+  char* d = nullptr;
+  const size_t b_raw = ((size_t)total + 16 + 255) & ~size_t(255);
+  CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&d), b_raw + sizeof(long long) * (nseq + 1), c->stream));
+  uint8_t* d_raw = reinterpret_cast<uint8_t*>(d);
+  long long* d_offs = reinterpret_cast<long long*>(d + b_raw);
+  if (total) CUDA_TRY(c, cudaMemcpyAsync(d_raw, seqs, (size_t)total, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(d_offs, offs, sizeof(long long) * (nseq + 1), cudaMemcpyHostToDevice, c->stream));
+  st = msa_core(c, d_raw, d_offs, h_offs, nseq, sc, out);
+  cudaFreeAsync(d, c->stream);
+  if (!st) st = check_deferred(c);
+  if (st && *out) { nw_msa_free(*out); *out = nullptr; }
+  return st;
+}
+
+nw_status nw_msa_center_star_dev(nw_ctx* c, const uint8_t* d_seqs, const int64_t* d_offs,
+                                 const int64_t* h_offs, int32_t nseq, const nw_scoring* sc,
+                                 nw_msa** out) {
+  if (!c) return NW_E_INVAL;
+  if (!out || !h_offs || !d_offs) return fail(c, NW_E_INVAL, "NULL argument");
+  *out = nullptr;
+  if (nseq < 2) return fail(c, NW_E_INVAL, "center star needs nseq >= 2 (S:295)");
+  const long long* ho = reinterpret_cast<const long long*>(h_offs);
+  nw_status st = batch_check(c, ho, nseq, nullptr, (long long)nseq * (nseq - 1) / 2, sc, 0);
+  if (st) return st;
+  if (ho[nseq] > 0 && !d_seqs) return fail(c, NW_E_INVAL, "NULL argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  st = upload_tables(c, sc);
+  if (st) return st;
+  return msa_core(c, d_seqs, reinterpret_cast<const long long*>(d_offs), ho, nseq, sc, out);
+}
+
+nw_status nw_msa_info(const nw_msa* h, int32_t* center, int64_t* width) {
+  if (!h || !center || !width) return NW_E_INVAL;
+  *center = h->center;
+  *width = h->W;
+  return NW_OK;
+}
+
+const uint8_t* nw_msa_rows_dev(const nw_msa* h) { return h ? h->d_rows : nullptr; }
+
+nw_status nw_msa_rows(nw_ctx* c, const nw_msa* h, uint8_t* rows, int64_t row_stride) {
+  if (!c || !h) return c ? fail(c, NW_E_INVAL, "NULL argument") : NW_E_INVAL;
+  if (h->ctx != c) return fail(c, NW_E_STATE, "msa handle belongs to another context");
+  if (row_stride < h->W) return fail(c, NW_E_TRUNC, "row_stride %lld < width %lld", (long long)row_stride, h->W);
+  if (h->W == 0) return NW_OK;
+  if (!rows) return fail(c, NW_E_INVAL, "NULL argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaMemcpy2DAsync(rows, (size_t)row_stride, h->d_rows, (size_t)h->W, (size_t)h->W,
+                                (size_t)h->nseq, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return NW_OK;
+}
+
+void nw_msa_free(nw_msa* h) {
+  if (!h) return;
+  if (h->d_rows) cudaFreeAsync(h->d_rows, h->ctx->stream);
+  delete h;
 }
 
 }  // extern "C"

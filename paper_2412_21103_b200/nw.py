@@ -76,6 +76,12 @@ def lib() -> ctypes.CDLL:
         "nw_cblock_recv_bytes": ([i64], i64),
         "nw_score_only_cblock_rank_dev": ([vp, vp, i64, vp, i64, P(_Scoring), i32, i32, i32, vp,
                                            vp, vp], ctypes.c_int),
+        "nw_msa_center_star": ([vp, vp, vp, i32, P(_Scoring), P(vp)], ctypes.c_int),
+        "nw_msa_center_star_dev": ([vp, vp, vp, vp, i32, P(_Scoring), P(vp)], ctypes.c_int),
+        "nw_msa_info": ([vp, P(i32), P(i64)], ctypes.c_int),
+        "nw_msa_rows": ([vp, vp, vp, i64], ctypes.c_int),
+        "nw_msa_rows_dev": ([vp], vp),
+        "nw_msa_free": ([vp], None),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -89,7 +95,9 @@ EXPORTED = ("nw_ctx_create", "nw_ctx_destroy", "nw_strerror", "nw_last_error", "
             "nw_ctx_sync", "nw_ctx_launches", "nw_ctx_set_timing", "nw_ctx_kernel_time", "nw_score_only", "nw_score_only_dev",
             "nw_align_pair", "nw_align_pair_dev", "nw_traceback", "nw_traceback_dev",
             "nw_tb_free", "nw_align_batch", "nw_align_batch_dev", "nw_batch_ops_offsets",
-            "nw_score_only_cblock", "nw_cblock_recv_bytes", "nw_score_only_cblock_rank_dev")
+            "nw_score_only_cblock", "nw_cblock_recv_bytes", "nw_score_only_cblock_rank_dev",
+            "nw_msa_center_star", "nw_msa_center_star_dev", "nw_msa_info", "nw_msa_rows",
+            "nw_msa_rows_dev", "nw_msa_free")
 
 
 def _scoring(sc) -> tuple[_Scoring, object]:
@@ -330,3 +338,58 @@ def nw_score_only_cblock_rank_dev(ctx: Context, d_a, d_b, sc, rank: int, ranks: 
                                                    d_b.numel(), ctypes.byref(s), rank, ranks,
                                                    block_cols, _ptr(recv_self), nxt,
                                                    _ptr(d_score)))
+
+
+class Msa:
+    """nw_msa handle: center-star alignment rows resident on the device."""
+
+    def __init__(self, ctx: Context, h: ctypes.c_void_p, nseq: int):
+        self.ctx, self._h, self.nseq = ctx, h, nseq
+        c, w = ctypes.c_int32(0), ctypes.c_int64(0)
+        ctx._check(lib().nw_msa_info(h, ctypes.byref(c), ctypes.byref(w)))
+        self.center, self.width = c.value, w.value
+
+    def rows_array(self) -> np.ndarray:
+        """(nseq, width) uint8 gapped rows ('-' = gap), input order."""
+        out = np.empty((self.nseq, max(self.width, 1)), dtype=np.uint8)
+        self.ctx._check(lib().nw_msa_rows(self.ctx.handle, self._h, out.ctypes.data, out.shape[1]))
+        return out[:, :self.width]
+
+    def rows(self) -> list[str]:
+        return [r.tobytes().decode() for r in self.rows_array()]
+
+    def rows_dev_ptr(self) -> int:
+        return lib().nw_msa_rows_dev(self._h)
+
+    def free(self):
+        if self._h:
+            lib().nw_msa_free(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def nw_msa_center_star(ctx: Context, seqs, offs, sc) -> Msa:
+    """Center-star MSA of the sequences seqs[offs[k]:offs[k+1]] (host inputs)."""
+    seqs = _host_bytes(seqs)
+    offs = np.ascontiguousarray(offs, dtype=np.int64)
+    s, keep = _scoring(sc)
+    h = ctypes.c_void_p()
+    ctx._check(lib().nw_msa_center_star(ctx.handle, _ptr(seqs), offs.ctypes.data, len(offs) - 1,
+                                        ctypes.byref(s), ctypes.byref(h)))
+    return Msa(ctx, h, len(offs) - 1)
+
+
+def nw_msa_center_star_dev(ctx: Context, d_seqs, d_offs, h_offs, sc) -> Msa:
+    """Device-input variant (torch CUDA tensors; h_offs the numpy host copy of d_offs)."""
+    h_offs = np.ascontiguousarray(h_offs, dtype=np.int64)
+    s, keep = _scoring(sc)
+    h = ctypes.c_void_p()
+    ctx._check(lib().nw_msa_center_star_dev(ctx.handle, _ptr(d_seqs), _ptr(d_offs),
+                                            h_offs.ctypes.data, len(h_offs) - 1, ctypes.byref(s),
+                                            ctypes.byref(h)))
+    return Msa(ctx, h, len(h_offs) - 1)
