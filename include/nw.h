@@ -199,6 +199,21 @@ nw_status nw_msa_rows(nw_ctx *ctx, const nw_msa *msa, uint8_t *rows, int64_t row
 const uint8_t *nw_msa_rows_dev(const nw_msa *msa);
 void nw_msa_free(nw_msa *msa);
 
+/* ---- the paper's per-cell kernel, corrected ----
+ * Ablation baseline, not the product path: one thread per cell spinning on its
+ * up/left neighbours' direction codes (acquire/release), full H (int32) and
+ * direction grids ((m+1)(n+1) x 5 bytes of device memory, NW_E_NOMEM if they do
+ * not fit), serial backtrack. Same results as nw_align_pair +
+ * nw_traceback. Host variant: synchronous, ops/cap/len as nw_traceback
+ * (NW_E_TRUNC with *len set if cap < len). Device variant: d_ops holds m+n
+ * bytes, *d_len the path length; async on ctx's stream. */
+nw_status nw_align_pair_percell(nw_ctx *ctx, const uint8_t *a, int64_t m, const uint8_t *b,
+                                int64_t n, const nw_scoring *sc, int64_t *score, uint8_t *ops,
+                                int64_t cap, int64_t *len);
+nw_status nw_align_pair_percell_dev(nw_ctx *ctx, const uint8_t *d_a, int64_t m, const uint8_t *d_b,
+                                    int64_t n, const nw_scoring *sc, int64_t *d_score,
+                                    uint8_t *d_ops, int64_t *d_len);
+
 /* Wait for the context's stream and report any deferred device-side error
  * (alphabet violations, watchdog) raised by earlier _dev calls. */
 nw_status nw_ctx_sync(nw_ctx *ctx);

@@ -18,6 +18,7 @@
 #define NW_COMMON_KERNELS 1
 #include "nw_launch.cuh"
 #include "nw_msa.cuh"
+#include "nw_percell.cuh"
 
 using namespace nwk;
 
@@ -1405,6 +1406,109 @@ void nw_msa_free(nw_msa* h) {
   if (!h) return;
   if (h->d_rows) cudaFreeAsync(h->d_rows, h->ctx->stream);
   delete h;
+}
+
+}  // extern "C"
+
+namespace {
+
+// The paper's per-cell kernel: full H and direction grids,
+// one thread per cell with acquire/release flags, serial backtrack.
+nw_status percell_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b, long long n,
+                        const nw_scoring* sc, bool host, long long* d_score, uint8_t* d_ops,
+                        long long* d_len) {
+  nw_status st = check_scoring(c, sc);
+  if (st) return st;
+  st = check_bounds(c, sc, m, n);
+  if (st) return st;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  st = upload_tables(c, sc);
+  if (st) return st;
+  constexpr long long R = R_MAX;
+  const long long la = pad16(PAD + m + R + PAD), lb = pad16(PAD + n + R + PAD);
+  st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
+  if (st) return st;
+  ZeroRanges zr{{c->d_codes, nullptr, nullptr, nullptr}, {la + lb, 0, 0, 0}};
+  st = init_small(c, 8, zr);
+  if (st) return st;
+  uint8_t *ca, *cb;
+  st = stage_pair(c, a, m, b, n, host, &ca, &cb);
+  if (st) return st;
+  const size_t cells = (size_t)(m + 1) * (size_t)(n + 1);
+  const size_t b_H = (cells * sizeof(int) + 255) & ~size_t(255);
+  char* mem = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&mem), b_H + cells + (size_t)(m + n) + 16, c->stream);
+  if (e != cudaSuccess)
+    return fail(c, NW_E_NOMEM, "per-cell grids of %zu bytes: %s", b_H + cells, cudaGetErrorString(e));
+  int* H = reinterpret_cast<int*>(mem);
+  uint8_t* T = reinterpret_cast<uint8_t*>(mem + b_H);
+  uint8_t* rev = T + cells;
+  k_percell_init<<<c->sm_count * 8, 256, 0, c->stream>>>(H, T, (int)m, (int)n, sc->gap);
+  LAUNCHED(c);
+  {
+    KernelTimer kt(c, 0);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_percell_fill, 256, 0);
+    const long long want = (m * n + 255) / 256;
+    const int grid = (int)std::max<long long>(1, std::min<long long>(want, (long long)c->sm_count * std::max(per_sm, 1)));
+    k_percell_fill<<<grid, 256, 0, c->stream>>>(ca, cb, c->d_prof, sc->K, (int)m, (int)n, sc->gap,
+                                                 sc->tie[0], sc->tie[1], sc->tie[2], H, T);
+    LAUNCHED(c);
+  }
+  k_percell_score<<<1, 1, 0, c->stream>>>(H, (int)m, (int)n, d_score);
+  LAUNCHED(c);
+  {
+    KernelTimer kt(c, 1);
+    k_percell_walk<<<1, 32, 0, c->stream>>>(T, (int)m, (int)n, rev, d_len);
+    LAUNCHED(c);
+    k_percell_reverse<<<c->sm_count, 256, 0, c->stream>>>(rev, d_len, d_ops);
+    LAUNCHED(c);
+  }
+  cudaFreeAsync(mem, c->stream);
+  CUDA_TRY(c, cudaGetLastError());
+  return NW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+nw_status nw_align_pair_percell_dev(nw_ctx* c, const uint8_t* d_a, int64_t m, const uint8_t* d_b,
+                                    int64_t n, const nw_scoring* sc, int64_t* d_score,
+                                    uint8_t* d_ops, int64_t* d_len) {
+  if (!c) return NW_E_INVAL;
+  if ((m > 0 && !d_a) || (n > 0 && !d_b) || !d_score || !d_len || (m + n > 0 && !d_ops))
+    return fail(c, NW_E_INVAL, "NULL argument");
+  return percell_entry(c, d_a, m, d_b, n, sc, false, reinterpret_cast<long long*>(d_score), d_ops,
+                       reinterpret_cast<long long*>(d_len));
+}
+
+nw_status nw_align_pair_percell(nw_ctx* c, const uint8_t* a, int64_t m, const uint8_t* b,
+                                int64_t n, const nw_scoring* sc, int64_t* score, uint8_t* ops,
+                                int64_t cap, int64_t* len) {
+  if (!c) return NW_E_INVAL;
+  if ((m > 0 && !a) || (n > 0 && !b) || !score || !len) return fail(c, NW_E_INVAL, "NULL argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  uint8_t* d_ops = nullptr;
+  CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&d_ops), (size_t)(m + n) + 16, c->stream));
+  nw_status st = percell_entry(c, a, m, b, n, sc, true, c->d_score, d_ops, c->d_len);
+  if (st) { cudaFreeAsync(d_ops, c->stream); return st; }
+  long long hl = 0, hs = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&hs, c->d_score, sizeof hs, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(&hl, c->d_len, sizeof hl, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  st = check_deferred(c);
+  if (st) { cudaFreeAsync(d_ops, c->stream); return st; }
+  *score = hs;
+  *len = hl;
+  if (cap < hl) {
+    cudaFreeAsync(d_ops, c->stream);
+    return fail(c, NW_E_TRUNC, "cap %lld < length %lld", (long long)cap, hl);
+  }
+  if (hl) CUDA_TRY(c, cudaMemcpyAsync(ops, d_ops, (size_t)hl, cudaMemcpyDeviceToHost, c->stream));
+  cudaFreeAsync(d_ops, c->stream);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return NW_OK;
 }
 
 }  // extern "C"

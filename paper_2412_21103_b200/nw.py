@@ -82,6 +82,9 @@ def lib() -> ctypes.CDLL:
         "nw_msa_rows": ([vp, vp, vp, i64], ctypes.c_int),
         "nw_msa_rows_dev": ([vp], vp),
         "nw_msa_free": ([vp], None),
+        "nw_align_pair_percell": ([vp, vp, i64, vp, i64, P(_Scoring), P(i64), vp, i64, P(i64)],
+                                  ctypes.c_int),
+        "nw_align_pair_percell_dev": ([vp, vp, i64, vp, i64, P(_Scoring), vp, vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -97,7 +100,7 @@ EXPORTED = ("nw_ctx_create", "nw_ctx_destroy", "nw_strerror", "nw_last_error", "
             "nw_tb_free", "nw_align_batch", "nw_align_batch_dev", "nw_batch_ops_offsets",
             "nw_score_only_cblock", "nw_cblock_recv_bytes", "nw_score_only_cblock_rank_dev",
             "nw_msa_center_star", "nw_msa_center_star_dev", "nw_msa_info", "nw_msa_rows",
-            "nw_msa_rows_dev", "nw_msa_free")
+            "nw_msa_rows_dev", "nw_msa_free", "nw_align_pair_percell", "nw_align_pair_percell_dev")
 
 
 def _scoring(sc) -> tuple[_Scoring, object]:
@@ -393,3 +396,23 @@ def nw_msa_center_star_dev(ctx: Context, d_seqs, d_offs, h_offs, sc) -> Msa:
                                             h_offs.ctypes.data, len(h_offs) - 1, ctypes.byref(s),
                                             ctypes.byref(h)))
     return Msa(ctx, h, len(h_offs) - 1)
+
+
+def nw_align_pair_percell(ctx: Context, a, b, sc) -> tuple[int, np.ndarray]:
+    """The paper's per-cell kernel (ablation baseline, NEXT #4): (score, forward ops)."""
+    a, b = _host_bytes(a), _host_bytes(b)
+    s, keep = _scoring(sc)
+    score, ln = ctypes.c_int64(0), ctypes.c_int64(0)
+    ops = np.empty(max(len(a) + len(b), 1), dtype=np.uint8)
+    ctx._check(lib().nw_align_pair_percell(ctx.handle, _ptr(a), len(a), _ptr(b), len(b),
+                                           ctypes.byref(s), ctypes.byref(score), ops.ctypes.data,
+                                           len(ops), ctypes.byref(ln)))
+    return score.value, ops[:ln.value].copy()
+
+
+def nw_align_pair_percell_dev(ctx: Context, d_a, d_b, sc, d_score, d_ops, d_len) -> None:
+    """Device variant of nw_align_pair_percell (torch CUDA tensors). Async."""
+    s, keep = _scoring(sc)
+    ctx._check(lib().nw_align_pair_percell_dev(ctx.handle, _ptr(d_a), d_a.numel(), _ptr(d_b),
+                                               d_b.numel(), ctypes.byref(s), _ptr(d_score),
+                                               _ptr(d_ops), _ptr(d_len)))
