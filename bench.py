@@ -50,6 +50,8 @@ WORKLOADS = {
     "c4": "C4: 100,000 protein pairs of 100-1,000 residues, BLOSUM62, g=-5, score + traceback",
     "c5": "C5: single DNA pair 1,000,000 x 1,000,000, score-only (linear memory)",
     "c1p": "C1 with the paper's per-cell kernel (Code 1, corrected; ablation baseline, NEXT #4)",
+    "c5tb": "C5 with the full canonical traceback: checkpointed refill within half the free "
+            "HBM for directions (SURVEY.md 8(f) NEXT #3)",
     "msa": "center-star MSA of the C3 set (2,048 DNA sequences of 500-2,000 bp): all-pairs "
            "scores, center, 2,047 alignments with traceback, union-gap merge (SURVEY.md 8(f) NEXT #1)",
 }
@@ -130,8 +132,9 @@ def load_peaks():
 def cpu_oracle_sample(workload: str, budget_s: float = 15.0):
     """Time the oracle (as it stands) on a bounded sample of the workload."""
     import oracle
-    if workload in ("c1", "c2", "c1p", "c2p"):
-        a, b = nwgen.config_c1() if workload in ("c1", "c1p") else nwgen.config_c2()
+    if workload in ("c1", "c2", "c1p", "c2p", "c5tb"):
+        a, b = (nwgen.config_c1() if workload in ("c1", "c1p") else
+                nwgen.config_c5() if workload == "c5tb" else nwgen.config_c2())
         # full pair if it fits the budget (~0.06 GCUPS single-core full+dirs), else a prefix
         side = len(a)
         est = side * side / 0.06e9
@@ -209,12 +212,13 @@ class PairWorkload:
         self.nwb, self.ctx, self.torch = nwb, ctx, torch
         self.workload = workload
         self.percell = workload in ("c1p", "c2p")
+        self.linear = workload == "c5tb"
         gen = {"c1": nwgen.config_c1, "c2": nwgen.config_c2, "c5": nwgen.config_c5,
-               "c1p": nwgen.config_c1, "c2p": nwgen.config_c2}[workload]
+               "c1p": nwgen.config_c1, "c2p": nwgen.config_c2, "c5tb": nwgen.config_c5}[workload]
         a, b = gen()
         self.a, self.b = a, b
         self.m, self.n = len(a), len(b)
-        self.dirs = workload != "c5"
+        self.dirs = workload not in ("c5", "c5tb")
         self.sc = nwgen.PAPER_DNA
         self.da = torch.frombuffer(bytearray(a), dtype=torch.uint8).cuda()
         self.db = torch.frombuffer(bytearray(b), dtype=torch.uint8).cuda()
@@ -226,7 +230,9 @@ class PairWorkload:
         self.pipeline = workload == "c5" and int(os.environ.get("WORLD_SIZE", "1")) > 1
 
     def step(self):
-        if self.percell:
+        if self.linear:  # host-pointer API (it synchronises per segment); inputs 2 MB
+            self.nwb.nw_align_pair_linear(self.ctx, self.a, self.b, self.sc)
+        elif self.percell:
             self.nwb.nw_align_pair_percell_dev(self.ctx, self.da, self.db, self.sc, self.d_score,
                                                self.d_ops, self.d_len)
         elif self.dirs:
@@ -242,6 +248,9 @@ class PairWorkload:
 
     def step_host(self):
         """The same step through the host-pointer ABI (e2e)."""
+        if self.linear:
+            score, ops = self.nwb.nw_align_pair_linear(self.ctx, self.a, self.b, self.sc)
+            return 8 + 8 + len(ops)
         if self.percell:
             score, ops = self.nwb.nw_align_pair_percell(self.ctx, self.a, self.b, self.sc)
             return 8 + 8 + len(ops)
@@ -373,7 +382,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     ctx = nwb.Context(local, stream.cuda_stream)
     wl = args.workload
-    if wl in ("c1", "c2", "c5", "c1p", "c2p"):
+    if wl in ("c1", "c2", "c5", "c1p", "c2p", "c5tb"):
         W = PairWorkload(ctx, torch, wl, rank)
     elif wl == "msa":
         W = MsaWorkload(ctx, torch, wl, rank)
@@ -419,7 +428,7 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    if wl in ("c1", "c2", "msa", "c1p", "c2p") or (wl == "c5" and world == 1):
+    if wl in ("c1", "c2", "msa", "c1p", "c2p", "c5tb") or (wl == "c5" and world == 1):
         cells_all = W.cells * world  # replicas: every rank aligns its own pair / set
     elif wl == "c5":
         cells_all = W.cells          # one pair pipelined across the ranks
@@ -429,7 +438,7 @@ def run_ours(args):
     # ---- e2e through the host-pointer ABI
     torch.cuda.synchronize()
     barrier()
-    e2e_steps = max(1, min(args.steps, 5 if wl in ("c3", "c4", "msa") else args.steps))
+    e2e_steps = max(1, min(args.steps, 5 if wl in ("c3", "c4", "msa") else 2 if wl == "c5tb" else args.steps))
     d2h = 0
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
@@ -444,10 +453,14 @@ def run_ours(args):
            "d2h_bytes_per_step": d2h}
     # ---- roofline of the dominant kernel (the fill)
     fill_avg_ms = fill_ms / max(fill_n, 1)
-    mode = "dirs" if (wl in ("c1", "c2", "c4", "c1p", "c2p")) else "score"
+    mode = "dirs" if (wl in ("c1", "c2", "c4", "c1p", "c2p", "c5tb")) else "score"
     ops = OPS_PER_CELL[mode]
     cells_per_launch = W.cells
     achieved = cells_per_launch * ops / (fill_avg_ms / 1e3) / 1e12 if fill_n else None
+    if wl == "c5tb":  # one score-only pass + the direction refills of every segment
+        fill_avg_ms = fill_ms / max(args.steps, 1)
+        ops = f"{OPS_PER_CELL['score']} (checkpoint pass; refill ops not counted: a lower bound)"
+        achieved = W.cells * OPS_PER_CELL["score"] / (fill_avg_ms / 1e3) / 1e12 if fill_n else None
     if wl == "msa":  # two batch launches per step: all pairs score-only, center pairs + dirs
         ops = f"{OPS_PER_CELL['score']} (all pairs) / {OPS_PER_CELL['dirs']} (center alignments)"
         fill_step_ms = fill_ms / max(args.steps, 1)
@@ -462,7 +475,7 @@ def run_ours(args):
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (int32 lane-ops)",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "kernel": ("k_percell_fill" if wl in ("c1p", "c2p") else
-                           "k_fill_pair" if wl in ("c1", "c2", "c5") else "k_batch"),
+                           "k_fill_pair" if wl in ("c1", "c2", "c5", "c5tb") else "k_batch"),
                 **({"kernel_ms_is": "both k_batch launches of one step"} if wl == "msa" else {}),
                 "ops_per_cell": ops, "kernel_ms_per_launch": fill_avg_ms,
                 "kernel_share_of_step": (fill_ms / total_ms) if total_ms else None,
@@ -473,11 +486,11 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "strong" if (wl == "c5" and world > 1) else "weak", "vs_baseline": None,
         # arithmetic of the fill kernel in use: int32 strips, or two 16-bit cells per register
-        "dtype": "int32" if wl in ("c1", "c2", "c1p", "c2p") else "u16x2",
+        "dtype": "int32" if wl in ("c1", "c2", "c1p", "c2p", "c5tb") else "u16x2",
         **({"msa": {"center": W.center, "width": W.width}} if wl == "msa" else {}),
         "data": "synthetic (nwgen seeded, SURVEY.md §8(d) recipe)",
         "config": {"workload": WORKLOADS[wl], "cells_per_step": cells_all,
-                   "parallelism": (f"replicas{world}" if wl in ("c1", "c2", "msa", "c1p", "c2p") or (wl == "c5" and world == 1)
+                   "parallelism": (f"replicas{world}" if wl in ("c1", "c2", "msa", "c1p", "c2p", "c5tb") or (wl == "c5" and world == 1)
                                    else f"column-blocks{world}" if wl == "c5" else f"pairs-sharded{world}"),
                    "l2": "flushed between steps (256 MB write)"},
         "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roofline,

@@ -199,6 +199,19 @@ nw_status nw_msa_rows(nw_ctx *ctx, const nw_msa *msa, uint8_t *rows, int64_t row
 const uint8_t *nw_msa_rows_dev(const nw_msa *msa);
 void nw_msa_free(nw_msa *msa);
 
+/* ---- checkpointed traceback for pairs whose directions do not fit ----
+ * Score + canonical traceback of one pair keeping at most ~dirs_budget bytes of
+ * 2-bit directions on the device (<= 0: half of the free memory): a score-only
+ * pass stores the H' row every seg_rows rows (seg_rows from the budget), then
+ * segments are refilled with directions bottom-up from their checkpoint row and
+ * walked to their top row. Same score and ops as nw_align_pair
+ * + nw_traceback for every input (the refill repeats the same decisions).
+ * Host pointers, synchronous; ops/cap/len as nw_traceback (NW_E_TRUNC with *len
+ * set if cap < len); extra device memory ~ 8 (n + 66) bytes per checkpoint. */
+nw_status nw_align_pair_linear(nw_ctx *ctx, const uint8_t *a, int64_t m, const uint8_t *b,
+                               int64_t n, const nw_scoring *sc, int64_t dirs_budget,
+                               int64_t *score, uint8_t *ops, int64_t cap, int64_t *len);
+
 /* ---- the paper's per-cell kernel, corrected ----
  * Ablation baseline, not the product path: one thread per cell spinning on its
  * up/left neighbours' direction codes (acquire/release), full H (int32) and

@@ -365,7 +365,9 @@ nw_status init_small(nw_ctx* c, int nints, ZeroRanges zr = ZeroRanges{{nullptr, 
 // Device-side core of nw_score_only / nw_align_pair on already-encoded codes.
 // ca, cb: codes with PAD before and >= R + PAD after. Writes H(m,n) to d_score.
 nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb, long long n,
-                    const nw_scoring* sc, long long* d_score, nw_tb* tb, int kr);
+                    const nw_scoring* sc, long long* d_score, nw_tb* tb, int kr,
+                    unsigned long long* ckpt = nullptr, int ck_every = 0, long long ck_stride = 0,
+                    const unsigned long long* top_row = nullptr);
 
 }  // namespace
 
@@ -379,7 +381,9 @@ __global__ void k_finish_score(const int* hm, long long gmn, long long* out, int
 namespace {
 
 nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb, long long n,
-                    const nw_scoring* sc, long long* d_score, nw_tb* tb, int kr) {
+                    const nw_scoring* sc, long long* d_score, nw_tb* tb, int kr,
+                    unsigned long long* ckpt, int ck_every, long long ck_stride,
+                    const unsigned long long* top_row) {
   const int R = 32 * kr;
   const int nstrips = (int)((m + R - 1) / R);
   const bool dirs = tb != nullptr;
@@ -396,6 +400,7 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     A.dirs = dirs ? tb->dirs : nullptr;
     A.wpl = dirs ? tb->wpl : 0;
     A.hm = hm; A.err = errf;
+    A.ckpt = ckpt; A.ck_every = ck_every; A.ck_stride = ck_stride; A.top_row = top_row;
     const bool profreg = sc->K <= 4;
     const size_t smem = profreg ? 0 : (size_t)sc->K * R;
     const bool d16 = !dirs && kr == 16;
@@ -692,7 +697,10 @@ void nw_tb_free(nw_tb* tb) {
   delete tb;
 }
 
-static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops) {
+// pad_top = false, exit_col: stop at row 0 (the top of a checkpoint segment,
+// DESIGN.md §3.12) instead of walking the border, and report the column reached.
+static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops, bool pad_top = true,
+                                int* exit_col = nullptr) {
   const long long L = (long long)tb->m + tb->n;
   nw_status st = grow(c, c->d_rev, c->rev_cap, (size_t)std::max<long long>(L, 1));
   if (st) return st;
@@ -735,7 +743,7 @@ static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops) {
     cudaFuncSetAttribute(kseg, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     kseg<<<S, 32, smem_bytes, c->stream>>>(tb->dirs, tb->wpl, tb->m, tb->n, tb->tie[0],
                                            tb->tie[1], tb->tie[2], tb->cs, tb->seg, tb->segstride,
-                                           tb->seglen, smem_bytes / 2);
+                                           tb->seglen, smem_bytes / 2, pad_top ? 1 : 0, exit_col);
     LAUNCHED(c);
     k_tb_assemble<<<S, 256, 0, c->stream>>>(tb->seg, tb->segstride, tb->seglen, d_ops, c->d_len);
     LAUNCHED(c);
@@ -1508,6 +1516,137 @@ nw_status nw_align_pair_percell(nw_ctx* c, const uint8_t* a, int64_t m, const ui
   if (hl) CUDA_TRY(c, cudaMemcpyAsync(ops, d_ops, (size_t)hl, cudaMemcpyDeviceToHost, c->stream));
   cudaFreeAsync(d_ops, c->stream);
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return NW_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Checkpointed traceback: a score-only
+// pass that keeps the H' row at every seg_rows-th row, then, bottom-up, each
+// segment is refilled with directions from its checkpoint row (columns only up
+// to where the path enters it) and walked to its top row. The refill makes the
+// same decisions as a full fill, so the path is the canonical one.
+nw_status linear_core(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b, long long n,
+                      const nw_scoring* sc, long long budget, long long* score_out,
+                      std::vector<uint8_t>& path) {
+  constexpr long long R = R_MAX;
+  const long long la = pad16(PAD + m + R + PAD), lb = pad16(PAD + n + R + PAD);
+  nw_status st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
+  if (st) return st;
+  const long long bstr = bnd_stride(n);
+  const long long bbytes = (long long)sizeof(unsigned long long) * 2 * bstr;
+  st = grow(c, c->d_bnd, c->bnd_cap, (size_t)bbytes);
+  if (st) return st;
+  ZeroRanges zr{{c->d_codes, c->d_bnd, nullptr, nullptr}, {la + lb, bbytes, 0, 0}};
+  st = init_small(c, 8, zr);
+  if (st) return st;
+  uint8_t *ca, *cb;
+  st = stage_pair(c, a, m, b, n, true, &ca, &cb);
+  if (st) return st;
+  // segment height: directions take (n + 38) / 4 bytes per row
+  int kr_ck = choose_kr(m, n, false);
+  if (kr_ck == 16) kr_ck = 8;
+  const long long Rck = 32LL * kr_ck;
+  const long long rows_max = std::max<long long>(1, budget / ((n + 38) / 4 + 1));
+  const long long K = std::max<long long>(1, rows_max / Rck);
+  const long long seg_rows = K * Rck;
+  const long long nseg = (m + seg_rows - 1) / seg_rows;
+  unsigned long long* ckpt = nullptr;
+  if (nseg > 1) {  // one slot per segment boundary, plus one for a last strip ending on one
+    const size_t ckb = sizeof(unsigned long long) * (size_t)bstr * (size_t)nseg;
+    CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&ckpt), ckb, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(ckpt, 0, ckb, c->stream));
+  }
+  auto done = [&](nw_status e) { if (ckpt) cudaFreeAsync(ckpt, c->stream); return e; };
+  st = pair_core(c, ca, m, cb, n, sc, c->d_score, nullptr, kr_ck, ckpt, (int)K, bstr, nullptr);
+  if (st) return done(st);
+  CUDA_TRY(c, cudaMemcpyAsync(score_out, c->d_score, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  st = check_deferred(c);  // synchronises; reports alphabet errors
+  if (st) return done(st);
+  std::vector<std::vector<uint8_t>> segs((size_t)nseg);
+  long long col = n;  // where the path enters the current segment's bottom row
+  uint8_t* d_ops = nullptr;
+  CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&d_ops), (size_t)(seg_rows + n) + 16, c->stream));
+  for (long long sg = nseg - 1; sg >= 0; --sg) {
+    const long long r0 = sg * seg_rows, r1 = std::min(m, r0 + seg_rows), mm = r1 - r0;
+    if (col == 0) {  // the path reached column 0: straight up to the origin (R7)
+      segs[(size_t)sg].assign((size_t)r1, (uint8_t)NW_UP);
+      break;
+    }
+    ZeroRanges zb{{c->d_bnd, nullptr, nullptr, nullptr}, {bbytes, 0, 0, 0}};
+    st = init_small(c, 8, zb);  // fresh ticket, error flag and ring tags for this fill
+    if (st) break;
+    const int kr = choose_kr(mm, col, true);
+    nw_tb* tb = nullptr;
+    st = new_tb(c, mm, col, sc, kr, &tb);
+    if (st) break;
+    const unsigned long long* top = sg > 0 ? ckpt + (sg - 1) * bstr : nullptr;
+    st = pair_core(c, ca + r0, mm, cb, col, sc, c->d_score, tb, kr, nullptr, 0, 0, top);
+    int* d_exit = c->d_ints + 6;
+    if (!st) st = grow(c, c->d_rev, c->rev_cap, (size_t)(mm + col));
+    if (!st) st = traceback_core(c, tb, d_ops, sg == 0, d_exit);
+    long long L = 0;
+    int ex = 0;
+    if (!st) {
+      CUDA_TRY(c, cudaMemcpyAsync(&L, c->d_len, sizeof L, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(c, cudaMemcpyAsync(&ex, d_exit, sizeof ex, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      segs[(size_t)sg].resize((size_t)L);
+      if (L) CUDA_TRY(c, cudaMemcpy(segs[(size_t)sg].data(), d_ops, (size_t)L, cudaMemcpyDeviceToHost));
+    }
+    nw_tb_free(tb);
+    if (st) break;
+    st = check_deferred(c);
+    if (st) break;
+    col = ex;
+  }
+  cudaFreeAsync(d_ops, c->stream);
+  if (st) return done(st);
+  path.clear();
+  for (auto& v : segs) path.insert(path.end(), v.begin(), v.end());
+  return done(NW_OK);
+}
+
+}  // namespace
+
+extern "C" {
+
+nw_status nw_align_pair_linear(nw_ctx* c, const uint8_t* a, int64_t m, const uint8_t* b, int64_t n,
+                               const nw_scoring* sc, int64_t dirs_budget, int64_t* score,
+                               uint8_t* ops, int64_t cap, int64_t* len) {
+  if (!c) return NW_E_INVAL;
+  if ((m > 0 && !a) || (n > 0 && !b) || !score || !len) return fail(c, NW_E_INVAL, "NULL argument");
+  nw_status st = check_scoring(c, sc);
+  if (st) return st;
+  st = check_bounds(c, sc, m, n);
+  if (st) return st;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  st = upload_tables(c, sc);
+  if (st) return st;
+  if (dirs_budget <= 0) {  // default: half of the free device memory
+    size_t fr = 0, tot = 0;
+    CUDA_TRY(c, cudaMemGetInfo(&fr, &tot));
+    dirs_budget = (int64_t)(fr / 2);
+  }
+  std::vector<uint8_t> path;
+  long long sc_out = 0;
+  if (m == 0 || n == 0) {
+    sc_out = (long long)sc->gap * (m + n);
+    path.assign((size_t)(m + n), (uint8_t)(m > 0 ? NW_UP : NW_LEFT));
+  } else {
+    st = linear_core(c, a, m, b, n, sc, dirs_budget, &sc_out, path);
+    if (st) return st;
+  }
+  *score = sc_out;
+  *len = (int64_t)path.size();
+  if (cap < (int64_t)path.size())
+    return fail(c, NW_E_TRUNC, "cap %lld < length %lld", (long long)cap, (long long)path.size());
+  if (!path.empty()) {
+    if (!ops) return fail(c, NW_E_INVAL, "NULL argument");
+    memcpy(ops, path.data(), path.size());
+  }
   return NW_OK;
 }
 

@@ -52,6 +52,11 @@ struct FillArgs {
   long long wpl;       // 8-step groups per strip
   int* hm;             // H'(m, n) output
   int* err;            // watchdog flag (NW_E_DEADLOCK)
+  // Checkpointed traceback, MULTIWARP only; null / 0 otherwise:
+  unsigned long long* ckpt;           // strips s with (s+1) % ck_every == 0 write their bottom
+  int ck_every;                       //   row here (tagged, slot (s+1)/ck_every - 1) instead of
+  long long ck_stride;                //   the ring; strip s+1 reads it from there
+  const unsigned long long* top_row;  // tagged H' of the row above strip 0 (null: zeros)
 };
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
@@ -101,6 +106,7 @@ struct StripCtx {
   const uint8_t* b;
   const int8_t* sprof;              // shared profile [K][R] (not PROFREG)
   const void* bnd_in;               // boundary row read (strip s-1's bottom), null for s == 0
+  const unsigned long long* top_in; // strip 0 of a segment: the checkpoint row above it
   void* bnd_out;                    // boundary row written (this strip's bottom)
   uint16_t* dir_base;               // this lane's decision-bit halfwords
   int* err;
@@ -126,6 +132,8 @@ __device__ __forceinline__ unsigned long long chunk_issue(const StripCtx& C, int
   const int jj = c0 + 1 + C.lane;
   if (C.lane >= 8 || jj > C.n) return 0ull;
   if (!MULTIWARP) return (unsigned)static_cast<const int*>(C.bnd_in)[jj];
+  if (C.top_in)  // a checkpoint row (complete before the launch): re-tag it for strip 0
+    return (C.top_in[jj] & 0xffffffffull) | ((unsigned long long)(unsigned)C.s << 32);
   return ld_relaxed_u64(static_cast<const unsigned long long*>(C.bnd_in) + jj);
 }
 
@@ -272,6 +280,11 @@ __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, 
   char* bnd = static_cast<char*>(A.bnd);
   C.bnd_in = (s > 0) ? bnd + esz * (size_t)((s % A.nslots) * A.bstride) : nullptr;
   C.bnd_out = bnd + esz * (size_t)(((s + 1) % A.nslots) * A.bstride);
+  C.top_in = (MULTIWARP && s == 0) ? A.top_row : nullptr;
+  if (MULTIWARP && A.ckpt != nullptr) {  // checkpoint strips hand their row over through ckpt
+    if ((s + 1) % A.ck_every == 0) C.bnd_out = A.ckpt + (long long)((s + 1) / A.ck_every - 1) * A.ck_stride;
+    if (s > 0 && s % A.ck_every == 0) C.bnd_in = A.ckpt + (long long)(s / A.ck_every - 1) * A.ck_stride;
+  }
   C.dir_base = DIRS ? A.dirs + (long long)s * A.wpl * (KR * 32) + lane : nullptr;
   C.err = A.err;
   C.hm = A.hm;
@@ -284,13 +297,14 @@ __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, 
     C.hm_lane = rr / KR; C.hm_r = rr % KR; C.hm_t = n - 1 + C.hm_lane;
   }
   st.bc_nxt = __ldg(A.b - lane);  // b_{j-1} for step 0 (j = 1 - lane)
-  if (s > 0) st.chunk_nxt = chunk_verify<MULTIWARP>(C, 0, chunk_issue<MULTIWARP>(C, 0));
+  const bool has_top = s > 0 || C.top_in != nullptr;
+  if (has_top) st.chunk_nxt = chunk_verify<MULTIWARP>(C, 0, chunk_issue<MULTIWARP>(C, 0));
   const int ngrp = (n + 31 + 7) / 8;  // steps 0 .. n+30 in groups of 8
 #pragma unroll 1
   for (int g = 0; g < ngrp; ++g) {
     const int t0 = g * 8;
     st.chunk_cur = st.chunk_nxt;
-    const bool more = s > 0 && t0 + 8 < n;
+    const bool more = has_top && t0 + 8 < n;
     unsigned long long raw = 0;
     if (more) raw = chunk_issue<MULTIWARP>(C, t0 + 8);
     const bool masked = t0 < 31 || t0 + 7 >= n - 1;

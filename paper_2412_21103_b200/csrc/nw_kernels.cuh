@@ -356,7 +356,8 @@ template <int KR>
 __global__ void __launch_bounds__(32) k_tb_segments(const uint16_t* __restrict__ dirs, long long G,
                                                    int m, int n, int X, int Y, int Z,
                                                    const int* __restrict__ cs, uint8_t* seg,
-                                                   long long segstride, int* seglen, int smem_hw) {
+                                                   long long segstride, int* seglen, int smem_hw,
+                                                   int pad_top, int* exit_col) {
   constexpr int R = 32 * KR;
   constexpr int GS = KR * 32;  // halfwords per (strip, group)
   extern __shared__ __align__(16) uint16_t sh[];
@@ -395,8 +396,11 @@ __global__ void __launch_bounds__(32) k_tb_segments(const uint16_t* __restrict__
     i -= (code != 3);
     j -= (code != 2);
   }
-  if (s == 0)
-    while (j > 0) { out[k++] = 3; --j; }  // row 0: horizontal (R7)
+  if (s == 0) {
+    if (exit_col) *exit_col = j;  // a segment of a checkpointed traceback stops at its top row
+    if (pad_top)
+      while (j > 0) { out[k++] = 3; --j; }  // row 0: horizontal (R7)
+  }
   seglen[s] = k;
 }
 
@@ -515,7 +519,7 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       A.a = B.codes + ao; A.b = B.codes + bo; A.prof = B.prof; A.K = B.K;
       constexpr int RS = PACKED ? 32 * KR16 : R;  // strip height of the sweep in use
       A.m = m; A.n = n; A.nstrips = (m + RS - 1) / RS; A.nslots = 2;
-      A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr;
+      A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr; A.ckpt = nullptr; A.ck_every = 0; A.ck_stride = 0; A.top_row = nullptr;
       A.dirs = wd;
       A.wpl = PACKED ? (n + 63 + 7) / 8 : (n + 31 + 7) / 8;  // 8-step groups per strip
       A.hm = B.whm + gw; A.err = B.err;

@@ -85,6 +85,8 @@ def lib() -> ctypes.CDLL:
         "nw_align_pair_percell": ([vp, vp, i64, vp, i64, P(_Scoring), P(i64), vp, i64, P(i64)],
                                   ctypes.c_int),
         "nw_align_pair_percell_dev": ([vp, vp, i64, vp, i64, P(_Scoring), vp, vp, vp], ctypes.c_int),
+        "nw_align_pair_linear": ([vp, vp, i64, vp, i64, P(_Scoring), i64, P(i64), vp, i64, P(i64)],
+                                 ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -100,7 +102,8 @@ EXPORTED = ("nw_ctx_create", "nw_ctx_destroy", "nw_strerror", "nw_last_error", "
             "nw_tb_free", "nw_align_batch", "nw_align_batch_dev", "nw_batch_ops_offsets",
             "nw_score_only_cblock", "nw_cblock_recv_bytes", "nw_score_only_cblock_rank_dev",
             "nw_msa_center_star", "nw_msa_center_star_dev", "nw_msa_info", "nw_msa_rows",
-            "nw_msa_rows_dev", "nw_msa_free", "nw_align_pair_percell", "nw_align_pair_percell_dev")
+            "nw_msa_rows_dev", "nw_msa_free", "nw_align_pair_percell", "nw_align_pair_percell_dev",
+            "nw_align_pair_linear")
 
 
 def _scoring(sc) -> tuple[_Scoring, object]:
@@ -416,3 +419,16 @@ def nw_align_pair_percell_dev(ctx: Context, d_a, d_b, sc, d_score, d_ops, d_len)
     ctx._check(lib().nw_align_pair_percell_dev(ctx.handle, _ptr(d_a), d_a.numel(), _ptr(d_b),
                                                d_b.numel(), ctypes.byref(s), _ptr(d_score),
                                                _ptr(d_ops), _ptr(d_len)))
+
+
+def nw_align_pair_linear(ctx: Context, a, b, sc, dirs_budget: int = 0) -> tuple[int, np.ndarray]:
+    """Score + canonical traceback with at most ~dirs_budget bytes of directions on
+    the device (checkpointed refill, NEXT #3). Returns (score, forward ops)."""
+    a, b = _host_bytes(a), _host_bytes(b)
+    s, keep = _scoring(sc)
+    score, ln = ctypes.c_int64(0), ctypes.c_int64(0)
+    ops = np.empty(max(len(a) + len(b), 1), dtype=np.uint8)
+    ctx._check(lib().nw_align_pair_linear(ctx.handle, _ptr(a), len(a), _ptr(b), len(b),
+                                          ctypes.byref(s), dirs_budget, ctypes.byref(score),
+                                          ops.ctypes.data, len(ops), ctypes.byref(ln)))
+    return score.value, ops[:ln.value].copy()
