@@ -367,7 +367,7 @@ nw_status init_small(nw_ctx* c, int nints, ZeroRanges zr = ZeroRanges{{nullptr, 
 nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb, long long n,
                     const nw_scoring* sc, long long* d_score, nw_tb* tb, int kr,
                     unsigned long long* ckpt = nullptr, int ck_every = 0, long long ck_stride = 0,
-                    const unsigned long long* top_row = nullptr);
+                    const unsigned long long* top_row = nullptr, unsigned top_tag = 0);
 
 }  // namespace
 
@@ -383,7 +383,7 @@ namespace {
 nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb, long long n,
                     const nw_scoring* sc, long long* d_score, nw_tb* tb, int kr,
                     unsigned long long* ckpt, int ck_every, long long ck_stride,
-                    const unsigned long long* top_row) {
+                    const unsigned long long* top_row, unsigned top_tag) {
   const int R = 32 * kr;
   const int nstrips = (int)((m + R - 1) / R);
   const bool dirs = tb != nullptr;
@@ -400,7 +400,8 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     A.dirs = dirs ? tb->dirs : nullptr;
     A.wpl = dirs ? tb->wpl : 0;
     A.hm = hm; A.err = errf;
-    A.ckpt = ckpt; A.ck_every = ck_every; A.ck_stride = ck_stride; A.top_row = top_row;
+    A.ckpt = ckpt; A.ck_every = ck_every; A.ck_stride = ck_stride;
+    A.top_row = top_row; A.top_tag = top_tag;
     const bool profreg = sc->K <= 4;
     const size_t smem = profreg ? 0 : (size_t)sc->K * R;
     const bool d16 = !dirs && kr == 16;
@@ -1583,7 +1584,9 @@ nw_status linear_core(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b
     st = new_tb(c, mm, col, sc, kr, &tb);
     if (st) break;
     const unsigned long long* top = sg > 0 ? ckpt + (sg - 1) * bstr : nullptr;
-    st = pair_core(c, ca + r0, mm, cb, col, sc, c->d_score, tb, kr, nullptr, 0, 0, top);
+    // the checkpoint row above segment sg was written by strip sg*K - 1: tag sg*K
+    st = pair_core(c, ca + r0, mm, cb, col, sc, c->d_score, tb, kr, nullptr, 0, 0, top,
+                   (unsigned)(sg * K));
     int* d_exit = c->d_ints + 6;
     if (!st) st = grow(c, c->d_rev, c->rev_cap, (size_t)(mm + col));
     if (!st) st = traceback_core(c, tb, d_ops, sg == 0, d_exit);

@@ -56,7 +56,8 @@ struct FillArgs {
   unsigned long long* ckpt;           // strips s with (s+1) % ck_every == 0 write their bottom
   int ck_every;                       //   row here (tagged, slot (s+1)/ck_every - 1) instead of
   long long ck_stride;                //   the ring; strip s+1 reads it from there
-  const unsigned long long* top_row;  // tagged H' of the row above strip 0 (null: zeros)
+  const unsigned long long* top_row;  // tagged H' of the row above strip 0 (null: zeros),
+  unsigned top_tag;                   //   tagged top_tag (the checkpoint writer's s+1)
 };
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
@@ -106,7 +107,7 @@ struct StripCtx {
   const uint8_t* b;
   const int8_t* sprof;              // shared profile [K][R] (not PROFREG)
   const void* bnd_in;               // boundary row read (strip s-1's bottom), null for s == 0
-  const unsigned long long* top_in; // strip 0 of a segment: the checkpoint row above it
+  unsigned tag_in;                  // tag the bnd_in entries carry (strip s-1 wrote s)
   void* bnd_out;                    // boundary row written (this strip's bottom)
   uint16_t* dir_base;               // this lane's decision-bit halfwords
   int* err;
@@ -132,8 +133,6 @@ __device__ __forceinline__ unsigned long long chunk_issue(const StripCtx& C, int
   const int jj = c0 + 1 + C.lane;
   if (C.lane >= 8 || jj > C.n) return 0ull;
   if (!MULTIWARP) return (unsigned)static_cast<const int*>(C.bnd_in)[jj];
-  if (C.top_in)  // a checkpoint row (complete before the launch): re-tag it for strip 0
-    return (C.top_in[jj] & 0xffffffffull) | ((unsigned long long)(unsigned)C.s << 32);
   return ld_relaxed_u64(static_cast<const unsigned long long*>(C.bnd_in) + jj);
 }
 
@@ -142,7 +141,7 @@ __device__ __forceinline__ int chunk_verify(const StripCtx& C, int c0, unsigned 
   if (!MULTIWARP) return (int)(unsigned)v;
   const int jj = c0 + 1 + C.lane;
   const bool need = C.lane < 8 && jj <= C.n;
-  const unsigned tag = (unsigned)C.s;  // strip s-1 writes tag (s-1)+1
+  const unsigned tag = C.tag_in;  // strip s-1 writes tag (s-1)+1 (a checkpoint row: top_tag)
   bool ok = !need || (unsigned)(v >> 32) == tag;
   if (__all_sync(FULL, ok)) return (int)(unsigned)v;
   const unsigned long long* p = static_cast<const unsigned long long*>(C.bnd_in) + jj;
@@ -280,7 +279,11 @@ __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, 
   char* bnd = static_cast<char*>(A.bnd);
   C.bnd_in = (s > 0) ? bnd + esz * (size_t)((s % A.nslots) * A.bstride) : nullptr;
   C.bnd_out = bnd + esz * (size_t)(((s + 1) % A.nslots) * A.bstride);
-  C.top_in = (MULTIWARP && s == 0) ? A.top_row : nullptr;
+  C.tag_in = (unsigned)s;
+  if (MULTIWARP && s == 0 && A.top_row != nullptr) {  // a segment's strip 0: the checkpoint row
+    C.bnd_in = A.top_row;
+    C.tag_in = A.top_tag;
+  }
   if (MULTIWARP && A.ckpt != nullptr) {  // checkpoint strips hand their row over through ckpt
     if ((s + 1) % A.ck_every == 0) C.bnd_out = A.ckpt + (long long)((s + 1) / A.ck_every - 1) * A.ck_stride;
     if (s > 0 && s % A.ck_every == 0) C.bnd_in = A.ckpt + (long long)(s / A.ck_every - 1) * A.ck_stride;
@@ -297,7 +300,7 @@ __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, 
     C.hm_lane = rr / KR; C.hm_r = rr % KR; C.hm_t = n - 1 + C.hm_lane;
   }
   st.bc_nxt = __ldg(A.b - lane);  // b_{j-1} for step 0 (j = 1 - lane)
-  const bool has_top = s > 0 || C.top_in != nullptr;
+  const bool has_top = C.bnd_in != nullptr;
   if (has_top) st.chunk_nxt = chunk_verify<MULTIWARP>(C, 0, chunk_issue<MULTIWARP>(C, 0));
   const int ngrp = (n + 31 + 7) / 8;  // steps 0 .. n+30 in groups of 8
 #pragma unroll 1

@@ -130,7 +130,7 @@ __device__ __forceinline__ void strip_sweep_d16(const FillArgs& A, int s, int la
   st.chunk_cur = st.chunk_nxt = 0;
   st.bc_nxt = __ldg(A.b - 2 * lane);  // code at jT - 1 for step 0
   StripCtx C;
-  C.top_in = nullptr;
+  C.tag_in = (unsigned)s;
   C.b = A.b;
   C.sprof = nullptr;
   const size_t esz = MULTIWARP ? 8 : 4;

@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       A.a = B.codes + ao; A.b = B.codes + bo; A.prof = B.prof; A.K = B.K;
       constexpr int RS = PACKED ? 32 * KR16 : R;  // strip height of the sweep in use
       A.m = m; A.n = n; A.nstrips = (m + RS - 1) / RS; A.nslots = 2;
-      A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr; A.ckpt = nullptr; A.ck_every = 0; A.ck_stride = 0; A.top_row = nullptr;
+      A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr; A.ckpt = nullptr; A.ck_every = 0; A.ck_stride = 0; A.top_row = nullptr; A.top_tag = 0;
       A.dirs = wd;
       A.wpl = PACKED ? (n + 63 + 7) / 8 : (n + 31 + 7) / 8;  // 8-step groups per strip
       A.hm = B.whm + gw; A.err = B.err;
