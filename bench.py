@@ -52,6 +52,8 @@ WORKLOADS = {
     "c1p": "C1 with the paper's per-cell kernel (Code 1, corrected; ablation baseline, NEXT #4)",
     "c5tb": "C5 with the full canonical traceback: checkpointed refill within half the free "
             "HBM for directions (SURVEY.md 8(f) NEXT #3)",
+    "c1co": "C1 co-optimal alignments: exact count + the first 256 in depth-first pi order (NEXT #2)",
+    "c2co": "C2 co-optimal alignments: exact count + the first 256 in depth-first pi order (NEXT #2)",
     "msa": "center-star MSA of the C3 set (2,048 DNA sequences of 500-2,000 bp): all-pairs "
            "scores, center, 2,047 alignments with traceback, union-gap merge (SURVEY.md 8(f) NEXT #1)",
 }
@@ -132,8 +134,8 @@ def load_peaks():
 def cpu_oracle_sample(workload: str, budget_s: float = 15.0):
     """Time the oracle (as it stands) on a bounded sample of the workload."""
     import oracle
-    if workload in ("c1", "c2", "c1p", "c2p", "c5tb"):
-        a, b = (nwgen.config_c1() if workload in ("c1", "c1p") else
+    if workload in ("c1", "c2", "c1p", "c2p", "c5tb", "c1co", "c2co"):
+        a, b = (nwgen.config_c1() if workload in ("c1", "c1p", "c1co") else
                 nwgen.config_c5() if workload == "c5tb" else nwgen.config_c2())
         # full pair if it fits the budget (~0.06 GCUPS single-core full+dirs), else a prefix
         side = len(a)
@@ -213,8 +215,10 @@ class PairWorkload:
         self.workload = workload
         self.percell = workload in ("c1p", "c2p")
         self.linear = workload == "c5tb"
+        self.coopt = workload in ("c1co", "c2co")
         gen = {"c1": nwgen.config_c1, "c2": nwgen.config_c2, "c5": nwgen.config_c5,
-               "c1p": nwgen.config_c1, "c2p": nwgen.config_c2, "c5tb": nwgen.config_c5}[workload]
+               "c1p": nwgen.config_c1, "c2p": nwgen.config_c2, "c5tb": nwgen.config_c5,
+               "c1co": nwgen.config_c1, "c2co": nwgen.config_c2}[workload]
         a, b = gen()
         self.a, self.b = a, b
         self.m, self.n = len(a), len(b)
@@ -230,7 +234,9 @@ class PairWorkload:
         self.pipeline = workload == "c5" and int(os.environ.get("WORLD_SIZE", "1")) > 1
 
     def step(self):
-        if self.linear:  # host-pointer API (it synchronises per segment); inputs 2 MB
+        if self.coopt:  # host-pointer API (synchronous)
+            self.nwb.nw_cooptimal(self.ctx, self.a, self.b, self.sc, 256)
+        elif self.linear:  # host-pointer API (it synchronises per segment); inputs 2 MB
             self.nwb.nw_align_pair_linear(self.ctx, self.a, self.b, self.sc)
         elif self.percell:
             self.nwb.nw_align_pair_percell_dev(self.ctx, self.da, self.db, self.sc, self.d_score,
@@ -248,6 +254,9 @@ class PairWorkload:
 
     def step_host(self):
         """The same step through the host-pointer ABI (e2e)."""
+        if self.coopt:
+            cnt, sat, paths = self.nwb.nw_cooptimal(self.ctx, self.a, self.b, self.sc, 256)
+            return 8 + 8 * 257 + sum(len(p) for p in paths)
         if self.linear:
             score, ops = self.nwb.nw_align_pair_linear(self.ctx, self.a, self.b, self.sc)
             return 8 + 8 + len(ops)
@@ -382,7 +391,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     ctx = nwb.Context(local, stream.cuda_stream)
     wl = args.workload
-    if wl in ("c1", "c2", "c5", "c1p", "c2p", "c5tb"):
+    if wl in ("c1", "c2", "c5", "c1p", "c2p", "c5tb", "c1co", "c2co"):
         W = PairWorkload(ctx, torch, wl, rank)
     elif wl == "msa":
         W = MsaWorkload(ctx, torch, wl, rank)
@@ -428,7 +437,7 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    if wl in ("c1", "c2", "msa", "c1p", "c2p", "c5tb") or (wl == "c5" and world == 1):
+    if wl in ("c1", "c2", "msa", "c1p", "c2p", "c5tb", "c1co", "c2co") or (wl == "c5" and world == 1):
         cells_all = W.cells * world  # replicas: every rank aligns its own pair / set
     elif wl == "c5":
         cells_all = W.cells          # one pair pipelined across the ranks
@@ -438,7 +447,7 @@ def run_ours(args):
     # ---- e2e through the host-pointer ABI
     torch.cuda.synchronize()
     barrier()
-    e2e_steps = max(1, min(args.steps, 5 if wl in ("c3", "c4", "msa") else 2 if wl == "c5tb" else args.steps))
+    e2e_steps = max(1, min(args.steps, 5 if wl in ("c3", "c4", "msa") else 2 if wl in ("c5tb", "c2co") else args.steps))
     d2h = 0
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
@@ -453,7 +462,7 @@ def run_ours(args):
            "d2h_bytes_per_step": d2h}
     # ---- roofline of the dominant kernel (the fill)
     fill_avg_ms = fill_ms / max(fill_n, 1)
-    mode = "dirs" if (wl in ("c1", "c2", "c4", "c1p", "c2p", "c5tb")) else "score"
+    mode = "dirs" if (wl in ("c1", "c2", "c4", "c1p", "c2p", "c5tb", "c1co", "c2co")) else "score"
     ops = OPS_PER_CELL[mode]
     cells_per_launch = W.cells
     achieved = cells_per_launch * ops / (fill_avg_ms / 1e3) / 1e12 if fill_n else None
@@ -486,11 +495,11 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "strong" if (wl == "c5" and world > 1) else "weak", "vs_baseline": None,
         # arithmetic of the fill kernel in use: int32 strips, or two 16-bit cells per register
-        "dtype": "int32" if wl in ("c1", "c2", "c1p", "c2p", "c5tb") else "u16x2",
+        "dtype": "int32" if wl in ("c1", "c2", "c1p", "c2p", "c5tb", "c1co", "c2co") else "u16x2",
         **({"msa": {"center": W.center, "width": W.width}} if wl == "msa" else {}),
         "data": "synthetic (nwgen seeded, SURVEY.md §8(d) recipe)",
         "config": {"workload": WORKLOADS[wl], "cells_per_step": cells_all,
-                   "parallelism": (f"replicas{world}" if wl in ("c1", "c2", "msa", "c1p", "c2p", "c5tb") or (wl == "c5" and world == 1)
+                   "parallelism": (f"replicas{world}" if wl in ("c1", "c2", "msa", "c1p", "c2p", "c5tb", "c1co", "c2co") or (wl == "c5" and world == 1)
                                    else f"column-blocks{world}" if wl == "c5" else f"pairs-sharded{world}"),
                    "l2": "flushed between steps (256 MB write)"},
         "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roofline,

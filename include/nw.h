@@ -212,6 +212,19 @@ nw_status nw_align_pair_linear(nw_ctx *ctx, const uint8_t *a, int64_t m, const u
                                int64_t n, const nw_scoring *sc, int64_t dirs_budget,
                                int64_t *score, uint8_t *ops, int64_t cap, int64_t *len);
 
+/* ---- co-optimal alignments ----
+ * *count = number of optimal global alignments (paths from (m,n) to (0,0) along
+ * branches whose candidate equals H, borders forced), saturating at 2^64-1
+ * (*saturated = 1 then). With cap > 0 also the first cap of them in depth-first
+ * order, each cell's optimal branches tried in the tie order (the first is the
+ * canonical traceback; R24-R25, §3.13): path k is ops[ops_off[k] ..
+ * ops_off[k+1]) (forward codes 1/2/3), *nfound <= cap paths; enumeration stops
+ * early if ops_cap bytes are used up. Needs (m+1)(n+1) bytes of device memory
+ * for the branch masks when cap > 0. Host pointers, synchronous. */
+nw_status nw_cooptimal(nw_ctx *ctx, const uint8_t *a, int64_t m, const uint8_t *b, int64_t n,
+                       const nw_scoring *sc, int32_t cap, uint64_t *count, int32_t *saturated,
+                       uint8_t *ops, int64_t ops_cap, int64_t *ops_off, int32_t *nfound);
+
 /* ---- the paper's per-cell kernel, corrected ----
  * Ablation baseline, not the product path: one thread per cell spinning on its
  * up/left neighbours' direction codes (acquire/release), full H (int32) and

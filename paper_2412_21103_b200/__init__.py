@@ -8,7 +8,8 @@ from .nw import (NW_DIAG, batch_paths, NW_LEFT, NW_SCORE_ONLY, NW_TRACEBACK, NW_
                  nw_align_pair_dev, nw_batch_ops_offsets, nw_cblock_recv_bytes, nw_score_only, nw_score_only_cblock,
                  nw_score_only_cblock_rank_dev, nw_score_only_dev,
                  nw_traceback, nw_traceback_dev, Msa, nw_msa_center_star, nw_msa_center_star_dev,
-                 nw_align_pair_percell, nw_align_pair_percell_dev, nw_align_pair_linear)
+                 nw_align_pair_percell, nw_align_pair_percell_dev, nw_align_pair_linear,
+                 nw_cooptimal)
 
 __all__ = ["Context", "NWError", "Traceback", "lib", "nw_score_only", "nw_score_only_dev",
            "nw_score_only_cblock", "nw_score_only_cblock_rank_dev", "nw_cblock_recv_bytes",
@@ -16,4 +17,5 @@ __all__ = ["Context", "NWError", "Traceback", "lib", "nw_score_only", "nw_score_
            "nw_align_batch", "nw_align_batch_dev", "nw_batch_ops_offsets", "NW_DIAG", "NW_UP",
            "NW_LEFT", "NW_SCORE_ONLY", "NW_TRACEBACK", "batch_paths", "Msa",
            "nw_msa_center_star", "nw_msa_center_star_dev", "nw_align_pair_percell",
-           "nw_align_pair_percell_dev", "nw_align_pair_linear"]
+           "nw_align_pair_percell_dev", "nw_align_pair_linear",
+           "nw_cooptimal"]

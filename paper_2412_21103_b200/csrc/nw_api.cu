@@ -19,6 +19,7 @@
 #include "nw_launch.cuh"
 #include "nw_msa.cuh"
 #include "nw_percell.cuh"
+#include "nw_coopt.cuh"
 
 using namespace nwk;
 
@@ -1651,6 +1652,105 @@ nw_status nw_align_pair_linear(nw_ctx* c, const uint8_t* a, int64_t m, const uin
     memcpy(ops, path.data(), path.size());
   }
   return NW_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+nw_status nw_cooptimal(nw_ctx* c, const uint8_t* a, int64_t m, const uint8_t* b, int64_t n,
+                       const nw_scoring* sc, int32_t cap, uint64_t* count, int32_t* saturated,
+                       uint8_t* ops, int64_t ops_cap, int64_t* ops_off, int32_t* nfound) {
+  if (!c) return NW_E_INVAL;
+  if ((m > 0 && !a) || (n > 0 && !b) || !count || !saturated || cap < 0)
+    return fail(c, NW_E_INVAL, "NULL argument or cap < 0");
+  if (cap > 0 && (!ops_off || !nfound || (ops_cap > 0 && !ops)))
+    return fail(c, NW_E_INVAL, "NULL argument");
+  nw_status st = check_scoring(c, sc);
+  if (st) return st;
+  st = check_bounds(c, sc, m, n);
+  if (st) return st;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  st = upload_tables(c, sc);
+  if (st) return st;
+  constexpr long long R = R_MAX;
+  const long long la = pad16(PAD + m + R + PAD), lb = pad16(PAD + n + R + PAD);
+  st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
+  if (st) return st;
+  ZeroRanges zr{{c->d_codes, nullptr, nullptr, nullptr}, {la + lb, 0, 0, 0}};
+  st = init_small(c, 8, zr);
+  if (st) return st;
+  uint8_t *ca, *cb;
+  st = stage_pair(c, a, m, b, n, true, &ca, &cb);
+  if (st) return st;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const long long stride = (n + 1 + 3) & ~3ll;  // mask bytes per row
+  const int S = (int)((m + 31) / 32);
+  const size_t b_h = al(sizeof(int) * 2 * (n + 1)), b_n = al(sizeof(unsigned long long) * 2 * (n + 1)),
+               b_c = al(sizeof(unsigned long long)), b_p = al(sizeof(int) * ((size_t)S + 1)),
+               b_m = cap > 0 ? al((size_t)(m + 1) * (size_t)stride) : 0,
+               b_s = cap > 0 ? al((size_t)(m + n + 1)) : 0, b_o = cap > 0 ? al((size_t)ops_cap + 1) : 0,
+               b_oo = cap > 0 ? al(sizeof(long long) * ((size_t)cap + 1)) : 0, b_nf = al(sizeof(int));
+  char* mem = nullptr;
+  const size_t total = b_h + b_n + b_c + b_p + b_m + 2 * b_s + b_o + b_oo + b_nf;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&mem), total, c->stream);
+  if (e != cudaSuccess) return fail(c, NW_E_NOMEM, "co-optimal buffers of %zu bytes: %s", total, cudaGetErrorString(e));
+  char* q = mem;
+  int* rowH = reinterpret_cast<int*>(q); q += b_h;
+  unsigned long long* rowN = reinterpret_cast<unsigned long long*>(q); q += b_n;
+  unsigned long long* d_count = reinterpret_cast<unsigned long long*>(q); q += b_c;
+  int* d_prog = reinterpret_cast<int*>(q); q += b_p;
+  uint8_t* d_mask = cap > 0 ? reinterpret_cast<uint8_t*>(q) : nullptr; q += b_m;
+  uint8_t* d_rev = reinterpret_cast<uint8_t*>(q); q += b_s;
+  uint8_t* d_trial = reinterpret_cast<uint8_t*>(q); q += b_s;
+  uint8_t* d_ops = reinterpret_cast<uint8_t*>(q); q += b_o;
+  long long* d_oo = reinterpret_cast<long long*>(q); q += b_oo;
+  int* d_nf = reinterpret_cast<int*>(q);
+  CUDA_TRY(c, cudaMemsetAsync(d_prog, 0, b_p, c->stream));
+  unsigned long long one = 1;
+  CUDA_TRY(c, cudaMemcpyAsync(d_count, &one, sizeof one, cudaMemcpyHostToDevice, c->stream));  // m or n = 0
+  if (d_mask) {  // borders (R24): row 0 = L, column 0 = U, origin 0
+    CUDA_TRY(c, cudaMemsetAsync(d_mask, 4, (size_t)stride, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(d_mask, 0, 1, c->stream));
+    if (m > 0) CUDA_TRY(c, cudaMemset2DAsync(d_mask + stride, (size_t)stride, 2, 1, (size_t)m, c->stream));
+  }
+  if (m > 0 && n > 0) {
+    KernelTimer kt(c, 0);
+    nwk::CooptArgs A;
+    A.a = ca; A.b = cb; A.prof = c->d_prof; A.K = sc->K; A.m = (int)m; A.n = (int)n; A.S = S;
+    A.ticket = c->d_ints; A.progress = d_prog; A.rowH = rowH; A.rowN = rowN;
+    A.mask = reinterpret_cast<uint32_t*>(d_mask); A.stride = stride; A.count = d_count;
+    const int grid = std::min(S, c->sm_count * 8);
+    k_coopt_fill<<<grid, 32, 0, c->stream>>>(A);
+    LAUNCHED(c);
+  }
+  if (cap > 0) {
+    KernelTimer kt(c, 1);
+    const size_t sm_need = 2 * (size_t)(m + n + 1);
+    const int use_smem = sm_need <= 200 * 1024;
+    if (use_smem) cudaFuncSetAttribute(k_coopt_enum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_need);
+    k_coopt_enum<<<1, 32, use_smem ? sm_need : 0, c->stream>>>(
+        d_mask, (int)m, (int)n, stride, sc->tie[0], sc->tie[1], sc->tie[2], cap, d_ops, ops_cap,
+        d_oo, d_nf, d_rev, d_trial, use_smem);
+    LAUNCHED(c);
+  }
+  unsigned long long hc = 0;
+  int hnf = 0;
+  auto bail = [&](nw_status x) { cudaFreeAsync(mem, c->stream); return x; };
+  if (cudaMemcpyAsync(&hc, d_count, sizeof hc, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+    return bail(fail(c, NW_E_CUDA, "copy"));
+  if (cap > 0 && cudaMemcpyAsync(&hnf, d_nf, sizeof hnf, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+    return bail(fail(c, NW_E_CUDA, "copy"));
+  st = check_deferred(c);
+  if (st) return bail(st);
+  *count = hc;
+  *saturated = hc == ~0ull ? 1 : 0;
+  if (cap > 0) {
+    *nfound = hnf;
+    CUDA_TRY(c, cudaMemcpy(ops_off, d_oo, sizeof(long long) * ((size_t)hnf + 1), cudaMemcpyDeviceToHost));
+    if (ops_off[hnf] > 0) CUDA_TRY(c, cudaMemcpy(ops, d_ops, (size_t)ops_off[hnf], cudaMemcpyDeviceToHost));
+  }
+  return bail(NW_OK);
 }
 
 }  // extern "C"

@@ -87,6 +87,8 @@ def lib() -> ctypes.CDLL:
         "nw_align_pair_percell_dev": ([vp, vp, i64, vp, i64, P(_Scoring), vp, vp, vp], ctypes.c_int),
         "nw_align_pair_linear": ([vp, vp, i64, vp, i64, P(_Scoring), i64, P(i64), vp, i64, P(i64)],
                                  ctypes.c_int),
+        "nw_cooptimal": ([vp, vp, i64, vp, i64, P(_Scoring), i32, P(ctypes.c_uint64), P(i32), vp,
+                          i64, vp, P(i32)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("NW_LIB_PATH") and not hasattr(L, name):
@@ -105,7 +107,7 @@ EXPORTED = ("nw_ctx_create", "nw_ctx_destroy", "nw_strerror", "nw_last_error", "
             "nw_score_only_cblock", "nw_cblock_recv_bytes", "nw_score_only_cblock_rank_dev",
             "nw_msa_center_star", "nw_msa_center_star_dev", "nw_msa_info", "nw_msa_rows",
             "nw_msa_rows_dev", "nw_msa_free", "nw_align_pair_percell", "nw_align_pair_percell_dev",
-            "nw_align_pair_linear")
+            "nw_align_pair_linear", "nw_cooptimal")
 
 
 def _scoring(sc) -> tuple[_Scoring, object]:
@@ -434,3 +436,19 @@ def nw_align_pair_linear(ctx: Context, a, b, sc, dirs_budget: int = 0) -> tuple[
                                           ctypes.byref(s), dirs_budget, ctypes.byref(score),
                                           ops.ctypes.data, len(ops), ctypes.byref(ln)))
     return score.value, ops[:ln.value].copy()
+
+
+def nw_cooptimal(ctx: Context, a, b, sc, cap: int = 0):
+    """(count, saturated, paths): the number of optimal alignments (saturating
+    uint64) and, with cap > 0, the first cap of them in depth-first pi order."""
+    a, b = _host_bytes(a), _host_bytes(b)
+    s, keep = _scoring(sc)
+    cnt, sat, nf = ctypes.c_uint64(0), ctypes.c_int32(0), ctypes.c_int32(0)
+    ops_cap = cap * (len(a) + len(b))
+    ops = np.empty(max(ops_cap, 1), dtype=np.uint8)
+    off = np.zeros(cap + 1, dtype=np.int64)
+    ctx._check(lib().nw_cooptimal(ctx.handle, _ptr(a), len(a), _ptr(b), len(b), ctypes.byref(s),
+                                  cap, ctypes.byref(cnt), ctypes.byref(sat), ops.ctypes.data,
+                                  ops_cap, off.ctypes.data, ctypes.byref(nf)))
+    paths = [ops[off[k]:off[k + 1]].copy() for k in range(nf.value)] if cap else []
+    return cnt.value, bool(sat.value), paths
