@@ -730,8 +730,10 @@ static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops, bool
     {
       auto kchain = kr == 2 ? k_tb_chain<2> : (kr == 4 ? k_tb_chain<4> : k_tb_chain<8>);
       // exact walks: windows of ~96 KB of decision bits left of the entry
-      const int win_groups = 96 * 1024 / gw_bytes;
-      const int left_exact = (win_groups - 6) * 8;
+      // a window of 2R + 256 columns left of the entry (re-staged further left
+      // when a long gap leaves it): staging, not the walk, dominated at 96 KB
+      const int left_exact = 2 * R + 256;
+      const int win_groups = left_exact / 8 + 6;
       const int CH = std::max(1, std::min(S, (int)(64 * 1024 / (B.nb * 4))));
       const size_t smem = (size_t)CH * B.nb * 4 + (size_t)win_groups * gw_bytes;
       cudaFuncSetAttribute(kchain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
