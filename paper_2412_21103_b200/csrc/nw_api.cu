@@ -261,7 +261,8 @@ void launch_score(const FillArgs& A, bool profreg, int grid, size_t smem, cudaSt
 bool dispatch_fill(bool dirs, int pi, int kr, bool profreg, const FillArgs& A, int grid,
                    size_t smem, cudaStream_t st, bool d16 = false) {
   if (!dirs && d16) {  // packed difference form, KR rows per lane (2 per register)
-    if (kr == 16) launch_fill_t<16, false, true, 123, true>(A, grid, smem, st);
+    if (kr == 32) launch_fill_t<32, false, true, 123, true>(A, grid, smem, st);
+    else if (kr == 16) launch_fill_t<16, false, true, 123, true>(A, grid, smem, st);
     else if (kr == 8) launch_fill_t<8, false, true, 123, true>(A, grid, smem, st);
     else launch_fill_t<4, false, true, 123, true>(A, grid, smem, st);
     return true;
@@ -405,7 +406,7 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     A.top_row = top_row; A.top_tag = top_tag;
     const bool profreg = sc->K <= 4;
     const size_t smem = profreg ? 0 : (size_t)sc->K * R;
-    const bool d16 = !dirs && kr == 16;
+    const bool d16 = !dirs && kr >= 16;
     // persistent grid: one warp per CTA, at most the resident capacity
     int per_sm = 16;
     int grid = std::min<long long>(nstrips, (long long)c->sm_count * per_sm);
@@ -520,7 +521,10 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
   // halves the ALU work per cell but doubles the lane skew, so it only pays when
   // there are enough 512-row strips to fill the GPU (measured: 1M^2 2.4 -> 5.9
   // TCUPS; 20k^2 1.44 -> 2.14 ms, slower)
-  if (!want_dirs && d16_ok(sc) && m >= 32LL * 16 * 150) kr = 16;
+  // and 32 rows per lane once there are >= ~150 strips of 1,024 rows (1M^2: 5.4 -> 6.2
+  // TCUPS; 64 rows: 4.5). NW_D16_KR overrides (16 or 32).
+  if (!want_dirs && d16_ok(sc) && m >= 32LL * 16 * 150)
+    kr = env_int("NW_D16_KR", m >= 32LL * 32 * 150 ? 32 : 16, 16) >= 32 ? 32 : 16;
   st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
   if (st) return st;
   const long long bbytes = (long long)sizeof(unsigned long long) * 2 * bnd_stride(n);

@@ -103,7 +103,7 @@ __device__ __forceinline__ void d16_group(D16State<KR>& st, const StripCtx& C, i
 // *A.hm (atomic for MULTIWARP; the batch kernel's warp owns its accumulator).
 template <int KR, bool MULTIWARP>
 __device__ __forceinline__ void strip_sweep_d16(const FillArgs& A, int s, int lane) {
-  static_assert(KR % 2 == 0 && KR <= 16, "KR must be even");
+  static_assert(KR % 2 == 0 && KR <= 32, "KR must be even");
   constexpr int H = KR / 2;
   constexpr int R = 32 * KR;
   const int n = A.n;

@@ -8,7 +8,7 @@
 namespace nwk {
 
 constexpr int KR_MAX = 8;    // rows per lane: single-pair kernels pick 2, 4 or 8 per shape
-constexpr int R_MAX = 32 * 16;  // tallest strip of any sweep (packed KR = 16): code padding
+constexpr int R_MAX = 32 * 32;  // tallest strip of any sweep (packed KR = 32): code padding
 constexpr int KR_BATCH = 8;  // rows per lane, batch kernel
 
 // DIRS = true launchers, one instantiation per tie order PI (nw_inst_<PI>.cu)
