@@ -406,7 +406,7 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     A.top_row = top_row; A.top_tag = top_tag;
     const bool profreg = sc->K <= 4;
     const size_t smem = profreg ? 0 : (size_t)sc->K * R;
-    const bool d16 = !dirs && kr >= 16;
+    const bool d16 = !dirs && (kr >= 16 || (!ckpt && getenv("NW_D16_FORCE") && d16_ok(sc)));
     // persistent grid: one warp per CTA, at most the resident capacity
     int per_sm = 16;
     int grid = std::min<long long>(nstrips, (long long)c->sm_count * per_sm);
@@ -525,6 +525,11 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
   // TCUPS; 64 rows: 4.5). NW_D16_KR overrides (16 or 32).
   if (!want_dirs && d16_ok(sc) && m >= 32LL * 16 * 150)
     kr = env_int("NW_D16_KR", m >= 32LL * 32 * 150 ? 32 : 16, 16) >= 32 ? 32 : 16;
+  // experiments: NW_D16_FORCE=<4|8|16|32> runs any score-only pair in the packed form
+  if (!want_dirs && d16_ok(sc) && getenv("NW_D16_FORCE")) {
+    const int f = env_int("NW_D16_FORCE", 16, 4);
+    kr = f >= 32 ? 32 : (f >= 16 ? 16 : (f >= 8 ? 8 : 4));
+  }
   st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
   if (st) return st;
   const long long bbytes = (long long)sizeof(unsigned long long) * 2 * bnd_stride(n);

@@ -281,10 +281,12 @@ def batch_paths(ops: np.ndarray, ops_off: np.ndarray, ops_len: np.ndarray) -> li
     return [ops[ops_off[k]:ops_off[k] + ops_len[k]] for k in range(len(ops_len))]
 
 
-def nw_align_batch(ctx: Context, seqs, offs, pairs, sc, flags: int = NW_SCORE_ONLY):
+def nw_align_batch(ctx: Context, seqs, offs, pairs, sc, flags: int = NW_SCORE_ONLY, out=None):
     """Host batch. Returns scores (int32[npairs]); with NW_TRACEBACK returns
     (scores, ops, ops_off, ops_len): pair k's path is ops[ops_off[k]:ops_off[k]+ops_len[k]]
-    (see batch_paths)."""
+    (see batch_paths). `out` = caller-owned output arrays to fill instead of fresh ones
+    (scores, or (scores, ops, ops_off, ops_len) with NW_TRACEBACK), e.g. page-locked
+    buffers so the library's copies run at DMA speed."""
     seqs = _host_bytes(seqs)
     offs = np.ascontiguousarray(offs, dtype=np.int64)
     nseq = len(offs) - 1
@@ -294,15 +296,25 @@ def nw_align_batch(ctx: Context, seqs, offs, pairs, sc, flags: int = NW_SCORE_ON
         pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
         npairs = len(pairs)
     s, keep = _scoring(sc)
-    scores = np.empty(npairs, dtype=np.int32)
     tbk = bool(flags & NW_TRACEBACK)
-    ops_off = np.empty(npairs + 1, dtype=np.int64) if tbk else None
-    if tbk:
-        tot = int(nw_batch_ops_offsets(offs, pairs)[-1])
-        ops = np.empty(max(tot, 1), dtype=np.uint8)
-        ops_len = np.empty(max(npairs, 1), dtype=np.int32)
+    if out is not None:
+        scores, ops, ops_off, ops_len = (out, None, None, None) if not tbk else out
+        if tbk:
+            tot = int(nw_batch_ops_offsets(offs, pairs)[-1])
+            if (len(scores) < npairs or len(ops_off) < npairs + 1 or len(ops) < max(tot, 1)
+                    or len(ops_len) < max(npairs, 1)):
+                raise ValueError("nw_align_batch: out buffers too small")
+        elif len(scores) < npairs:
+            raise ValueError("nw_align_batch: out buffer too small")
     else:
-        ops = ops_len = None
+        scores = np.empty(npairs, dtype=np.int32)
+        ops_off = np.empty(npairs + 1, dtype=np.int64) if tbk else None
+        if tbk:
+            tot = int(nw_batch_ops_offsets(offs, pairs)[-1])
+            ops = np.empty(max(tot, 1), dtype=np.uint8)
+            ops_len = np.empty(max(npairs, 1), dtype=np.int32)
+        else:
+            ops = ops_len = None
     ctx._check(lib().nw_align_batch(ctx.handle, _ptr(seqs), offs.ctypes.data, nseq, _ptr(pairs),
                                     npairs, ctypes.byref(s), flags, _ptr(scores), _ptr(ops_off),
                                     _ptr(ops), _ptr(ops_len)))

@@ -1,0 +1,8 @@
+# ncu captures of the current batch kernels (C3 packed score-only, C4 packed traceback)
+# and the C5 difference-form fill (one launch each).
+set -x
+mkdir -p gpurun_out
+ncu --set full --clock-control none --import-source on -k regex:k_batch -s 1 -c 1 -o gpurun_out/prof_c4_batch -f python bench.py --workload c4 --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_c4.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_batch -s 1 -c 1 -o gpurun_out/prof_c3_batch -f python bench.py --workload c3 --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_c3.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_fill_pair -s 3 -c 1 -o gpurun_out/prof_c5_fill -f python bench.py --workload c5 --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_c5.log 2>&1
+tail -2 gpurun_out/ncu_c3.log gpurun_out/ncu_c4.log gpurun_out/ncu_c5.log
