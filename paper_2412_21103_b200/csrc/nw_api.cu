@@ -262,6 +262,15 @@ bool dispatch_fill(bool dirs, int pi, int kr, bool profreg, const FillArgs& A, i
                    size_t smem, cudaStream_t st, bool d16 = false) {
   if (!dirs && d16) {  // packed difference form, KR rows per lane (2 per register)
     if (kr == 32) launch_fill_t<32, false, true, 123, true>(A, grid, smem, st);
+    else if (kr == 30) launch_fill_t<30, false, true, 123, true>(A, grid, smem, st);
+    else if (kr == 28) launch_fill_t<28, false, true, 123, true>(A, grid, smem, st);
+    else if (kr == 26) launch_fill_t<26, false, true, 123, true>(A, grid, smem, st);
+    else if (kr == 24) launch_fill_t<24, false, true, 123, true>(A, grid, smem, st);
+    else if (kr == 22) launch_fill_t<22, false, true, 123, true>(A, grid, smem, st);
+    else if (kr == 20) launch_fill_t<20, false, true, 123, true>(A, grid, smem, st);
+    else if (kr == 18) launch_fill_t<18, false, true, 123, true>(A, grid, smem, st);
+    else if (kr == 14) launch_fill_t<14, false, true, 123, true>(A, grid, smem, st);
+    else if (kr == 12) launch_fill_t<12, false, true, 123, true>(A, grid, smem, st);
     else if (kr == 16) launch_fill_t<16, false, true, 123, true>(A, grid, smem, st);
     else if (kr == 8) launch_fill_t<8, false, true, 123, true>(A, grid, smem, st);
     else launch_fill_t<4, false, true, 123, true>(A, grid, smem, st);
@@ -402,11 +411,12 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     A.dirs = dirs ? tb->dirs : nullptr;
     A.wpl = dirs ? tb->wpl : 0;
     A.hm = hm; A.err = errf;
+    A.poll_ns = (unsigned)env_int("NW_POLL_NS", 0, 1);
     A.ckpt = ckpt; A.ck_every = ck_every; A.ck_stride = ck_stride;
     A.top_row = top_row; A.top_tag = top_tag;
     const bool profreg = sc->K <= 4;
     const size_t smem = profreg ? 0 : (size_t)sc->K * R;
-    const bool d16 = !dirs && (kr >= 16 || (!ckpt && getenv("NW_D16_FORCE") && d16_ok(sc)));
+    const bool d16 = !dirs && (kr >= 12 || (!ckpt && getenv("NW_D16_FORCE") && d16_ok(sc)));
     // persistent grid: one warp per CTA, at most the resident capacity
     int per_sm = 16;
     int grid = std::min<long long>(nstrips, (long long)c->sm_count * per_sm);
@@ -523,12 +533,22 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
   // TCUPS; 20k^2 1.44 -> 2.14 ms, slower)
   // and 32 rows per lane once there are >= ~150 strips of 1,024 rows (1M^2: 5.4 -> 6.2
   // TCUPS; 64 rows: 4.5). NW_D16_KR overrides (16 or 32).
-  if (!want_dirs && d16_ok(sc) && m >= 32LL * 16 * 150)
-    kr = env_int("NW_D16_KR", m >= 32LL * 32 * 150 ? 32 : 16, 16) >= 32 ? 32 : 16;
+  // The strips of one pair advance in lock-step (each waits on the one above), so
+  // the pair runs at the pace of the most loaded SM sub-partition: the rows per
+  // lane are the smallest even KR >= 16 that keeps the strip count within two
+  // warps per sub-partition (1M^2: KR 28 = 1,117 strips, 6.5 TCUPS, vs KR 32 =
+  // 977 strips 6.2 and KR 26 = 1,202 strips 5.5; tools/exp_c5kr.py).
+  if (!want_dirs && d16_ok(sc) && m >= 32LL * 16 * 150) {
+    int kd = 32;
+    for (int k = 16; k <= 32; k += 2)
+      if ((m + 32LL * k - 1) / (32LL * k) <= 8LL * c->sm_count) { kd = k; break; }
+    const int k = env_int("NW_D16_KR", kd, 12);
+    kr = (k >= 12 && k <= 32 && k % 2 == 0) ? k : kd;
+  }
   // experiments: NW_D16_FORCE=<4|8|16|32> runs any score-only pair in the packed form
   if (!want_dirs && d16_ok(sc) && getenv("NW_D16_FORCE")) {
     const int f = env_int("NW_D16_FORCE", 16, 4);
-    kr = f >= 32 ? 32 : (f >= 16 ? 16 : (f >= 8 ? 8 : 4));
+    kr = (f >= 12 && f <= 32 && f % 2 == 0) ? f : (f >= 32 ? 32 : (f >= 16 ? 16 : (f >= 8 ? 8 : 4)));
   }
   st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
   if (st) return st;

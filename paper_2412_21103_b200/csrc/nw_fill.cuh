@@ -33,9 +33,6 @@ namespace nwk {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int PAD = 64;  // code buffers carry PAD readable bytes before and after
-#ifndef NW_POLL_SLEEP_NS
-#define NW_POLL_SLEEP_NS 0
-#endif
 
 struct FillArgs {
   const uint8_t* a;    // row codes, a[-PAD .. m+PAD) readable
@@ -58,6 +55,7 @@ struct FillArgs {
   long long ck_stride;                //   the ring; strip s+1 reads it from there
   const unsigned long long* top_row;  // tagged H' of the row above strip 0 (null: zeros),
   unsigned top_tag;                   //   tagged top_tag (the checkpoint writer's s+1)
+  unsigned poll_ns = 0;               // back-off between re-polls of a boundary chunk (0: spin)
 };
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
@@ -112,6 +110,7 @@ struct StripCtx {
   uint16_t* dir_base;               // this lane's decision-bit halfwords
   int* err;
   int* hm;
+  unsigned poll_ns;
   int n, s, lane;
   int hm_lane, hm_r, hm_t;  // where H'(m, n) lives in this strip (hm_lane < 0: not here)
 };
@@ -145,11 +144,11 @@ __device__ __forceinline__ int chunk_verify(const StripCtx& C, int c0, unsigned 
   bool ok = !need || (unsigned)(v >> 32) == tag;
   if (__all_sync(FULL, ok)) return (int)(unsigned)v;
   const unsigned long long* p = static_cast<const unsigned long long*>(C.bnd_in) + jj;
-  // re-poll without sleeping: the waiting warp is usually alone on its SM
-  // sub-partition (one strip per warp), and a sleep adds its whole granularity
-  // to every strip-to-strip hand-off (NW_POLL_SLEEP_NS > 0 restores backoff)
+  // re-poll without sleeping by default: a single-pair warp is usually alone on its
+  // SM sub-partition, and a sleep adds its granularity to every strip hand-off;
+  // poll_ns > 0 backs off (frees issue slots for co-resident warps)
   for (long long it = 0;; ++it) {
-    if (NW_POLL_SLEEP_NS > 0) __nanosleep(NW_POLL_SLEEP_NS);
+    if (C.poll_ns) __nanosleep(C.poll_ns);
     if (!ok) {
       v = ld_relaxed_u64(p);
       ok = (unsigned)(v >> 32) == tag;
@@ -290,6 +289,7 @@ __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, 
   }
   C.dir_base = DIRS ? A.dirs + (long long)s * A.wpl * (KR * 32) + lane : nullptr;
   C.err = A.err;
+  C.poll_ns = A.poll_ns;
   C.hm = A.hm;
   C.n = n;
   C.s = s;

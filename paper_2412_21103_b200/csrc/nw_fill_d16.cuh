@@ -139,6 +139,7 @@ __device__ __forceinline__ void strip_sweep_d16(const FillArgs& A, int s, int la
   C.bnd_out = bnd + esz * (size_t)(((s + 1) % A.nslots) * A.bstride);
   C.dir_base = nullptr;
   C.err = A.err;
+  C.poll_ns = A.poll_ns;
   C.hm = A.hm;
   C.n = n;
   C.s = s;

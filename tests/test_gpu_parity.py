@@ -308,6 +308,26 @@ def test_score_only_tall_difference_form(ctx, m, n):
         assert nwb.nw_score_only(ctx, a, b, sc) == oracle.score(a, b, sc)
 
 
+@pytest.mark.parametrize("kr", [4, 8, 12, 14, 16, 18, 20, 22, 24, 26, 28, 30, 32])
+def test_score_only_difference_form_every_kr(ctx, monkeypatch, kr):
+    """The packed score-only sweep at every rows-per-lane setting the library can pick
+    (strip heights 128..1,024 rows, ragged last strips, one-strip pairs)."""
+    monkeypatch.setenv("NW_D16_FORCE", str(kr))
+    for k, (m, n) in enumerate([(2500, 700), (32 * kr * 3 + 17, 333), (5, 900), (1, 1)]):
+        a, b = _pair(9100 + 37 * kr + k, m, n)
+        for sc in (nwgen.PAPER_DNA, nwgen.Scoring(match=2, mismatch=-1, gap=-3)):
+            assert nwb.nw_score_only(ctx, a, b, sc) == oracle.score(a, b, sc), (kr, m, n)
+
+
+def test_c5_default_strip_choice(ctx):
+    """C5 at full size with the library's own rows-per-lane choice vs the closed forms."""
+    a, _ = nwgen.config_c5()
+    n = len(a)
+    sc = nwgen.PAPER_DNA
+    assert nwb.nw_score_only(ctx, a, a, sc) == n                         # a = b: m * match
+    assert nwb.nw_score_only(ctx, b"A" * n, b"C" * n, sc) == -n           # disjoint: -max(m, n)
+
+
 @pytest.mark.parametrize("G,w", [(2, 0), (3, 700)])
 def test_cblock_rank_api_concurrent_streams(ctx, monkeypatch, G, w):
     """The per-rank (real multi-GPU) entry point, with the G ranks as concurrent
