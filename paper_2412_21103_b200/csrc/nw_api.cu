@@ -57,6 +57,13 @@ struct nw_ctx {
   size_t scratch_cap = 0;
   void* d_aux = nullptr;        // batch perm/order/offs/pairs staging
   size_t aux_cap = 0;
+  void* h_stage = nullptr;      // page-locked staging for per-call host tables (batch order, offsets)
+  size_t stage_cap = 0;
+  cudaEvent_t stage_ev = nullptr;  // the last staged copy (the buffer is reused after it)
+  void* d_tbdirs = nullptr;     // two-phase batch traceback: every pair's decision words
+  size_t tbdirs_cap = 0;
+  long long* d_tdoff = nullptr; // ... and their word offsets per task
+  size_t tdoff_cap = 0;
   // kernel timing (nw_ctx_set_timing): event pairs per kernel class
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_open[2];
@@ -155,6 +162,36 @@ nw_status grow(nw_ctx* c, T*& p, size_t& cap, size_t need_bytes) {
   bytes = bytes + bytes / 4;
   CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, c->stream));
   cap = bytes;
+  return NW_OK;
+}
+
+// Host -> device copies of per-call tables through a page-locked staging buffer:
+// an async copy from pageable memory may wait for the stream, which leaves the
+// GPU idle while the host prepares the rest of the call. Waits only for the
+// previous staged copy (normally long finished) before reusing the buffer.
+struct StagedCopy { void* dst; const void* src; size_t bytes; };
+nw_status upload_staged(nw_ctx* c, const StagedCopy* cp, int k) {
+  size_t total = 0;
+  for (int i = 0; i < k; ++i) total += (cp[i].bytes + 255) & ~size_t(255);
+  if (total == 0) return NW_OK;
+  if (c->stage_ev) CUDA_TRY(c, cudaEventSynchronize(c->stage_ev));
+  else CUDA_TRY(c, cudaEventCreateWithFlags(&c->stage_ev, cudaEventDisableTiming));
+  if (total > c->stage_cap) {
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    c->h_stage = nullptr;
+    c->stage_cap = 0;
+    const size_t bytes = total + total / 4;
+    CUDA_TRY(c, cudaMallocHost(&c->h_stage, bytes));
+    c->stage_cap = bytes;
+  }
+  char* h = static_cast<char*>(c->h_stage);
+  for (int i = 0; i < k; ++i) {
+    if (!cp[i].bytes) continue;
+    memcpy(h, cp[i].src, cp[i].bytes);
+    CUDA_TRY(c, cudaMemcpyAsync(cp[i].dst, h, cp[i].bytes, cudaMemcpyHostToDevice, c->stream));
+    h += (cp[i].bytes + 255) & ~size_t(255);
+  }
+  CUDA_TRY(c, cudaEventRecord(c->stage_ev, c->stream));
   return NW_OK;
 }
 
@@ -660,6 +697,10 @@ void nw_ctx_destroy(nw_ctx* c) {
   if (c->d_rev) cudaFreeAsync(c->d_rev, c->stream);
   if (c->d_scratch) cudaFreeAsync(c->d_scratch, c->stream);
   if (c->d_aux) cudaFreeAsync(c->d_aux, c->stream);
+  if (c->stage_ev) { cudaEventSynchronize(c->stage_ev); cudaEventDestroy(c->stage_ev); }
+  if (c->h_stage) cudaFreeHost(c->h_stage);
+  if (c->d_tbdirs) cudaFreeAsync(c->d_tbdirs, c->stream);
+  if (c->d_tdoff) cudaFreeAsync(c->d_tdoff, c->stream);
   cudaStreamSynchronize(c->stream);
   for (auto& v : c->ev_open)
     for (auto& pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
@@ -1055,19 +1096,28 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
       return (h_offs[x + 1] - h_offs[x]) > (h_offs[y + 1] - h_offs[y]);
     });
   } else {
+    // counting sort on the cost quantised to NB levels (descending, stable): O(npairs),
+    // where a comparison sort of C4's 100k pairs took ~15 ms of host time per call
+    // and left the GPU idle (tools/exp_c4.py)
     aux.resize(npairs);
-    for (long long k = 0; k < npairs; ++k) aux[k] = (int)k;
-    auto cost = [&](int k) {
+    std::vector<long long> cst((size_t)npairs);
+    long long cmax = 1;
+    for (long long k = 0; k < npairs; ++k) {
       const int p = h_pairs[2 * k], q = h_pairs[2 * k + 1];
-      return (h_offs[p + 1] - h_offs[p]) * (h_offs[q + 1] - h_offs[q]);
-    };
-    std::stable_sort(aux.begin(), aux.end(), [&](int x, int y) { return cost(x) > cost(y); });
+      cst[k] = (h_offs[p + 1] - h_offs[p]) * (h_offs[q + 1] - h_offs[q]);
+      cmax = std::max(cmax, cst[k]);
+    }
+    constexpr int NB = 4096;
+    const double scale = (double)(NB - 1) / (double)cmax;
+    std::vector<int> cnt(NB + 1, 0);
+    auto bucket = [&](long long k) { return (NB - 1) - std::min(NB - 1, (int)((double)cst[k] * scale)); };
+    for (long long k = 0; k < npairs; ++k) ++cnt[bucket(k) + 1];
+    for (int b = 0; b < NB; ++b) cnt[b + 1] += cnt[b];
+    for (long long k = 0; k < npairs; ++k) aux[cnt[bucket(k)]++] = (int)k;
   }
   st = grow(c, c->d_aux, c->aux_cap, sizeof(int) * aux.size() + 16);
   if (st) return st;
-  if (!aux.empty())
-    CUDA_TRY(c, cudaMemcpyAsync(c->d_aux, aux.data(), sizeof(int) * aux.size(),
-                                cudaMemcpyHostToDevice, c->stream));
+
   // per-warp scratch
   const int warps_per_cta = 4;
   const bool profreg = sc->K <= 4;
@@ -1101,9 +1151,58 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
     if (const char* e = getenv("NW_BATCH_KR16")) packed_kr = atoi(e) == 8 ? 8 : 16;
   }
   const long long RS = packed_sweep ? 32 * (tbk && d16 ? packed_kr : 16) : R;
+  // Two-phase traceback (explicit pairs, packed flags): the fill keeps
+  // every pair's decision words in HBM (C4: 7.6 GB; the per-warp scratch of the
+  // in-warp walk spilled to HBM anyway) and k_batch_walk walks all pairs at once,
+  // one thread each, so the walk's dependent loads overlap across 100k pairs instead
+  // of idling 31 lanes of a filling warp. Pairs are cut into waves whose words fit
+  // the budget (half the free memory; NW_BATCH_TB_BUDGET bytes overrides).
+  const bool two_phase = tbk && d16 && h_pairs != nullptr && !getenv("NW_BATCH_WALK_INWARP");
+  std::vector<long long> tdoff, wave_end;
+  if (two_phase) {
+    const long long wpg = RS / 2;  // words per (strip, 8-step group): H packed rows x 32 lanes
+    auto words_of = [&](int k) {
+      const long long m = h_offs[h_pairs[2 * k] + 1] - h_offs[h_pairs[2 * k]];
+      const long long n = h_offs[h_pairs[2 * k + 1] + 1] - h_offs[h_pairs[2 * k + 1]];
+      return (m > 0 && n > 0) ? ((m + RS - 1) / RS) * ((n + 63 + 7) / 8) * wpg : 0LL;
+    };
+    long long all_words = 0;
+    for (long long k = 0; k < npairs; ++k) all_words += words_of((int)k);
+    long long budget = all_words;  // one wave when the kept buffer already holds it
+    if ((size_t)all_words * 4 > c->tbdirs_cap) {
+      size_t free_b = 0, tot_b = 0;
+      CUDA_TRY(c, cudaMemGetInfo(&free_b, &tot_b));
+      budget = (long long)((free_b + c->tbdirs_cap) / 2 / 4);
+    }
+    if (const char* e = getenv("NW_BATCH_TB_BUDGET")) budget = std::max(1LL, atoll(e) / 4);
+    tdoff.resize(npairs);
+    long long acc = 0, maxwave = 0;
+    for (long long t = 0; t < npairs; ++t) {
+      const long long words = words_of(aux[t]);
+      if (acc > 0 && acc + words > budget) {
+        wave_end.push_back(t);
+        maxwave = std::max(maxwave, acc);
+        acc = 0;
+      }
+      tdoff[t] = acc;
+      acc += words;
+    }
+    wave_end.push_back(npairs);
+    maxwave = std::max(maxwave, acc);
+    st = grow(c, c->d_tbdirs, c->tbdirs_cap, (size_t)std::max(1LL, maxwave) * 4);
+    if (st) return st;
+    st = grow(c, c->d_tdoff, c->tdoff_cap, sizeof(long long) * (size_t)std::max(1LL, npairs));
+    if (st) return st;
+  }
+  {
+    const StagedCopy cp[2] = {{c->d_aux, aux.data(), sizeof(int) * aux.size()},
+                              {c->d_tdoff, tdoff.data(), sizeof(long long) * tdoff.size()}};
+    st = upload_staged(c, cp, 2);
+    if (st) return st;
+  }
   const size_t smem_prof = profreg ? 0 : (((size_t)warps_per_cta * sc->K * RS + 15) & ~size_t(15));
   // packed traceback: per-warp window of NG_WIN groups x (RS/64) packed rows x 32 lanes words
-  const size_t smem_win = (tbk && d16) ? (size_t)warps_per_cta * NG_WIN * (RS / 64) * 32 * 4 : 0;
+  const size_t smem_win = (tbk && d16 && !two_phase) ? (size_t)warps_per_cta * NG_WIN * (RS / 64) * 32 * 4 : 0;
   const size_t smem = smem_prof + smem_win;
   int ctas_per_sm = 4;
   const long long nwarps = (long long)c->sm_count * ctas_per_sm * warps_per_cta;
@@ -1111,7 +1210,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   // direction scratch per warp, in halfwords: int32 sweep = halfword per (group,
   // row, lane); packed sweep = 32-bit word per (group, packed row, lane)
   const long long wpl = (maxlen + (packed_sweep ? 63 : 31) + 7) / 8;  // 8-step groups per strip
-  const long long dstride = !tbk ? 0
+  const long long dstride = (!tbk || two_phase) ? 0
       : packed_sweep ? ((maxlen + RS - 1) / RS) * wpl * (RS / 64) * 32 * 2
                      : ((maxlen + R - 1) / R) * wpl * KR_BATCH * 32;
   const size_t bytes_bnd = sizeof(int) * (size_t)(nwarps * 2 * bstride);
@@ -1144,6 +1243,10 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   B.ops = d_ops;
   B.ops_len = d_ops_len;
   B.win_off = (int)smem_prof;
+  B.tdirs = two_phase ? static_cast<uint32_t*>(c->d_tbdirs) : nullptr;
+  B.tdir_off = two_phase ? c->d_tdoff : nullptr;
+  B.task0 = 0;
+  B.task1 = npairs;
   B.X = sc->tie[0];
   B.Y = sc->tie[1];
   B.Z = sc->tie[2];
@@ -1154,6 +1257,33 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   // packed 16-bit sweep (score-only DNA-size alphabets) when s' = s - 2g >= 0 and
   // min(m,n) * max(s') <= 65535 for every pair (bounded by the longest sequence)
 
+  if (two_phase) {
+    long long t0 = 0;
+    for (const long long t1 : wave_end) {
+      if (t1 <= t0) continue;
+      B.task0 = t0;
+      B.task1 = t1;
+      if (t0 > 0) CUDA_TRY(c, cudaMemsetAsync(B.ticket, 0, sizeof(int), c->stream));
+      bool ok;
+      {
+        KernelTimer kt(c, 0);
+        ok = dispatch_batch(tbk, pi, profreg, u16, d16, packed_kr, B, grid, smem, c->stream);
+      }
+      if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
+      LAUNCHED(c);
+      CUDA_TRY(c, cudaGetLastError());
+      {
+        KernelTimer kt(c, 1);
+        const unsigned wg = (unsigned)((t1 - t0 + 255) / 256);
+        if (packed_kr == 8) k_batch_walk<8><<<wg, 256, 0, c->stream>>>(B);
+        else k_batch_walk<16><<<wg, 256, 0, c->stream>>>(B);
+      }
+      LAUNCHED(c);
+      CUDA_TRY(c, cudaGetLastError());
+      t0 = t1;
+    }
+    return NW_OK;
+  }
   bool ok;
   {
     KernelTimer kt(c, 0);

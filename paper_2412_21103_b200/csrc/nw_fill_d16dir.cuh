@@ -7,9 +7,10 @@
 // comparisons: each candidate is maximal exactly when its difference to Z is 0,
 //     D maximal <=> Z - (s-2g) == 0,   U maximal <=> U == 0,   L maximal <=> V == 0,
 // so the bits for the tie order pi = (X, Y, Z) are [q_X == 0], [q_Y == 0], tested
-// for both halves at once by VIADD.16x2(q, 0xffff'ffff) (the top bit of a half is
-// set iff that half was 0; every q < 2^15). Per packed register and 8 steps the
-// flags go to one 32-bit word (halves sharing a PRMT-gathered byte each):
+// for both halves at once by the 32-bit add q + 0x7fff7fff (bit 15 of a half is set
+// iff that half is nonzero; every q < 2^15, so no carry crosses a half), gathered by
+// one sign-replicating PRMT and inserted at bit q with one LOP3. Per packed register
+// and 8 steps the flags go to one 32-bit word (halves sharing a byte each):
 //   byte 0: X flags of the low cell, byte 1: X of the high cell,
 //   byte 2: Y flags of the low cell, byte 3: Y of the high cell,  step q at bit q.
 // Word index ((s*G + g)*H + k)*32 + lane, G = 8-step groups per strip.
@@ -86,10 +87,15 @@ __device__ __forceinline__ void d16dir_group(D16DirState<KR>& st, const FillArgs
       // q_X, q_Y in {D: dd, U: un, L: vn}; flag = [q == 0] per half (top bit of each half)
       const uint32_t qX = T::X == 1 ? dd : (T::X == 2 ? un : vn);
       const uint32_t qY = T::Y == 1 ? dd : (T::Y == 2 ? un : vn);
-      const uint32_t fX = __vadd2(qX, 0xffffffffu);
-      const uint32_t fY = __vadd2(qY, 0xffffffffu);
-      const uint32_t tk = prmt2(fX, fY, 0x7531u);  // bytes: X.lo, X.hi, Y.lo, Y.hi (flag = bit 7)
-      st.acc[k] = ((st.acc[k] >> 1) & 0x7f7f7f7fu) | (tk & 0x80808080u);
+      // bit 15 of a half of q + 0x7fff is set iff that half is nonzero (every q < 2^15,
+      // so no carry leaves a half): a plain 32-bit add, which ptxas can issue on the
+      // FMA pipe, instead of a VIADD.16x2 on the ALU pipe
+      const uint32_t nX = qX + 0x7fff7fffu;
+      const uint32_t nY = qY + 0x7fff7fffu;
+      // bytes X.lo, X.hi, Y.lo, Y.hi, each the sign-replicated top bit (0xff: not maximal)
+      const uint32_t tk = prmt2(nX, nY, 0xFDB9u);
+      // step q's flags at bit q of each byte; the word restarts every 8-step group
+      st.acc[k] = (q == 0 ? 0u : st.acc[k]) | (~tk & (0x01010101u << q));
       if (MASKED) un &= mask;  // U(i, 0) = 0 until each half reaches column 1
       st.Up[k] = un;
       vup = vn;

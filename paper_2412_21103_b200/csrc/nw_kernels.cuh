@@ -460,6 +460,12 @@ struct BatchArgs {
   int X, Y, Z;
   int* err;
   int win_off;             // byte offset of the per-warp traceback windows in dynamic smem
+  // Two-phase traceback (packed sweep, explicit pairs): the fill
+  // keeps every pair's decision words at tdirs + tdir_off[task] (32-bit words) and
+  // k_batch_walk walks them afterwards, one thread per pair. Null: walk in-warp.
+  uint32_t* tdirs;
+  const long long* tdir_off;
+  long long task0, task1;  // tasks [task0, task1) of this launch (a wave)
 };
 
 constexpr int NG_WIN = 16;  // 8-step groups per staged traceback window (packed layout)
@@ -493,10 +499,10 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
   int* bnd = B.wbnd + gw * 2 * B.bstride;
   uint16_t* wd = DIRS ? B.wdirs + gw * B.dstride : nullptr;
   for (;;) {
-    int task = 0;
-    if (lane == 0) task = atomicAdd(B.ticket, 1);
+    long long task = 0;
+    if (lane == 0) task = B.task0 + atomicAdd(B.ticket, 1);
     task = __shfl_sync(FULL, task, 0);
-    if (task >= B.npairs) break;
+    if (task >= B.task1) break;
     int p, q;
     long long outk;
     if (B.pairs) {
@@ -520,7 +526,7 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       constexpr int RS = PACKED ? 32 * KR16 : R;  // strip height of the sweep in use
       A.m = m; A.n = n; A.nstrips = (m + RS - 1) / RS; A.nslots = 2;
       A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr; A.ckpt = nullptr; A.ck_every = 0; A.ck_stride = 0; A.top_row = nullptr; A.top_tag = 0;
-      A.dirs = wd;
+      A.dirs = (PACKED == 3 && B.tdirs) ? reinterpret_cast<uint16_t*>(B.tdirs + B.tdir_off[task]) : wd;
       A.wpl = PACKED ? (n + 63 + 7) / 8 : (n + 31 + 7) / 8;  // 8-step groups per strip
       A.hm = B.whm + gw; A.err = B.err;
       if constexpr (PACKED == 1) {
@@ -539,7 +545,7 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       }
       __syncwarp();
       hmv = *(volatile int*)(B.whm + gw);
-      if (DIRS) {
+      if (DIRS && !(PACKED == 3 && B.tdirs)) {
         uint8_t* o = B.ops + B.ops_off[outk];
         long long L = 0;
         if constexpr (PACKED == 3) {
@@ -568,6 +574,79 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
     }
     if (lane == 0) B.scores[outk] = hmv + B.g * (m + n);
     __syncwarp();
+  }
+}
+
+// Phase 2 of the two-phase batch traceback: one thread per pair walks its kept
+// decision words from (m, n) to (0, 0) (flags decoded as in
+// tb_code_d16), writing the codes last-first from the end of the pair's ops slot
+// (capacity m + n); the warp then moves each path to the start of its slot with
+// coalesced copies. Tasks [t0, t1) of the fill's order; pairs with m = 0 or n = 0
+// were written by k_batch.
+template <int KR16>
+__global__ void __launch_bounds__(256) k_batch_walk(BatchArgs B) {
+  constexpr int H = KR16 / 2, RS = 32 * KR16;
+  const int lane = threadIdx.x & 31;
+  const long long task = B.task0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  bool act = task < B.task1;
+  int m = 0, n = 0;
+  long long outk = 0;
+  if (act) {
+    outk = B.order ? B.order[task] : task;
+    const int p = B.pairs[2 * outk], q = B.pairs[2 * outk + 1];
+    m = (int)(B.offs[p + 1] - B.offs[p]);
+    n = (int)(B.offs[q + 1] - B.offs[q]);
+    act = m > 0 && n > 0;
+  }
+  uint8_t* o = nullptr;
+  int pos = 0;
+  if (act) {
+    const uint32_t* d = B.tdirs + B.tdir_off[task];
+    const long long G = (n + 63 + 7) / 8;
+    o = B.ops + B.ops_off[outk];
+    pos = m + n;
+    int i = m, j = n;
+    long long cur = -1;
+    uint32_t w = 0;
+    while (i > 0 && j > 0) {
+      const int ia = i - 1;
+      const int s = ia / RS, rr = ia % RS, l = rr / KR16, r = rr % KR16;
+      const int hi = r >= H;
+      const int kk = hi ? r - H : r;
+      const int t = hi ? j + 2 * l : j - 1 + 2 * l;
+      const long long idx = (((long long)s * G + (t >> 3)) * H + kk) * 32 + l;
+      if (idx != cur) {  // a run of horizontal moves stays in one word
+        w = __ldg(d + idx);
+        cur = idx;
+      }
+      const int qq = t & 7;
+      const uint32_t fx = (w >> (8 * hi + qq)) & 1u, fy = (w >> (16 + 8 * hi + qq)) & 1u;
+      const int code = fx ? B.X : (fy ? B.Y : B.Z);
+      o[--pos] = (uint8_t)code;
+      i -= (code != 3);
+      j -= (code != 2);
+    }
+    while (i > 0) { o[--pos] = 2; --i; }  // column 0: vertical (R7)
+    while (j > 0) { o[--pos] = 3; --j; }  // row 0: horizontal
+    B.ops_len[outk] = m + n - pos;
+  }
+  // move each path [pos, m + n) of its slot to [0, L): increasing 32-byte chunks,
+  // all lanes read a chunk before any writes it, so the overlap is safe
+  unsigned pend = __ballot_sync(FULL, act && pos > 0);
+  while (pend) {
+    const int src_lane = __ffs(pend) - 1;
+    pend &= pend - 1;
+    uint8_t* ob = reinterpret_cast<uint8_t*>(__shfl_sync(FULL, reinterpret_cast<unsigned long long>(o), src_lane));
+    const int sb = __shfl_sync(FULL, pos, src_lane);
+    const int Lb = __shfl_sync(FULL, m + n - pos, src_lane);
+    __syncwarp();
+    for (int c0 = 0; c0 < Lb; c0 += 32) {
+      const bool in = c0 + lane < Lb;
+      const uint8_t v = in ? ob[sb + c0 + lane] : 0;
+      __syncwarp();
+      if (in) ob[c0 + lane] = v;
+      __syncwarp();
+    }
   }
 }
 

@@ -375,3 +375,28 @@ def test_batch_traceback_paths_all_orders(ctx, tie, scname):
     for k, (p, q) in enumerate(pairs):
         ws, wops = oracle.align(ss.seq(p), ss.seq(q), sc)
         assert scores[k] == ws and paths[k].tolist() == wops.tolist(), (k, len(ss.seq(p)), len(ss.seq(q)))
+
+
+@pytest.mark.parametrize("mode", ["waves", "inwarp", "kr16"])
+def test_batch_traceback_two_phase_modes(ctx, monkeypatch, mode):
+    """Two-phase batch traceback (fill keeps every pair's flags, k_batch_walk walks
+    them, one thread per pair): split into many waves by a tiny direction budget,
+    the in-warp walk it replaced, and the 16-rows-per-lane strips; pairs include
+    empty sequences and lengths across strip edges."""
+    if mode == "waves":
+        monkeypatch.setenv("NW_BATCH_TB_BUDGET", str(300_000))
+    elif mode == "inwarp":
+        monkeypatch.setenv("NW_BATCH_WALK_INWARP", "1")
+    else:
+        monkeypatch.setenv("NW_BATCH_KR16", "16")
+    ss = nwgen.random_set(61, 30, 0, 1300, nwgen.PROTEIN)
+    rng = np.random.Generator(np.random.PCG64(61))
+    pairs = rng.integers(0, ss.nseq, size=(120, 2)).astype(np.int32)
+    for tie in [(1, 2, 3), (2, 3, 1)]:
+        sc = nwgen.Scoring(match=0, mismatch=0, gap=-5, alphabet=nwgen.PROTEIN,
+                           subst=nwgen.BLOSUM62, tie=tie)
+        scores, *flat = nwb.nw_align_batch(ctx, ss.residues, ss.offs, pairs, sc, nwb.NW_TRACEBACK)
+        paths = nwb.batch_paths(*flat)
+        for k, (p, q) in enumerate(pairs):
+            ws, wops = oracle.align(ss.seq(p), ss.seq(q), sc)
+            assert scores[k] == ws and paths[k].tolist() == wops.tolist(), (mode, k)
