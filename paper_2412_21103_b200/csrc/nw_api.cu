@@ -1243,6 +1243,12 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   B.ops = d_ops;
   B.ops_len = d_ops_len;
   B.win_off = (int)smem_prof;
+  {
+    bool sym = true;
+    for (int x = 0; x < sc->K; ++x)
+      for (int y = 0; y < x; ++y) sym = sym && score_of(sc, x, y) == score_of(sc, y, x);
+    B.transpose_ok = (!tbk && sym && !getenv("NW_BATCH_NO_TRANSPOSE")) ? 1 : 0;
+  }
   B.tdirs = two_phase ? static_cast<uint32_t*>(c->d_tbdirs) : nullptr;
   B.tdir_off = two_phase ? c->d_tdoff : nullptr;
   B.task0 = 0;

@@ -463,6 +463,7 @@ struct BatchArgs {
   // Two-phase traceback (packed sweep, explicit pairs): the fill
   // keeps every pair's decision words at tdirs + tdir_off[task] (32-bit words) and
   // k_batch_walk walks them afterwards, one thread per pair. Null: walk in-warp.
+  int transpose_ok;        // score-only, s symmetric: a pair may be filled transposed
   uint32_t* tdirs;
   const long long* tdir_off;
   long long task0, task1;  // tasks [task0, task1) of this launch (a wave)
@@ -517,8 +518,18 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       q = max(x, y);
       outk = (long long)p * B.nseq - (long long)p * (p + 1) / 2 + (q - p - 1);
     }
-    const long long ao = B.offs[p], bo = B.offs[q];
-    const int m = (int)(B.offs[p + 1] - ao), n = (int)(B.offs[q + 1] - bo);
+    long long ao = B.offs[p], bo = B.offs[q];
+    int m = (int)(B.offs[p + 1] - ao), n = (int)(B.offs[q + 1] - bo);
+    if (!DIRS && B.transpose_ok) {
+      // score-only with a symmetric s: Score(a, b) = Score(b, a) (the transpose
+      // invariant of the oracle pins), so put on the rows whichever sequence wastes
+      // fewer lanes of the last strip: strips x (columns + lane skew)
+      constexpr int RS = PACKED ? 32 * KR16 : R, SK = PACKED ? 64 : 32;
+      if ((long long)((m + RS - 1) / RS) * (n + SK) > (long long)((n + RS - 1) / RS) * (m + SK)) {
+        const long long to = ao; ao = bo; bo = to;
+        const int tm = m; m = n; n = tm;
+      }
+    }
     int hmv = 0;
     if (m > 0 && n > 0) {
       FillArgs A;

@@ -400,3 +400,23 @@ def test_batch_traceback_two_phase_modes(ctx, monkeypatch, mode):
         for k, (p, q) in enumerate(pairs):
             ws, wops = oracle.align(ss.seq(p), ss.seq(q), sc)
             assert scores[k] == ws and paths[k].tolist() == wops.tolist(), (mode, k)
+
+
+@pytest.mark.parametrize("sym", [True, False])
+def test_batch_score_only_orientation(ctx, monkeypatch, sym):
+    """Score-only batches fill each pair in the orientation that wastes fewer strip
+    rows when s is symmetric (Score(a,b) = Score(b,a)); an asymmetric s must keep
+    a on the rows. Lengths straddle the 512-row strip edges in both directions."""
+    subst = np.array([[3, -1, 0, -2], [-1, 2, -3, 0], [0, -3, 4, -1], [-2, 0, -1, 1]], dtype=np.int32)
+    if not sym:
+        subst[0, 1], subst[2, 3] = 1, -2  # s(A,C) != s(C,A), s(G,T) != s(T,G)
+    sc = nwgen.Scoring(gap=-2, subst=subst)
+    ss = nwgen.random_set(71 + sym, 12, 300, 1700)
+    pairs = nwgen.all_pairs(ss.nseq)
+    want = oracle.batch_score(ss.residues, ss.offs, pairs, sc)
+    assert nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc).tolist() == want.tolist()
+    rev = pairs[:, ::-1].copy()
+    assert nwb.nw_align_batch(ctx, ss.residues, ss.offs, rev, sc).tolist() == \
+        oracle.batch_score(ss.residues, ss.offs, rev, sc).tolist()
+    monkeypatch.setenv("NW_BATCH_NO_TRANSPOSE", "1")
+    assert nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc).tolist() == want.tolist()
