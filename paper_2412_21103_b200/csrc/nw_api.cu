@@ -1204,7 +1204,9 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   // packed traceback: per-warp window of NG_WIN groups x (RS/64) packed rows x 32 lanes words
   const size_t smem_win = (tbk && d16 && !two_phase) ? (size_t)warps_per_cta * NG_WIN * (RS / 64) * 32 * 4 : 0;
   const size_t smem = smem_prof + smem_win;
-  int ctas_per_sm = 4;
+  // 6 x 4 warps per SM (24 warps, 72 registers each): C4 2.11 -> 2.26 TCUPS, C3 6.73 -> 6.84
+  // over 4 per SM; 8 no better (tools/exp_ctas.sh, profiles/r01_exp_ctas.txt)
+  int ctas_per_sm = env_int("NW_BATCH_CTAS", 6, 1);
   const long long nwarps = (long long)c->sm_count * ctas_per_sm * warps_per_cta;
   const long long bstride = maxlen + 1 + 64;
   // direction scratch per warp, in halfwords: int32 sweep = halfword per (group,
