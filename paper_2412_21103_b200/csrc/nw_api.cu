@@ -1253,6 +1253,9 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   }
   B.tdirs = two_phase ? static_cast<uint32_t*>(c->d_tbdirs) : nullptr;
   B.tdir_off = two_phase ? c->d_tdoff : nullptr;
+  // the walk as its own launch: walking every 32 pairs inside the filling warp was
+  // measured slower on C4 (fill + walk 12.74 vs 10.93 + 1.52 ms; tools/exp_c4.py)
+  B.walk_inline = getenv("NW_BATCH_WALK_INLINE") ? 1 : 0;
   B.task0 = 0;
   B.task1 = npairs;
   B.X = sc->tie[0];
@@ -1280,14 +1283,14 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
       if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
       LAUNCHED(c);
       CUDA_TRY(c, cudaGetLastError());
-      {
+      if (!B.walk_inline) {
         KernelTimer kt(c, 1);
         const unsigned wg = (unsigned)((t1 - t0 + 255) / 256);
         if (packed_kr == 8) k_batch_walk<8><<<wg, 256, 0, c->stream>>>(B);
         else k_batch_walk<16><<<wg, 256, 0, c->stream>>>(B);
+        LAUNCHED(c);
+        CUDA_TRY(c, cudaGetLastError());
       }
-      LAUNCHED(c);
-      CUDA_TRY(c, cudaGetLastError());
       t0 = t1;
     }
     return NW_OK;

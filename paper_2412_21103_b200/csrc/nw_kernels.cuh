@@ -460,12 +460,14 @@ struct BatchArgs {
   int X, Y, Z;
   int* err;
   int win_off;             // byte offset of the per-warp traceback windows in dynamic smem
+  int transpose_ok;        // score-only, s symmetric: a pair may be filled transposed
   // Two-phase traceback (packed sweep, explicit pairs): the fill
   // keeps every pair's decision words at tdirs + tdir_off[task] (32-bit words) and
-  // k_batch_walk walks them afterwards, one thread per pair. Null: walk in-warp.
-  int transpose_ok;        // score-only, s symmetric: a pair may be filled transposed
+  // they are walked one thread per pair: by the filling warp itself after every 32
+  // pairs (walk_inline), else by k_batch_walk after the fill. Null: walk in-warp.
   uint32_t* tdirs;
   const long long* tdir_off;
+  int walk_inline;
   long long task0, task1;  // tasks [task0, task1) of this launch (a wave)
 };
 
@@ -488,6 +490,9 @@ __device__ __forceinline__ void unrank_pair(long long k, int N, int& p, int& q) 
 // 1 = the H' half-row sweep of nw_fill16.cuh (score-only, K <= 4, every H' < 2^16),
 // 2 = the difference-form sweep of nw_fill_d16.cuh (score-only, K <= 4, any length),
 // 3 = the difference-form sweep with decision flags of nw_fill_d16dir.cuh (DIRS).
+template <int KR16, bool COHERENT>
+__device__ __forceinline__ void walk_lanes(const BatchArgs& B, long long task, bool act, int lane);
+
 template <int KR, bool DIRS, bool PROFREG, int PI, int PACKED = 0, int KR16 = 16>
 __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
   constexpr int R = 32 * KR;
@@ -499,6 +504,11 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
   int8_t* sprof = smem + (PROFREG ? 0 : wib * (B.K * RSP));
   int* bnd = B.wbnd + gw * 2 * B.bstride;
   uint16_t* wd = DIRS ? B.wdirs + gw * B.dstride : nullptr;
+  // walk_inline: lane k holds the k-th of the last filled pairs; every 32 pairs the
+  // warp walks them lane-parallel (latency-bound loads that overlap the other
+  // warps' fills instead of a separate latency-bound launch)
+  long long held = -1;
+  int nheld = 0;
   for (;;) {
     long long task = 0;
     if (lane == 0) task = B.task0 + atomicAdd(B.ticket, 1);
@@ -585,21 +595,32 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
     }
     if (lane == 0) B.scores[outk] = hmv + B.g * (m + n);
     __syncwarp();
+    if constexpr (PACKED == 3) {
+      if (B.tdirs && B.walk_inline) {
+        if (lane == nheld) held = task;
+        if (++nheld == 32) {
+          walk_lanes<KR16, true>(B, held, true, lane);
+          held = -1;
+          nheld = 0;
+        }
+      }
+    }
+  }
+  if constexpr (PACKED == 3) {
+    if (B.tdirs && B.walk_inline && nheld > 0) walk_lanes<KR16, true>(B, held, held >= 0, lane);
   }
 }
 
-// Phase 2 of the two-phase batch traceback: one thread per pair walks its kept
+// Phase 2 of the two-phase batch traceback: each lane walks one pair's kept
 // decision words from (m, n) to (0, 0) (flags decoded as in
 // tb_code_d16), writing the codes last-first from the end of the pair's ops slot
 // (capacity m + n); the warp then moves each path to the start of its slot with
-// coalesced copies. Tasks [t0, t1) of the fill's order; pairs with m = 0 or n = 0
-// were written by k_batch.
-template <int KR16>
-__global__ void __launch_bounds__(256) k_batch_walk(BatchArgs B) {
+// coalesced copies. Called by all 32 lanes; act = this lane has a pair (task of
+// the fill's order). Pairs with m = 0 or n = 0 were written by k_batch. COHERENT:
+// the words were written in this kernel (by this warp), so no read-only-path loads.
+template <int KR16, bool COHERENT>
+__device__ __forceinline__ void walk_lanes(const BatchArgs& B, long long task, bool act, int lane) {
   constexpr int H = KR16 / 2, RS = 32 * KR16;
-  const int lane = threadIdx.x & 31;
-  const long long task = B.task0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  bool act = task < B.task1;
   int m = 0, n = 0;
   long long outk = 0;
   if (act) {
@@ -627,7 +648,7 @@ __global__ void __launch_bounds__(256) k_batch_walk(BatchArgs B) {
       const int t = hi ? j + 2 * l : j - 1 + 2 * l;
       const long long idx = (((long long)s * G + (t >> 3)) * H + kk) * 32 + l;
       if (idx != cur) {  // a run of horizontal moves stays in one word
-        w = __ldg(d + idx);
+        w = COHERENT ? __ldcg(d + idx) : __ldg(d + idx);
         cur = idx;
       }
       const int qq = t & 7;
@@ -659,6 +680,13 @@ __global__ void __launch_bounds__(256) k_batch_walk(BatchArgs B) {
       __syncwarp();
     }
   }
+}
+
+// The walk as its own launch after the fill (walk_inline = 0): one thread per task.
+template <int KR16>
+__global__ void __launch_bounds__(256) k_batch_walk(BatchArgs B) {
+  const long long task = B.task0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  walk_lanes<KR16, false>(B, task, task < B.task1, threadIdx.x & 31);
 }
 
 }  // namespace nwk
