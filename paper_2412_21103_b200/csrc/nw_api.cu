@@ -316,6 +316,8 @@ bool dispatch_fill(bool dirs, int pi, int kr, bool profreg, const FillArgs& A, i
   if (!dirs) {
     if (kr == 2) launch_score<2>(A, profreg, grid, smem, st);
     else if (kr == 4) launch_score<4>(A, profreg, grid, smem, st);
+    else if (kr == 5 && profreg) launch_fill_t<5, false, true, 123>(A, grid, smem, st);  // experiments
+    else if (kr == 6 && profreg) launch_fill_t<6, false, true, 123>(A, grid, smem, st);
     else launch_score<8>(A, profreg, grid, smem, st);
     return true;
   }
@@ -347,7 +349,7 @@ int choose_kr(long long m, long long n, bool dirs) {
   const char* env = getenv("NW_KR");
   if (env) {
     const int k = atoi(env);
-    if (k == 2 || k == 4 || k == 8) return k;
+    if (k == 2 || k == 4 || k == 8 || ((k == 5 || k == 6) && !dirs)) return k;
   }
   (void)dirs;
   // Tall pairs (>= ~150 strips at KR = 8): the largest KR, the lag is amortised
