@@ -177,14 +177,14 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
     st.bc_nxt = __ldg(C.b + j);  // next step's b_{j+1} (PAD makes j in [-31, n+62] readable)
     uint32_t sel = 0;
     uint2 pw = make_uint2(0, 0);
-    if (PROFREG) {
+    if constexpr (PROFREG) {
       sel = bc * 0x1111u + 0x8880u;  // byte bc, sign-replicated into bytes 1..3 (bc < 8: no carry)
-    } else if (KR == 8) {
+    } else if constexpr (KR == 8) {
       pw = *reinterpret_cast<const uint2*>(C.sprof + bc * R + lane * KR);
-    } else if (KR == 4) {
+    } else if constexpr (KR == 4) {
       pw.x = *reinterpret_cast<const uint32_t*>(C.sprof + bc * R + lane * KR);
     } else {
-      static_assert(KR == 2 || KR == 4 || KR == 8, "KR must be 2, 4 or 8");
+      static_assert(KR == 2, "shared-memory profile: KR must be 2, 4 or 8");
       pw.x = *reinterpret_cast<const uint16_t*>(C.sprof + bc * R + lane * KR);
     }
     // up = H'(top-1, j): lane 0 from the boundary row (0 for strip 0), others from lane-1
