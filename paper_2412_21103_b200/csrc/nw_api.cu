@@ -1159,17 +1159,31 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   // one thread each, so the walk's dependent loads overlap across 100k pairs instead
   // of idling 31 lanes of a filling warp. Pairs are cut into waves whose words fit
   // the budget (half the free memory; NW_BATCH_TB_BUDGET bytes overrides).
-  const bool two_phase = tbk && d16 && h_pairs != nullptr && !getenv("NW_BATCH_WALK_INWARP");
+  const bool two_phase = tbk && d16;
   std::vector<long long> tdoff, wave_end;
   if (two_phase) {
     const long long wpg = RS / 2;  // words per (strip, 8-step group): H packed rows x 32 lanes
-    auto words_of = [&](int k) {
-      const long long m = h_offs[h_pairs[2 * k] + 1] - h_offs[h_pairs[2 * k]];
-      const long long n = h_offs[h_pairs[2 * k + 1] + 1] - h_offs[h_pairs[2 * k + 1]];
+    auto len = [&](int s) { return h_offs[s + 1] - h_offs[s]; };
+    auto words_mn = [&](long long m, long long n) {
       return (m > 0 && n > 0) ? ((m + RS - 1) / RS) * ((n + 63 + 7) / 8) * wpg : 0LL;
     };
+    // words of every task in the fill's order: explicit pairs by aux (LPT), implicit
+    // all-pairs in rank order over the length-sorted sequences (aux = that perm),
+    // the row sequence being the lower original index as in task_pair
+    std::vector<long long> tw((size_t)npairs);
+    if (h_pairs) {
+      for (long long t = 0; t < npairs; ++t)
+        tw[t] = words_mn(len(h_pairs[2 * aux[t]]), len(h_pairs[2 * aux[t] + 1]));
+    } else {
+      long long t = 0;
+      for (int pr = 0; pr < nseq; ++pr)
+        for (int qr = pr + 1; qr < nseq; ++qr, ++t) {
+          const int x = aux[pr], y = aux[qr];
+          tw[t] = words_mn(len(std::min(x, y)), len(std::max(x, y)));
+        }
+    }
     long long all_words = 0;
-    for (long long k = 0; k < npairs; ++k) all_words += words_of((int)k);
+    for (long long t = 0; t < npairs; ++t) all_words += tw[t];
     long long budget = all_words;  // one wave when the kept buffer already holds it
     if ((size_t)all_words * 4 > c->tbdirs_cap) {
       size_t free_b = 0, tot_b = 0;
@@ -1180,7 +1194,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
     tdoff.resize(npairs);
     long long acc = 0, maxwave = 0;
     for (long long t = 0; t < npairs; ++t) {
-      const long long words = words_of(aux[t]);
+      const long long words = tw[t];
       if (acc > 0 && acc + words > budget) {
         wave_end.push_back(t);
         maxwave = std::max(maxwave, acc);
@@ -1203,9 +1217,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
     if (st) return st;
   }
   const size_t smem_prof = profreg ? 0 : (((size_t)warps_per_cta * sc->K * RS + 15) & ~size_t(15));
-  // packed traceback: per-warp window of NG_WIN groups x (RS/64) packed rows x 32 lanes words
-  const size_t smem_win = (tbk && d16 && !two_phase) ? (size_t)warps_per_cta * NG_WIN * (RS / 64) * 32 * 4 : 0;
-  const size_t smem = smem_prof + smem_win;
+  const size_t smem = smem_prof;
   // 6 x 4 warps per SM (24 warps, 72 registers each): C4 2.11 -> 2.26 TCUPS, C3 6.73 -> 6.84
   // over 4 per SM; 8 no better (tools/exp_ctas.sh, profiles/r01_exp_ctas.txt)
   int ctas_per_sm = env_int("NW_BATCH_CTAS", 6, 1);
@@ -1246,7 +1258,6 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   B.ops_off = d_ops_off;
   B.ops = d_ops;
   B.ops_len = d_ops_len;
-  B.win_off = (int)smem_prof;
   {
     bool sym = true;
     for (int x = 0; x < sc->K; ++x)
@@ -1255,9 +1266,6 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   }
   B.tdirs = two_phase ? static_cast<uint32_t*>(c->d_tbdirs) : nullptr;
   B.tdir_off = two_phase ? c->d_tdoff : nullptr;
-  // the walk as its own launch: walking every 32 pairs inside the filling warp was
-  // measured slower on C4 (fill + walk 12.74 vs 10.93 + 1.52 ms; tools/exp_c4.py)
-  B.walk_inline = getenv("NW_BATCH_WALK_INLINE") ? 1 : 0;
   B.task0 = 0;
   B.task1 = npairs;
   B.X = sc->tie[0];
@@ -1285,7 +1293,8 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
       if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
       LAUNCHED(c);
       CUDA_TRY(c, cudaGetLastError());
-      if (!B.walk_inline) {
+      {  // (walking every 32 pairs inside the filling warp instead was slower on C4:
+         // fill + walk 12.74 vs 10.93 + 1.52 ms, profiles/r01_exp_c4_walk_inline.txt)
         KernelTimer kt(c, 1);
         const unsigned wg = (unsigned)((t1 - t0 + 255) / 256);
         if (packed_kr == 8) k_batch_walk<8><<<wg, 256, 0, c->stream>>>(B);

@@ -189,94 +189,4 @@ __device__ __forceinline__ void strip_sweep_d16dir(const FillArgs& A, int s, int
   __syncwarp();
 }
 
-// Decode the decision flags of interior cell (i, j) (1-based) -> P:90 code.
-template <int KR>
-__device__ __forceinline__ int tb_code_d16(const uint32_t* dirs, long long G, int i, int j,
-                                           int X, int Y, int Z) {
-  constexpr int H = KR / 2, R = 32 * KR;
-  const int ia = i - 1;
-  const int s = ia / R, rr = ia % R, l = rr / KR, r = rr % KR;
-  const int hi = r >= H;
-  const int k = hi ? r - H : r;
-  const int t = hi ? j + 2 * l : j - 1 + 2 * l;
-  const uint32_t w = __ldca(dirs + (((long long)s * G + (t >> 3)) * H + k) * 32 + l);
-  const int q = t & 7;
-  const uint32_t fx = (w >> (8 * hi + q)) & 1u, fy = (w >> (16 + 8 * hi + q)) & 1u;
-  return fx ? X : (fy ? Y : Z);
-}
-
-// Walk from (m, n) to (0, 0) over the packed flags; rev[k] = k-th code from the end.
-template <int KR>
-__device__ long long tb_walk_d16(const uint32_t* dirs, long long G, int m, int n, int X, int Y,
-                                 int Z, uint8_t* rev) {
-  int i = m, j = n;
-  long long k = 0;
-  while (i > 0 && j > 0) {
-    const int code = tb_code_d16<KR>(dirs, G, i, j, X, Y, Z);
-    rev[k++] = (uint8_t)code;
-    i -= (code != 3);
-    j -= (code != 2);
-  }
-  while (i > 0) { rev[k++] = 2; --i; }
-  while (j > 0) { rev[k++] = 3; --j; }
-  return k;
-}
-
-// Warp-cooperative walk: the decision words of a window (one strip x NG 8-step
-// groups = NG*H*32 contiguous words) are staged in shared memory by all lanes
-// with 16-byte loads; lane 0 walks inside the window and the warp restages when
-// the path leaves it (up into the next strip, or left past the window). Each
-// step is then a shared-memory read instead of a dependent L2 round trip.
-// Must be called by all 32 lanes; returns the path length (valid in every lane).
-template <int KR, int NG>
-__device__ long long tb_walk_d16_win(const uint32_t* dirs, long long G, int m, int n, int X,
-                                     int Y, int Z, uint8_t* rev, uint32_t* win, int lane) {
-  constexpr int H = KR / 2, R = 32 * KR;
-  constexpr int WW = NG * H * 32;  // words per window
-  int i = m, j = n;
-  long long k = 0;
-  int ws = -1, g0 = 0;
-  for (;;) {
-    int need = 0, ns = 0, ng = 0;
-    if (lane == 0) {
-      while (i > 0 && j > 0) {
-        const int ia = i - 1;
-        const int s = ia / R, rr = ia % R, l = rr / KR, r = rr % KR;
-        const int hi = r >= H;
-        const int kk = hi ? r - H : r;
-        const int t = hi ? j + 2 * l : j - 1 + 2 * l;
-        const int g = t >> 3;
-        if (s != ws || g < g0 || g >= g0 + NG) { need = 1; ns = s; ng = g; break; }
-        const uint32_t w = win[((g - g0) * H + kk) * 32 + l];
-        const int q = t & 7;
-        const uint32_t fx = (w >> (8 * hi + q)) & 1u, fy = (w >> (16 + 8 * hi + q)) & 1u;
-        const int code = fx ? X : (fy ? Y : Z);
-        rev[k++] = (uint8_t)code;
-        i -= (code != 3);
-        j -= (code != 2);
-      }
-    }
-    need = __shfl_sync(FULL, need, 0);
-    if (!need) break;
-    ns = __shfl_sync(FULL, ns, 0);
-    ng = __shfl_sync(FULL, ng, 0);
-    // window = groups [g0, g0 + NG) of strip ns, with the path's current group at its top
-    ws = ns;
-    g0 = max(0, ng - NG + 1);
-    const long long gav = G - g0;
-    const int nload = (int)(gav < NG ? gav : NG) * H * 32;  // words present in memory
-    const uint4* src = reinterpret_cast<const uint4*>(dirs + ((long long)ws * G + g0) * (H * 32));
-    uint4* dst = reinterpret_cast<uint4*>(win);
-    for (int q = lane; q < nload / 4; q += 32) dst[q] = __ldcg(src + q);
-    (void)WW;
-    __syncwarp();
-  }
-  if (lane == 0) {
-    while (i > 0) { rev[k++] = 2; --i; }
-    while (j > 0) { rev[k++] = 3; --j; }
-  }
-  k = __shfl_sync(FULL, k, 0);
-  return k;
-}
-
 }  // namespace nwk

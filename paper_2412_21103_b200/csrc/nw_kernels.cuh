@@ -459,19 +459,14 @@ struct BatchArgs {
   int* ops_len;
   int X, Y, Z;
   int* err;
-  int win_off;             // byte offset of the per-warp traceback windows in dynamic smem
   int transpose_ok;        // score-only, s symmetric: a pair may be filled transposed
-  // Two-phase traceback (packed sweep, explicit pairs): the fill
+  // Two-phase traceback (the packed sweep, PACKED == 3): the fill
   // keeps every pair's decision words at tdirs + tdir_off[task] (32-bit words) and
-  // they are walked one thread per pair: by the filling warp itself after every 32
-  // pairs (walk_inline), else by k_batch_walk after the fill. Null: walk in-warp.
+  // k_batch_walk walks them after the fill, one thread per pair.
   uint32_t* tdirs;
   const long long* tdir_off;
-  int walk_inline;
   long long task0, task1;  // tasks [task0, task1) of this launch (a wave)
 };
-
-constexpr int NG_WIN = 16;  // 8-step groups per staged traceback window (packed layout)
 
 // flat rank-space index k -> (p', q'), p' < q', lexicographic over N items
 __device__ __forceinline__ void unrank_pair(long long k, int N, int& p, int& q) {
@@ -484,6 +479,25 @@ __device__ __forceinline__ void unrank_pair(long long k, int N, int& p, int& q) 
   while (pp + 1 <= N - 2 && off(pp + 1) <= k) ++pp;
   p = (int)pp;
   q = (int)(k - off(pp) + pp + 1);
+}
+
+// Task -> pair (p, q) and its output index: explicit pairs in the host's LPT order,
+// or the flat rank-space index over sequences sorted by length, mapped back to the
+// lexicographic p < q index.
+__device__ __forceinline__ void task_pair(const BatchArgs& B, long long task, int& p, int& q,
+                                          long long& outk) {
+  if (B.pairs) {
+    outk = B.order ? B.order[task] : task;
+    p = B.pairs[2 * outk];
+    q = B.pairs[2 * outk + 1];
+  } else {
+    int pr, qr;
+    unrank_pair(task, B.nseq, pr, qr);
+    const int x = B.perm[pr], y = B.perm[qr];
+    p = min(x, y);
+    q = max(x, y);
+    outk = (long long)p * B.nseq - (long long)p * (p + 1) / 2 + (q - p - 1);
+  }
 }
 
 // PACKED (s - 2g >= 0), KR16 rows per lane, two per register:
@@ -504,11 +518,6 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
   int8_t* sprof = smem + (PROFREG ? 0 : wib * (B.K * RSP));
   int* bnd = B.wbnd + gw * 2 * B.bstride;
   uint16_t* wd = DIRS ? B.wdirs + gw * B.dstride : nullptr;
-  // walk_inline: lane k holds the k-th of the last filled pairs; every 32 pairs the
-  // warp walks them lane-parallel (latency-bound loads that overlap the other
-  // warps' fills instead of a separate latency-bound launch)
-  long long held = -1;
-  int nheld = 0;
   for (;;) {
     long long task = 0;
     if (lane == 0) task = B.task0 + atomicAdd(B.ticket, 1);
@@ -516,18 +525,7 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
     if (task >= B.task1) break;
     int p, q;
     long long outk;
-    if (B.pairs) {
-      outk = B.order ? B.order[task] : task;
-      p = B.pairs[2 * outk];
-      q = B.pairs[2 * outk + 1];
-    } else {
-      int pr, qr;
-      unrank_pair(task, B.nseq, pr, qr);
-      const int x = B.perm[pr], y = B.perm[qr];
-      p = min(x, y);
-      q = max(x, y);
-      outk = (long long)p * B.nseq - (long long)p * (p + 1) / 2 + (q - p - 1);
-    }
+    task_pair(B, task, p, q, outk);
     long long ao = B.offs[p], bo = B.offs[q];
     int m = (int)(B.offs[p + 1] - ao), n = (int)(B.offs[q + 1] - bo);
     if (!DIRS && B.transpose_ok) {
@@ -547,7 +545,7 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       constexpr int RS = PACKED ? 32 * KR16 : R;  // strip height of the sweep in use
       A.m = m; A.n = n; A.nstrips = (m + RS - 1) / RS; A.nslots = 2;
       A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr; A.ckpt = nullptr; A.ck_every = 0; A.ck_stride = 0; A.top_row = nullptr; A.top_tag = 0;
-      A.dirs = (PACKED == 3 && B.tdirs) ? reinterpret_cast<uint16_t*>(B.tdirs + B.tdir_off[task]) : wd;
+      A.dirs = PACKED == 3 ? reinterpret_cast<uint16_t*>(B.tdirs + B.tdir_off[task]) : wd;
       A.wpl = PACKED ? (n + 63 + 7) / 8 : (n + 31 + 7) / 8;  // 8-step groups per strip
       A.hm = B.whm + gw; A.err = B.err;
       if constexpr (PACKED == 1) {
@@ -566,18 +564,14 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       }
       __syncwarp();
       hmv = *(volatile int*)(B.whm + gw);
-      if (DIRS && !(PACKED == 3 && B.tdirs)) {
+      // the int32 sweep walks its pair in-warp; the packed flags (PACKED == 3) are
+      // walked by k_batch_walk, one thread per pair (an in-warp walk compiled into
+      // this kernel made ptxas emit every shuffle of the sweep as a collective)
+      if (DIRS && PACKED != 3) {
         uint8_t* o = B.ops + B.ops_off[outk];
         long long L = 0;
-        if constexpr (PACKED == 3) {
-          // all lanes: staged windows of decision words (NG_WIN groups per window)
-          uint32_t* win = reinterpret_cast<uint32_t*>(smem + B.win_off) + wib * (NG_WIN * (KR16 / 2) * 32);
-          L = tb_walk_d16_win<KR16, NG_WIN>(reinterpret_cast<const uint32_t*>(wd), A.wpl, m, n, B.X,
-                                            B.Y, B.Z, o, win, lane);
-        } else {
-          if (lane == 0) L = tb_walk<KR>(wd, A.wpl, m, n, B.X, B.Y, B.Z, o);
-          L = __shfl_sync(FULL, L, 0);
-        }
+        if (lane == 0) L = tb_walk<KR>(wd, A.wpl, m, n, B.X, B.Y, B.Z, o);
+        L = __shfl_sync(FULL, L, 0);
         __syncwarp();
         // reverse in place: o[0..L) holds the codes last-first
         for (long long a0 = lane; a0 < L / 2; a0 += 32) {
@@ -595,25 +589,12 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
     }
     if (lane == 0) B.scores[outk] = hmv + B.g * (m + n);
     __syncwarp();
-    if constexpr (PACKED == 3) {
-      if (B.tdirs && B.walk_inline) {
-        if (lane == nheld) held = task;
-        if (++nheld == 32) {
-          walk_lanes<KR16, true>(B, held, true, lane);
-          held = -1;
-          nheld = 0;
-        }
-      }
-    }
-  }
-  if constexpr (PACKED == 3) {
-    if (B.tdirs && B.walk_inline && nheld > 0) walk_lanes<KR16, true>(B, held, held >= 0, lane);
   }
 }
 
 // Phase 2 of the two-phase batch traceback: each lane walks one pair's kept
-// decision words from (m, n) to (0, 0) (flags decoded as in
-// tb_code_d16), writing the codes last-first from the end of the pair's ops slot
+// decision words from (m, n) to (0, 0) (word and bit of cell (i, j) in
+// the layout of nw_fill_d16dir.cuh), writing the codes last-first from the end of the pair's ops slot
 // (capacity m + n); the warp then moves each path to the start of its slot with
 // coalesced copies. Called by all 32 lanes; act = this lane has a pair (task of
 // the fill's order). Pairs with m = 0 or n = 0 were written by k_batch. COHERENT:
@@ -624,8 +605,8 @@ __device__ __forceinline__ void walk_lanes(const BatchArgs& B, long long task, b
   int m = 0, n = 0;
   long long outk = 0;
   if (act) {
-    outk = B.order ? B.order[task] : task;
-    const int p = B.pairs[2 * outk], q = B.pairs[2 * outk + 1];
+    int p, q;
+    task_pair(B, task, p, q, outk);
     m = (int)(B.offs[p + 1] - B.offs[p]);
     n = (int)(B.offs[q + 1] - B.offs[q]);
     act = m > 0 && n > 0;
@@ -682,7 +663,7 @@ __device__ __forceinline__ void walk_lanes(const BatchArgs& B, long long task, b
   }
 }
 
-// The walk as its own launch after the fill (walk_inline = 0): one thread per task.
+// The walk as its own launch after the fill: one thread per task.
 template <int KR16>
 __global__ void __launch_bounds__(256) k_batch_walk(BatchArgs B) {
   const long long task = B.task0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;

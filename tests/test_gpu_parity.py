@@ -377,28 +377,27 @@ def test_batch_traceback_paths_all_orders(ctx, tie, scname):
         assert scores[k] == ws and paths[k].tolist() == wops.tolist(), (k, len(ss.seq(p)), len(ss.seq(q)))
 
 
-@pytest.mark.parametrize("mode", ["waves", "inwarp", "kr16", "inline"])
+@pytest.mark.parametrize("mode", ["waves", "kr16", "implicit"])
 def test_batch_traceback_two_phase_modes(ctx, monkeypatch, mode):
-    """Two-phase batch traceback (fill keeps every pair's flags; k_batch_walk walks
-    them after the fill, one thread per pair, or the filling warp every 32 pairs
-    lane-parallel): split into many waves by a tiny direction budget, the in-warp
-    walk it replaced, 16-rows-per-lane strips, the inline walk; pairs include empty
-    sequences and lengths across strip edges."""
-    if mode == "waves":
-        monkeypatch.setenv("NW_BATCH_TB_BUDGET", str(300_000))
-    elif mode == "inwarp":
-        monkeypatch.setenv("NW_BATCH_WALK_INWARP", "1")
-    elif mode == "kr16":
+    """Two-phase batch traceback (the fill keeps every pair's flags, k_batch_walk walks
+    them, one thread per pair): split into many waves by a tiny direction budget,
+    16-rows-per-lane strips, and all pairs (pairs=None: tasks in rank order over the
+    length-sorted sequences) in waves; pairs include empty sequences and lengths
+    across strip edges."""
+    if mode == "kr16":
         monkeypatch.setenv("NW_BATCH_KR16", "16")
     else:
-        monkeypatch.setenv("NW_BATCH_WALK_INLINE", "1")
-    ss = nwgen.random_set(61, 30, 0, 1300, nwgen.PROTEIN)
+        monkeypatch.setenv("NW_BATCH_TB_BUDGET", str(300_000))
+    ss = nwgen.random_set(61, 30 if mode != "implicit" else 14, 0, 1300, nwgen.PROTEIN)
     rng = np.random.Generator(np.random.PCG64(61))
     pairs = rng.integers(0, ss.nseq, size=(120, 2)).astype(np.int32)
+    if mode == "implicit":
+        pairs = nwgen.all_pairs(ss.nseq)
     for tie in [(1, 2, 3), (2, 3, 1)]:
         sc = nwgen.Scoring(match=0, mismatch=0, gap=-5, alphabet=nwgen.PROTEIN,
                            subst=nwgen.BLOSUM62, tie=tie)
-        scores, *flat = nwb.nw_align_batch(ctx, ss.residues, ss.offs, pairs, sc, nwb.NW_TRACEBACK)
+        arg = None if mode == "implicit" else pairs
+        scores, *flat = nwb.nw_align_batch(ctx, ss.residues, ss.offs, arg, sc, nwb.NW_TRACEBACK)
         paths = nwb.batch_paths(*flat)
         for k, (p, q) in enumerate(pairs):
             ws, wops = oracle.align(ss.seq(p), ss.seq(q), sc)

@@ -1,5 +1,6 @@
 """C4 step anatomy: host enqueue time vs device time per nw_align_batch_dev call,
-two-phase walk vs the in-warp walk (NW_BATCH_WALK_INWARP)."""
+fill and walk kernel times (the in-warp walk variant it was first compared with,
+NW_BATCH_WALK_INWARP, is gone: profiles/r01_exp_c4_anatomy.txt)."""
 import os, sys, time
 sys.path.insert(0, '.')
 import numpy as np
@@ -19,11 +20,7 @@ d_oo = torch.from_numpy(oo).cuda()
 d_ops = torch.zeros(int(oo[-1]) + 1, dtype=torch.uint8, device="cuda")
 d_len = torch.zeros(len(pairs), dtype=torch.int32, device="cuda")
 d_sc = torch.zeros(len(pairs), dtype=torch.int32, device="cuda")
-for mode in ("two_phase", "inwarp", "two_phase"):
-    if mode == "inwarp":
-        os.environ["NW_BATCH_WALK_INWARP"] = "1"
-    else:
-        os.environ.pop("NW_BATCH_WALK_INWARP", None)
+for mode in ("two_phase", "two_phase"):
     run = lambda: nwb.nw_align_batch_dev(ctx, d_seqs, d_offs, ss.offs, d_pairs, pairs, len(pairs), sc,
                                          nwb.NW_TRACEBACK, d_sc, d_oo, d_ops, d_len)
     run(); run(); torch.cuda.synchronize()
