@@ -345,11 +345,17 @@ bool d16_ok(const nw_scoring* sc) {
 // Rows per lane for a single pair: the strip count m/(32 KR)
 // is the number of warps that can work at once; small KR buys parallelism at the
 // cost of a longer lane skew (m/KR steps). NW_KR overrides (2, 4 or 8).
-int choose_kr(long long m, long long n, bool dirs) {
+int choose_kr_shape(long long m, long long n, bool dirs);
+// KR 5 and 6 exist only with register profiles (K <= 4)
+int choose_kr(long long m, long long n, bool dirs, int K) {
+  const int k = choose_kr_shape(m, n, dirs);
+  return (K > 4 && (k == 5 || k == 6)) ? 4 : k;
+}
+int choose_kr_shape(long long m, long long n, bool dirs) {
   const char* env = getenv("NW_KR");
   if (env) {
     const int k = atoi(env);
-    if (k == 2 || k == 4 || k == 8 || ((k == 5 || k == 6) && !dirs)) return k;
+    if (k == 2 || k == 4 || k == 8 || k == 5 || k == 6) return k;  // 5, 6: register profiles only
   }
   (void)dirs;
   // Tall pairs (>= ~150 strips at KR = 8): the largest KR, the lag is amortised
@@ -565,7 +571,7 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
   // workspace: padded code buffers and the tagged 2-slot boundary ring
   constexpr long long R = R_MAX;
   const long long la = pad16(PAD + m + R + PAD), lb = pad16(PAD + n + R + PAD);
-  int kr = choose_kr(m, n, want_dirs);
+  int kr = choose_kr(m, n, want_dirs, sc->K);
   // packed difference form (two rows per register) for tall score-only pairs: it
   // halves the ALU work per cell but doubles the lane skew, so it only pays when
   // there are enough 512-row strips to fill the GPU (measured: 1M^2 2.4 -> 5.9
@@ -792,7 +798,8 @@ static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops, bool
     const int left_cols = R + 128;  // > one strip's drift on a near-diagonal path
     const int gw_bytes = (kr * 16 + 1) * 4;
     if (S >= 2) {
-      auto kspec = kr == 2 ? k_tb_spec<2> : (kr == 4 ? k_tb_spec<4> : k_tb_spec<8>);
+      auto kspec = kr == 2 ? k_tb_spec<2> : kr == 4 ? k_tb_spec<4> : kr == 5 ? k_tb_spec<5>
+                 : kr == 6 ? k_tb_spec<6> : k_tb_spec<8>;
       const size_t win = (size_t)((32 * B.step + left_cols + 40) / 8 + 2) * gw_bytes;
       cudaFuncSetAttribute(kspec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win);
       kspec<<<(S - 1) * (B.nb / 32), 32, win, c->stream>>>(tb->dirs, tb->wpl, B, tb->tie[0],
@@ -800,7 +807,8 @@ static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops, bool
       LAUNCHED(c);
     }
     {
-      auto kchain = kr == 2 ? k_tb_chain<2> : (kr == 4 ? k_tb_chain<4> : k_tb_chain<8>);
+      auto kchain = kr == 2 ? k_tb_chain<2> : kr == 4 ? k_tb_chain<4> : kr == 5 ? k_tb_chain<5>
+                  : kr == 6 ? k_tb_chain<6> : k_tb_chain<8>;
       // exact walks: windows of ~96 KB of decision bits left of the entry
       // a window of 2R + 256 columns left of the entry (re-staged further left
       // when a long gap leaves it): staging, not the walk, dominated at 96 KB
@@ -815,7 +823,8 @@ static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops, bool
       LAUNCHED(c);
     }
     const int smem_bytes = 96 * 1024;
-    auto kseg = tb->kr == 2 ? k_tb_segments<2> : (tb->kr == 4 ? k_tb_segments<4> : k_tb_segments<8>);
+    auto kseg = kr == 2 ? k_tb_segments<2> : kr == 4 ? k_tb_segments<4> : kr == 5 ? k_tb_segments<5>
+              : kr == 6 ? k_tb_segments<6> : k_tb_segments<8>;
     cudaFuncSetAttribute(kseg, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     kseg<<<S, 32, smem_bytes, c->stream>>>(tb->dirs, tb->wpl, tb->m, tb->n, tb->tie[0],
                                            tb->tie[1], tb->tie[2], tb->cs, tb->seg, tb->segstride,
@@ -1731,7 +1740,7 @@ nw_status linear_core(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b
   st = stage_pair(c, a, m, b, n, true, &ca, &cb);
   if (st) return st;
   // segment height: directions take (n + 38) / 4 bytes per row
-  int kr_ck = choose_kr(m, n, false);
+  int kr_ck = choose_kr(m, n, false, sc->K);
   if (kr_ck == 16) kr_ck = 8;
   const long long Rck = 32LL * kr_ck;
   const long long rows_max = std::max<long long>(1, budget / ((n + 38) / 4 + 1));
@@ -1763,7 +1772,7 @@ nw_status linear_core(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b
     ZeroRanges zb{{c->d_bnd, nullptr, nullptr, nullptr}, {bbytes, 0, 0, 0}};
     st = init_small(c, 8, zb);  // fresh ticket, error flag and ring tags for this fill
     if (st) break;
-    const int kr = choose_kr(mm, col, true);
+    const int kr = choose_kr(mm, col, true, sc->K);
     nw_tb* tb = nullptr;
     st = new_tb(c, mm, col, sc, kr, &tb);
     if (st) break;

@@ -149,11 +149,11 @@ __device__ long long tb_walk(const uint16_t* dirs, long long G, int m, int n, in
 template <int KR>
 __device__ __forceinline__ int strip_exit_walk(const uint16_t* __restrict__ dirs, long long G,
                                                int i, int j, int i_stop, int X, int Y, int Z) {
-  constexpr int LKR = KR == 2 ? 1 : (KR == 4 ? 2 : 3), R = 32 * KR;
+  constexpr int R = 32 * KR;
   const uint16_t* base = dirs + (long long)((i - 1) / R) * G * (KR * 32);  // one strip
   while (i > i_stop && j > 0) {
-    const int ia = i - 1;
-    const int l = (ia >> LKR) & 31, r = ia & (KR - 1);
+    const unsigned ia = (unsigned)(i - 1);
+    const int l = (int)((ia % R) / KR), r = (int)(ia % KR);
     const int t = j - 1 + l;
     // L1-cached: consecutive steps mostly stay in one 128-byte line
     const uint32_t f = (uint32_t)__ldca(base + ((long long)(t >> 3) * KR + r) * 32 + l) >>
@@ -213,10 +213,10 @@ __device__ __forceinline__ void stage_groups(const uint16_t* __restrict__ src_hw
 template <int KR>
 __device__ __forceinline__ bool walk_window(const uint32_t* w32, int g_lo, int ng, int& i, int& j,
                                             int i_stop, int X, int Y, int Z) {
-  constexpr int LKR = KR == 2 ? 1 : (KR == 4 ? 2 : 3), GW = KR * 16 + 1;
+  constexpr int R = 32 * KR, GW = KR * 16 + 1;
   while (i > i_stop && j > 0) {
-    const int ia = i - 1;
-    const int l = (ia >> LKR) & 31, r = ia & (KR - 1);
+    const unsigned ia = (unsigned)(i - 1);
+    const int l = (int)((ia % R) / KR), r = (int)(ia % KR);
     const int t = j - 1 + l;
     const int g = (t >> 3) - g_lo;
     if ((unsigned)g >= (unsigned)ng) return false;

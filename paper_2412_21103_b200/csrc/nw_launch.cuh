@@ -42,6 +42,10 @@ void launch_batch_t(const BatchArgs& B, int grid, size_t smem, cudaStream_t st) 
     } else if (kr == 4) {                                                                     \
       if (profreg) launch_fill_t<4, true, true, PI>(A, grid, smem, st);                       \
       else launch_fill_t<4, true, false, PI>(A, grid, smem, st);                              \
+    } else if (kr == 5 && profreg) {                                                          \
+      launch_fill_t<5, true, true, PI>(A, grid, smem, st);                                    \
+    } else if (kr == 6 && profreg) {                                                          \
+      launch_fill_t<6, true, true, PI>(A, grid, smem, st);                                    \
     } else {                                                                                  \
       if (profreg) launch_fill_t<8, true, true, PI>(A, grid, smem, st);                       \
       else launch_fill_t<8, true, false, PI>(A, grid, smem, st);                              \

@@ -422,3 +422,22 @@ def test_batch_score_only_orientation(ctx, monkeypatch, sym):
         oracle.batch_score(ss.residues, ss.offs, rev, sc).tolist()
     monkeypatch.setenv("NW_BATCH_NO_TRANSPOSE", "1")
     assert nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc).tolist() == want.tolist()
+
+
+@pytest.mark.parametrize("kr", [2, 4, 5, 6, 8])
+def test_pair_every_rows_per_lane(ctx, monkeypatch, kr):
+    """The single-pair fill + strip traceback at every rows-per-lane setting (5 and 6:
+    strips of 160 / 192 rows, not powers of two), all tie orders on a tie-rich pair."""
+    monkeypatch.setenv("NW_KR", str(kr))
+    for k, (m, n) in enumerate([(32 * kr * 3 + 17, 1500), (2000, 700), (700, 2100), (5, 9)]):
+        a, b = _pair(9300 + 11 * kr + k, m, n)
+        check_pair(ctx, a, b, nwgen.PAPER_DNA)
+    rng = np.random.Generator(np.random.PCG64(kr))
+    a = nwgen.random_seq(rng, 1400, "AC")
+    b = nwgen.random_seq(rng, 1300, "AC")
+    for tie in ORDERS:
+        check_pair(ctx, a, b, nwgen.Scoring(tie=tie))
+    sc = nwgen.Scoring(match=0, mismatch=0, gap=-5, alphabet=nwgen.PROTEIN,
+                       subst=nwgen.BLOSUM62)        # K > 4: KR 5 / 6 fall back to 4
+    a, b = _pair(9400 + kr, 900, 1000, nwgen.PROTEIN)
+    check_pair(ctx, a, b, sc)
