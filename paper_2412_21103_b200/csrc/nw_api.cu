@@ -377,6 +377,19 @@ int choose_kr_shape(long long m, long long n, bool dirs) {
   return best;
 }
 
+// Rows per lane of the packed score-only sweep for a tall pair: the
+// strips advance in lock-step, so the pair runs at the pace of the most loaded SM
+// sub-partition: the smallest even KR >= 16 that keeps the strip count within two
+// warps per sub-partition (1M^2: KR 28 = 1,117 strips, 6.5 TCUPS, vs KR 32 = 977
+// strips 6.2 and KR 26 = 1,202 strips 5.5; tools/exp_c5kr.py). NW_D16_KR overrides.
+int d16_kr(long long m, int sm_count) {
+  int kd = 32;
+  for (int k = 16; k <= 32; k += 2)
+    if ((m + 32LL * k - 1) / (32LL * k) <= 8LL * sm_count) { kd = k; break; }
+  const int k = env_int("NW_D16_KR", kd, 12);
+  return (k >= 12 && k <= 32 && k % 2 == 0) ? k : kd;
+}
+
 bool dispatch_batch(bool dirs, int pi, bool profreg, bool u16, bool d16, int packed_kr,
                     const BatchArgs& B, int grid, size_t smem, cudaStream_t st) {
   if (!dirs) {
@@ -429,6 +442,59 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
 
 // ---- kernels for tiny bookkeeping ----
 namespace nwk {
+// Checkpoint rows of the packed score-only pass hold V(r, j) = H'(r, j) - H'(r, j-1)
+// as tagged entries j = 1..n; the refills read H'(r, j). One block
+// per slot turns each row into its inclusive prefix sum (H'(r, 0) = 0), tags kept.
+__global__ void __launch_bounds__(1024) k_ckpt_prefix(unsigned long long* ckpt, long long stride,
+                                                      int n, int nslots) {
+  if ((int)blockIdx.x >= nslots) return;
+  unsigned long long* row = ckpt + (long long)blockIdx.x * stride;
+  __shared__ int wsum[32];
+  __shared__ int carry_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int PER = 8, TILE = 1024 * PER;
+  if (tid == 0) carry_s = 0;
+  __syncthreads();
+  for (int base = 1; base <= n; base += TILE) {
+    unsigned long long e[PER];
+    int acc = 0;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int j = base + tid * PER + u;
+      e[u] = j <= n ? row[j] : 0ull;
+      acc += (int)(unsigned)e[u];
+    }
+    int x = acc;  // inclusive scan of the per-thread totals
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int w = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    int run = carry_s + (warp ? wsum[warp - 1] : 0) + x - acc;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int j = base + tid * PER + u;
+      run += (int)(unsigned)e[u];
+      if (j <= n) row[j] = (e[u] & 0xffffffff00000000ull) | (unsigned)run;
+    }
+    __syncthreads();
+    if (tid == 1023) carry_s = run;
+    __syncthreads();
+  }
+}
+
 __global__ void k_finish_score(const int* hm, long long gmn, long long* out, int m_or_n_zero) {
   *out = (m_or_n_zero ? 0 : (long long)*hm) + gmn;
 }
@@ -576,20 +642,8 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
   // halves the ALU work per cell but doubles the lane skew, so it only pays when
   // there are enough 512-row strips to fill the GPU (measured: 1M^2 2.4 -> 5.9
   // TCUPS; 20k^2 1.44 -> 2.14 ms, slower)
-  // and 32 rows per lane once there are >= ~150 strips of 1,024 rows (1M^2: 5.4 -> 6.2
-  // TCUPS; 64 rows: 4.5). NW_D16_KR overrides (16 or 32).
-  // The strips of one pair advance in lock-step (each waits on the one above), so
-  // the pair runs at the pace of the most loaded SM sub-partition: the rows per
-  // lane are the smallest even KR >= 16 that keeps the strip count within two
-  // warps per sub-partition (1M^2: KR 28 = 1,117 strips, 6.5 TCUPS, vs KR 32 =
-  // 977 strips 6.2 and KR 26 = 1,202 strips 5.5; tools/exp_c5kr.py).
-  if (!want_dirs && d16_ok(sc) && m >= 32LL * 16 * 150) {
-    int kd = 32;
-    for (int k = 16; k <= 32; k += 2)
-      if ((m + 32LL * k - 1) / (32LL * k) <= 8LL * c->sm_count) { kd = k; break; }
-    const int k = env_int("NW_D16_KR", kd, 12);
-    kr = (k >= 12 && k <= 32 && k % 2 == 0) ? k : kd;
-  }
+  // and 28-32 rows per lane by the strip-count rule of d16_kr.
+  if (!want_dirs && d16_ok(sc) && m >= 32LL * 16 * 150) kr = d16_kr(m, c->sm_count);
   // experiments: NW_D16_FORCE=<4|8|16|32> runs any score-only pair in the packed form
   if (!want_dirs && d16_ok(sc) && getenv("NW_D16_FORCE")) {
     const int f = env_int("NW_D16_FORCE", 16, 4);
@@ -1740,8 +1794,10 @@ nw_status linear_core(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b
   st = stage_pair(c, a, m, b, n, true, &ca, &cb);
   if (st) return st;
   // segment height: directions take (n + 38) / 4 bytes per row
-  int kr_ck = choose_kr(m, n, false, sc->K);
-  if (kr_ck == 16) kr_ck = 8;
+  // the checkpoint pass is score-only: the packed difference form when it applies
+  // (its rows carry V; k_ckpt_prefix turns them into H' for the refills)
+  const bool ck_d16 = d16_ok(sc) && m >= 32LL * 16 * 150 && !getenv("NW_LINEAR_INT32");
+  const int kr_ck = ck_d16 ? d16_kr(m, c->sm_count) : choose_kr(m, n, false, sc->K);
   const long long Rck = 32LL * kr_ck;
   const long long rows_max = std::max<long long>(1, budget / ((n + 38) / 4 + 1));
   const long long K = std::max<long long>(1, rows_max / Rck);
@@ -1756,6 +1812,11 @@ nw_status linear_core(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b
   auto done = [&](nw_status e) { if (ckpt) cudaFreeAsync(ckpt, c->stream); return e; };
   st = pair_core(c, ca, m, cb, n, sc, c->d_score, nullptr, kr_ck, ckpt, (int)K, bstr, nullptr);
   if (st) return done(st);
+  if (ck_d16 && nseg > 1) {
+    k_ckpt_prefix<<<(unsigned)nseg, 1024, 0, c->stream>>>(ckpt, bstr, (int)n, (int)nseg);
+    LAUNCHED(c);
+    CUDA_TRY(c, cudaGetLastError());
+  }
   CUDA_TRY(c, cudaMemcpyAsync(score_out, c->d_score, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   st = check_deferred(c);  // synchronises; reports alphabet errors
   if (st) return done(st);

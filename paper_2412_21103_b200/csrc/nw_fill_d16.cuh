@@ -137,6 +137,11 @@ __device__ __forceinline__ void strip_sweep_d16(const FillArgs& A, int s, int la
   char* bnd = static_cast<char*>(A.bnd);
   C.bnd_in = (s > 0) ? bnd + esz * (size_t)((s % A.nslots) * A.bstride) : nullptr;
   C.bnd_out = bnd + esz * (size_t)(((s + 1) % A.nslots) * A.bstride);
+  if (MULTIWARP && A.ckpt != nullptr) {  // checkpointed traceback pass:
+    // every ck_every-th strip hands its bottom row's V over through a kept slot
+    if ((s + 1) % A.ck_every == 0) C.bnd_out = A.ckpt + (long long)((s + 1) / A.ck_every - 1) * A.ck_stride;
+    if (s > 0 && s % A.ck_every == 0) C.bnd_in = A.ckpt + (long long)(s / A.ck_every - 1) * A.ck_stride;
+  }
   C.dir_base = nullptr;
   C.err = A.err;
   C.poll_ns = A.poll_ns;
