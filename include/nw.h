@@ -128,7 +128,12 @@ void nw_tb_free(nw_tb *tb);
  * With NW_TRACEBACK: ops_off: npairs+1 int64 filled by the library with the offsets
  *        (ops_off[k] = sum over k' < k of (m_k' + n_k'), the worst-case path lengths),
  *        ops: ops_off[npairs] bytes; pair k's path (forward codes) is at
- *        ops[ops_off[k] .. ops_off[k] + ops_len[k]). Unused otherwise (may be NULL). */
+ *        ops[ops_off[k] .. ops_off[k] + ops_len[k]). Unused otherwise (may be NULL).
+ * Workspace (owned by ctx, kept between calls): with NW_TRACEBACK and s - 2g >= 0 for
+ * every symbol pair, every pair's decision bits (about m*n/4 bytes each; C4: 7.6 GB)
+ * stay in device memory until a second kernel walks them; pairs are processed in
+ * waves that fit half the free device memory, NW_E_NOMEM if one pair does not. The
+ * score and paths do not depend on the order pairs are processed in. */
 #define NW_SCORE_ONLY 0u
 #define NW_TRACEBACK 1u
 nw_status nw_align_batch(nw_ctx *ctx, const uint8_t *seqs, const int64_t *offs, int32_t nseq,
