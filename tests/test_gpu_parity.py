@@ -441,3 +441,25 @@ def test_pair_every_rows_per_lane(ctx, monkeypatch, kr):
                        subst=nwgen.BLOSUM62)        # K > 4: KR 5 / 6 fall back to 4
     a, b = _pair(9400 + kr, 900, 1000, nwgen.PROTEIN)
     check_pair(ctx, a, b, sc)
+
+
+def test_batch_caller_owned_outputs(ctx):
+    """nw_align_batch(out=...) fills caller-owned (e.g. page-locked) arrays with the
+    same results as freshly allocated ones; too-small buffers are rejected."""
+    ss = nwgen.random_set(81, 20, 0, 600, nwgen.PROTEIN)
+    rng = np.random.Generator(np.random.PCG64(81))
+    pairs = rng.integers(0, ss.nseq, size=(50, 2)).astype(np.int32)
+    sc = nwgen.PROTEIN_BLOSUM62
+    want = nwb.nw_align_batch(ctx, ss.residues, ss.offs, pairs, sc, nwb.NW_TRACEBACK)
+    tot = int(nwb.nw_batch_ops_offsets(ss.offs, pairs)[-1])
+    out = (np.empty(50, np.int32), np.empty(tot + 1, np.uint8), np.empty(51, np.int64),
+           np.empty(50, np.int32))
+    got = nwb.nw_align_batch(ctx, ss.residues, ss.offs, pairs, sc, nwb.NW_TRACEBACK, out=out)
+    assert got[0] is out[0] and got[0].tolist() == want[0].tolist()
+    assert [p.tolist() for p in nwb.batch_paths(*got[1:])] == \
+        [p.tolist() for p in nwb.batch_paths(*want[1:])]
+    s_out = np.empty(len(nwgen.all_pairs(ss.nseq)), np.int32)
+    s = nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc, out=s_out)
+    assert s is s_out and s.tolist() == nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc).tolist()
+    with pytest.raises(ValueError):
+        nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc, out=s_out[:10])
