@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -57,6 +58,9 @@ struct nw_ctx {
   size_t scratch_cap = 0;
   void* d_aux = nullptr;        // batch perm/order/offs/pairs staging
   size_t aux_cap = 0;
+  // host scratch of the batch planner, kept between calls (no page faults per call)
+  std::vector<int> h_aux, h_bkt, h_cnt;
+  std::vector<long long> h_words, h_tw, h_tdoff;
   void* h_stage = nullptr;      // page-locked staging for per-call host tables (batch order, offsets)
   size_t stage_cap = 0;
   cudaEvent_t stage_ev = nullptr;  // the last staged copy (the buffer is reused after it)
@@ -1129,11 +1133,23 @@ nw_status nw_batch_ops_offsets(const int64_t* h_offs, int32_t nseq, const int32_
 namespace {
 
 // Shared body of the batch entry points. All pointers device; h_offs/h_pairs host.
+struct HostLaps {  // NW_HOST_PROFILE=1: host-side phase times of one call, to stderr
+  bool on = getenv("NW_HOST_PROFILE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "  [host] %-24s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool already_coded,
                      const long long* d_offs, const long long* h_offs, int nseq, const int* d_pairs,
                      const int* h_pairs, long long npairs, const nw_scoring* sc, uint32_t flags,
                      int* d_scores, const long long* d_ops_off, uint8_t* d_ops, int* d_ops_len) {
   constexpr int R = 32 * KR_BATCH;
+  HostLaps hl;
   const bool tbk = (flags & NW_TRACEBACK) != 0;
   const long long total = h_offs[nseq];
   long long maxlen = 0;
@@ -1151,37 +1167,19 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   uint8_t* codes = c->d_codes + PAD;
   (void)already_coded;
   launch_encode(c, d_codes_raw_or_codes, total, codes, 0);
+  hl.lap("bounds, memset, encode");
   // order: implicit all-pairs -> perm of sequences by length (descending);
   // explicit pairs -> LPT order by m*n (descending), bucketed.
-  std::vector<int> aux;
+  std::vector<int>& aux = c->h_aux;
+  aux.clear();
   if (!h_pairs) {
     aux.resize(nseq);
     for (int k = 0; k < nseq; ++k) aux[k] = k;
     std::stable_sort(aux.begin(), aux.end(), [&](int x, int y) {
       return (h_offs[x + 1] - h_offs[x]) > (h_offs[y + 1] - h_offs[y]);
     });
-  } else {
-    // counting sort on the cost quantised to NB levels (descending, stable): O(npairs),
-    // where a comparison sort of C4's 100k pairs took ~15 ms of host time per call
-    // and left the GPU idle (tools/exp_c4.py)
-    aux.resize(npairs);
-    std::vector<long long> cst((size_t)npairs);
-    long long cmax = 1;
-    for (long long k = 0; k < npairs; ++k) {
-      const int p = h_pairs[2 * k], q = h_pairs[2 * k + 1];
-      cst[k] = (h_offs[p + 1] - h_offs[p]) * (h_offs[q + 1] - h_offs[q]);
-      cmax = std::max(cmax, cst[k]);
-    }
-    constexpr int NB = 4096;
-    const double scale = (double)(NB - 1) / (double)cmax;
-    std::vector<int> cnt(NB + 1, 0);
-    auto bucket = [&](long long k) { return (NB - 1) - std::min(NB - 1, (int)((double)cst[k] * scale)); };
-    for (long long k = 0; k < npairs; ++k) ++cnt[bucket(k) + 1];
-    for (int b = 0; b < NB; ++b) cnt[b + 1] += cnt[b];
-    for (long long k = 0; k < npairs; ++k) aux[cnt[bucket(k)]++] = (int)k;
-  }
-  st = grow(c, c->d_aux, c->aux_cap, sizeof(int) * aux.size() + 16);
-  if (st) return st;
+  }  // explicit pairs: ordered below, once the strip height is known
+  hl.lap("implicit order");
 
   // per-warp scratch
   const int warps_per_cta = 4;
@@ -1223,7 +1221,61 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   // of idling 31 lanes of a filling warp. Pairs are cut into waves whose words fit
   // the budget (half the free memory; NW_BATCH_TB_BUDGET bytes overrides).
   const bool two_phase = tbk && d16;
-  std::vector<long long> tdoff, wave_end;
+  bool sym = true;  // s(x, y) = s(y, x): a pair may be filled transposed
+  for (int x = 0; x < sc->K; ++x)
+    for (int y = 0; y < x; ++y) sym = sym && score_of(sc, x, y) == score_of(sc, y, x);
+  long long ntr0 = npairs;  // explicit-pair tasks [ntr0, npairs) are filled transposed
+  if (h_pairs) {
+    // LPT order: counting sort on the cost quantised to NB levels (descending,
+    // stable), O(npairs) -- a comparison sort of C4's 100k pairs took ~15 ms of host
+    // time per call and left the GPU idle (tools/exp_c4.py). Two-phase traceback with
+    // a symmetric s also picks each pair's orientation here: a pair is filled with b
+    // on the rows when that sweeps fewer padded cells (strips x (columns + skew));
+    // its flags are those of the mirrored tie order (U <-> L) on the transposed grid,
+    // whose path is the pair's own with U and L exchanged (the oracle's mirror pin).
+    // C4: 1.38x -> 1.29x the useful cells. Transposed tasks come after the others
+    // (NB more buckets), each part in LPT order; each part is its own fill launch.
+    const bool orient = two_phase && sym && !getenv("NW_BATCH_NO_TRANSPOSE");
+    // one pass: bucket (cost quantised against maxlen^2, so no max pass), orientation
+    // and the pair's flag words; a second pass scatters them into LPT order
+    constexpr int NB = 4096;
+    const long long wpg = RS / 2;
+    int lrs = 0;  // RS is a power of two: strip counts by shifts (divisions dominated this loop)
+    while ((1LL << lrs) < RS) ++lrs;
+    // bucket = (NB-1) - floor(cost * (NB-1) / maxlen^2) in integers (cost <= maxlen^2)
+    const unsigned long long inv = ((unsigned long long)(NB - 1) << 32) /
+                                   (unsigned long long)std::max(1LL, maxlen * maxlen);
+    aux.resize(npairs);
+    c->h_bkt.resize(npairs);
+    c->h_words.resize(two_phase ? npairs : 0);
+    c->h_cnt.assign(2 * NB + 1, 0);
+    int* bk = c->h_bkt.data();
+    int* cnt = c->h_cnt.data();
+    long long* wd = c->h_words.data();
+    // (an OpenMP split of these loops made the C4 step slower: the worker threads'
+    // spin-wait competes with the launching thread)
+    for (long long k = 0; k < npairs; ++k) {
+      const int p = h_pairs[2 * k], q = h_pairs[2 * k + 1];
+      const long long m = h_offs[p + 1] - h_offs[p], n = h_offs[q + 1] - h_offs[q];
+      const long long sm_ = (m + RS - 1) >> lrs, sn_ = (n + RS - 1) >> lrs;
+      const bool tr = orient && m > 0 && n > 0 &&  // empty pairs never: k_batch writes their gaps
+                      sn_ * (m + 70) < sm_ * (n + 70);
+      const int q16 = (int)(((unsigned long long)(m * n) * inv) >> 32);
+      bk[k] = (tr ? NB : 0) + (NB - 1) - std::min(NB - 1, q16);
+      ++cnt[bk[k] + 1];
+      if (two_phase)
+        wd[k] = (m > 0 && n > 0) ? (tr ? sn_ * ((m + 70) >> 3) : sm_ * ((n + 70) >> 3)) * wpg : 0LL;
+    }
+    for (int b = 0; b < 2 * NB; ++b) cnt[b + 1] += cnt[b];
+    if (orient) ntr0 = cnt[NB];
+    for (long long k = 0; k < npairs; ++k) aux[cnt[bk[k]]++] = (int)k;
+  }
+  hl.lap("LPT order + orientation");
+  st = grow(c, c->d_aux, c->aux_cap, sizeof(int) * aux.size() + 16);
+  if (st) return st;
+  std::vector<long long>& tdoff = c->h_tdoff;
+  std::vector<long long> wave_end;
+  tdoff.clear();
   if (two_phase) {
     const long long wpg = RS / 2;  // words per (strip, 8-step group): H packed rows x 32 lanes
     auto len = [&](int s) { return h_offs[s + 1] - h_offs[s]; };
@@ -1233,10 +1285,13 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
     // words of every task in the fill's order: explicit pairs by aux (LPT), implicit
     // all-pairs in rank order over the length-sorted sequences (aux = that perm),
     // the row sequence being the lower original index as in task_pair
-    std::vector<long long> tw((size_t)npairs);
+    std::vector<long long>& tw = c->h_tw;
+    tw.resize(npairs);
     if (h_pairs) {
-      for (long long t = 0; t < npairs; ++t)
-        tw[t] = words_mn(len(h_pairs[2 * aux[t]]), len(h_pairs[2 * aux[t] + 1]));
+      const long long* wd = c->h_words.data();
+      const int* ax = aux.data();
+      long long* twp = tw.data();
+      for (long long t = 0; t < npairs; ++t) twp[t] = wd[ax[t]];
     } else {
       long long t = 0;
       for (int pr = 0; pr < nseq; ++pr)
@@ -1276,7 +1331,9 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   {
     const StagedCopy cp[2] = {{c->d_aux, aux.data(), sizeof(int) * aux.size()},
                               {c->d_tdoff, tdoff.data(), sizeof(long long) * tdoff.size()}};
+    hl.lap("words, waves, grow");
     st = upload_staged(c, cp, 2);
+    hl.lap("staged upload");
     if (st) return st;
   }
   const size_t smem_prof = profreg ? 0 : (((size_t)warps_per_cta * sc->K * RS + 15) & ~size_t(15));
@@ -1321,12 +1378,9 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   B.ops_off = d_ops_off;
   B.ops = d_ops;
   B.ops_len = d_ops_len;
-  {
-    bool sym = true;
-    for (int x = 0; x < sc->K; ++x)
-      for (int y = 0; y < x; ++y) sym = sym && score_of(sc, x, y) == score_of(sc, y, x);
-    B.transpose_ok = (!tbk && sym && !getenv("NW_BATCH_NO_TRANSPOSE")) ? 1 : 0;
-  }
+  B.transpose_ok = (!tbk && sym && !getenv("NW_BATCH_NO_TRANSPOSE")) ? 1 : 0;
+  B.transposed = 0;
+  B.ntr0 = ntr0;
   B.tdirs = two_phase ? static_cast<uint32_t*>(c->d_tbdirs) : nullptr;
   B.tdir_off = two_phase ? c->d_tdoff : nullptr;
   B.task0 = 0;
@@ -1342,20 +1396,34 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   // min(m,n) * max(s') <= 65535 for every pair (bounded by the longest sequence)
 
   if (two_phase) {
+    hl.lap("scratch, args");
     long long t0 = 0;
+    bool first = true;
     for (const long long t1 : wave_end) {
       if (t1 <= t0) continue;
+      // fills: the wave's normal tasks, then its transposed tasks (mirrored tie order)
+      for (int part = 0; part < 2; ++part) {
+        const long long a0 = part ? std::max(t0, ntr0) : t0, a1 = part ? t1 : std::min(t1, ntr0);
+        if (a1 <= a0) continue;
+        uint8_t tie[3];
+        for (int i = 0; i < 3; ++i) tie[i] = (uint8_t)(part && sc->tie[i] != 1 ? 5 - sc->tie[i] : sc->tie[i]);
+        B.task0 = a0;
+        B.task1 = a1;
+        B.transposed = part;
+        if (!first) CUDA_TRY(c, cudaMemsetAsync(B.ticket, 0, sizeof(int), c->stream));
+        first = false;
+        bool ok;
+        {
+          KernelTimer kt(c, 0);
+          ok = dispatch_batch(tbk, pi_code(tie), profreg, u16, d16, packed_kr, B, grid, smem, c->stream);
+        }
+        if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
+        LAUNCHED(c);
+        CUDA_TRY(c, cudaGetLastError());
+      }
       B.task0 = t0;
       B.task1 = t1;
-      if (t0 > 0) CUDA_TRY(c, cudaMemsetAsync(B.ticket, 0, sizeof(int), c->stream));
-      bool ok;
-      {
-        KernelTimer kt(c, 0);
-        ok = dispatch_batch(tbk, pi, profreg, u16, d16, packed_kr, B, grid, smem, c->stream);
-      }
-      if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
-      LAUNCHED(c);
-      CUDA_TRY(c, cudaGetLastError());
+      B.transposed = 0;
       {  // (walking every 32 pairs inside the filling warp instead was slower on C4:
          // fill + walk 12.74 vs 10.93 + 1.52 ms, profiles/r01_exp_c4_walk_inline.txt)
         KernelTimer kt(c, 1);
@@ -1367,6 +1435,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
       }
       t0 = t1;
     }
+    hl.lap("launches");
     return NW_OK;
   }
   bool ok;

@@ -466,6 +466,9 @@ struct BatchArgs {
   uint32_t* tdirs;
   const long long* tdir_off;
   long long task0, task1;  // tasks [task0, task1) of this launch (a wave)
+  int transposed;          // this fill launch sweeps its pairs transposed (b on the rows;
+                           // the kernel's tie order is the mirrored one)
+  long long ntr0;          // the walk: tasks >= ntr0 were filled transposed
 };
 
 // flat rank-space index k -> (p', q'), p' < q', lexicographic over N items
@@ -528,6 +531,10 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
     task_pair(B, task, p, q, outk);
     long long ao = B.offs[p], bo = B.offs[q];
     int m = (int)(B.offs[p + 1] - ao), n = (int)(B.offs[q + 1] - bo);
+    if (DIRS && PACKED == 3 && B.transposed && m > 0 && n > 0) {  // the host's orientation choice
+      const long long to = ao; ao = bo; bo = to;
+      const int tm = m; m = n; n = tm;
+    }
     if (!DIRS && B.transpose_ok) {
       // score-only with a symmetric s: Score(a, b) = Score(b, a) (the transpose
       // invariant of the oracle pins), so put on the rows whichever sequence wastes
@@ -611,6 +618,13 @@ __device__ __forceinline__ void walk_lanes(const BatchArgs& B, long long task, b
     n = (int)(B.offs[q + 1] - B.offs[q]);
     act = m > 0 && n > 0;
   }
+  // a transposed pair: walk the swept (transposed) grid with the mirrored tie order and
+  // emit its vertical moves as horizontal ones and vice versa
+  const bool tr = act && task >= B.ntr0;
+  if (tr) { const int tm = m; m = n; n = tm; }
+  const int cV = tr ? 3 : 2, cH = tr ? 2 : 3;
+  const int X = tr && B.X != 1 ? 5 - B.X : B.X, Y = tr && B.Y != 1 ? 5 - B.Y : B.Y,
+            Z = tr && B.Z != 1 ? 5 - B.Z : B.Z;
   uint8_t* o = nullptr;
   int pos = 0;
   if (act) {
@@ -634,13 +648,13 @@ __device__ __forceinline__ void walk_lanes(const BatchArgs& B, long long task, b
       }
       const int qq = t & 7;
       const uint32_t fx = (w >> (8 * hi + qq)) & 1u, fy = (w >> (16 + 8 * hi + qq)) & 1u;
-      const int code = fx ? B.X : (fy ? B.Y : B.Z);
-      o[--pos] = (uint8_t)code;
+      const int code = fx ? X : (fy ? Y : Z);
+      o[--pos] = (uint8_t)(code == 1 ? 1 : (code == 2 ? cV : cH));
       i -= (code != 3);
       j -= (code != 2);
     }
-    while (i > 0) { o[--pos] = 2; --i; }  // column 0: vertical (R7)
-    while (j > 0) { o[--pos] = 3; --j; }  // row 0: horizontal
+    while (i > 0) { o[--pos] = (uint8_t)cV; --i; }  // column 0: vertical (R7)
+    while (j > 0) { o[--pos] = (uint8_t)cH; --j; }  // row 0: horizontal
     B.ops_len[outk] = m + n - pos;
   }
   // move each path [pos, m + n) of its slot to [0, L): increasing 32-byte chunks,

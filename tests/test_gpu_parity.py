@@ -377,15 +377,24 @@ def test_batch_traceback_paths_all_orders(ctx, tie, scname):
         assert scores[k] == ws and paths[k].tolist() == wops.tolist(), (k, len(ss.seq(p)), len(ss.seq(q)))
 
 
-@pytest.mark.parametrize("mode", ["waves", "kr16", "implicit"])
+@pytest.mark.parametrize("mode", ["waves", "kr16", "implicit", "notranspose", "asymmetric"])
 def test_batch_traceback_two_phase_modes(ctx, monkeypatch, mode):
     """Two-phase batch traceback (the fill keeps every pair's flags, k_batch_walk walks
-    them, one thread per pair): split into many waves by a tiny direction budget,
-    16-rows-per-lane strips, and all pairs (pairs=None: tasks in rank order over the
-    length-sorted sequences) in waves; pairs include empty sequences and lengths
+    them, one thread per pair; pairs whose last strip would waste more lanes are
+    filled transposed under the mirrored tie order): split into many waves by a tiny
+    direction budget, 16-rows-per-lane strips, all pairs (pairs=None: tasks in rank
+    order over the length-sorted sequences) in waves, no transposition, and an
+    asymmetric s (never transposed); pairs include empty sequences and lengths
     across strip edges."""
+    subst = nwgen.BLOSUM62
     if mode == "kr16":
         monkeypatch.setenv("NW_BATCH_KR16", "16")
+    elif mode == "notranspose":
+        monkeypatch.setenv("NW_BATCH_NO_TRANSPOSE", "1")
+    elif mode == "asymmetric":  # s(x,y) != s(y,x): never filled transposed
+        subst = np.array(nwgen.BLOSUM62, dtype=np.int32).copy()
+        subst[0, 1] += 2
+        subst[5, 9] -= 1
     else:
         monkeypatch.setenv("NW_BATCH_TB_BUDGET", str(300_000))
     ss = nwgen.random_set(61, 30 if mode != "implicit" else 14, 0, 1300, nwgen.PROTEIN)
@@ -393,9 +402,9 @@ def test_batch_traceback_two_phase_modes(ctx, monkeypatch, mode):
     pairs = rng.integers(0, ss.nseq, size=(120, 2)).astype(np.int32)
     if mode == "implicit":
         pairs = nwgen.all_pairs(ss.nseq)
-    for tie in [(1, 2, 3), (2, 3, 1)]:
+    for tie in [(1, 2, 3), (2, 3, 1), (3, 1, 2)]:
         sc = nwgen.Scoring(match=0, mismatch=0, gap=-5, alphabet=nwgen.PROTEIN,
-                           subst=nwgen.BLOSUM62, tie=tie)
+                           subst=subst, tie=tie)
         arg = None if mode == "implicit" else pairs
         scores, *flat = nwb.nw_align_batch(ctx, ss.residues, ss.offs, arg, sc, nwb.NW_TRACEBACK)
         paths = nwb.batch_paths(*flat)

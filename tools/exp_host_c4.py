@@ -1,0 +1,24 @@
+"""Host-side phases of one C4 nw_align_batch_dev call (NW_HOST_PROFILE) plus the
+Python-level call time."""
+import os, sys, time
+os.environ["NW_HOST_PROFILE"] = "1"
+sys.path.insert(0, '.')
+import numpy as np, torch, nwgen
+import paper_2412_21103_b200 as nwb
+ctx = nwb.Context(0, torch.cuda.current_stream().cuda_stream)
+ss = nwgen.config_c4()
+pairs = nwgen.consecutive_pairs(ss.nseq // 2)
+sc = nwgen.PROTEIN_BLOSUM62
+d_seqs = torch.from_numpy(ss.residues).cuda(); d_offs = torch.from_numpy(ss.offs).cuda()
+d_pairs = torch.from_numpy(pairs).cuda()
+oo = nwb.nw_batch_ops_offsets(ss.offs, pairs); d_oo = torch.from_numpy(oo).cuda()
+d_ops = torch.zeros(int(oo[-1]) + 1, dtype=torch.uint8, device="cuda")
+d_len = torch.zeros(len(pairs), dtype=torch.int32, device="cuda")
+d_sc = torch.zeros(len(pairs), dtype=torch.int32, device="cuda")
+for i in range(4):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    nwb.nw_align_batch_dev(ctx, d_seqs, d_offs, ss.offs, d_pairs, pairs, len(pairs), sc, nwb.NW_TRACEBACK, d_sc, d_oo, d_ops, d_len)
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    print(f"call {i}: python-level enqueue {1e3*(t1-t0):.3f} ms", file=sys.stderr, flush=True)
