@@ -5,6 +5,7 @@
 // nw_kernels.cuh; this file only marshals. There is no CPU fallback: without
 // a CUDA device every entry point returns NW_E_CUDA.
 #include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -61,6 +62,8 @@ struct nw_ctx {
   // host scratch of the batch planner, kept between calls (no page faults per call)
   std::vector<int> h_aux, h_bkt, h_cnt;
   std::vector<long long> h_words, h_tw, h_tdoff;
+  void* d_plan = nullptr;        // device batch planner scratch (buckets, words, histogram, scan)
+  size_t plan_cap = 0;
   void* h_stage = nullptr;      // page-locked staging for per-call host tables (batch order, offsets)
   size_t stage_cap = 0;
   cudaEvent_t stage_ev = nullptr;  // the last staged copy (the buffer is reused after it)
@@ -763,6 +766,7 @@ void nw_ctx_destroy(nw_ctx* c) {
   if (c->d_rev) cudaFreeAsync(c->d_rev, c->stream);
   if (c->d_scratch) cudaFreeAsync(c->d_scratch, c->stream);
   if (c->d_aux) cudaFreeAsync(c->d_aux, c->stream);
+  if (c->d_plan) cudaFreeAsync(c->d_plan, c->stream);
   if (c->stage_ev) { cudaEventSynchronize(c->stage_ev); cudaEventDestroy(c->stage_ev); }
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->d_tbdirs) cudaFreeAsync(c->d_tbdirs, c->stream);
@@ -1133,6 +1137,126 @@ nw_status nw_batch_ops_offsets(const int64_t* h_offs, int32_t nseq, const int32_
 namespace {
 
 // Shared body of the batch entry points. All pointers device; h_offs/h_pairs host.
+// ---- device batch planner (explicit pairs, two-phase traceback) ----
+// The host plan of batch_core computed on the GPU: cost buckets (LPT), orientation,
+// per-pair flag words, bucket starts, a scatter into task order and the word
+// offsets (a CUB scan). Order within a bucket follows atomic arrival: it changes
+// only the schedule, never a result (every output is indexed by the pair).
+constexpr int PLAN_NB = 4096;
+
+__global__ void k_plan_bucket(const int* __restrict__ pairs, const long long* __restrict__ offs,
+                              long long np, int lrs, unsigned long long inv, int orient,
+                              long long wpg, int* bkt, long long* words, int* hist) {
+  __shared__ int h[2 * PLAN_NB];
+  for (int i = threadIdx.x; i < 2 * PLAN_NB; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const long long RS = 1LL << lrs;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < np;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int p = pairs[2 * k], q = pairs[2 * k + 1];
+    const long long m = offs[p + 1] - offs[p], n = offs[q + 1] - offs[q];
+    const long long sm_ = (m + RS - 1) >> lrs, sn_ = (n + RS - 1) >> lrs;
+    const bool tr = orient && m > 0 && n > 0 && sn_ * (m + 70) < sm_ * (n + 70);
+    const int q16 = (int)(((unsigned long long)(m * n) * inv) >> 32);
+    const int b = (tr ? PLAN_NB : 0) + (PLAN_NB - 1) - min(PLAN_NB - 1, q16);
+    bkt[k] = b;
+    words[k] = (m > 0 && n > 0) ? (tr ? sn_ * ((m + 70) >> 3) : sm_ * ((n + 70) >> 3)) * wpg : 0LL;
+    atomicAdd(&h[b], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * PLAN_NB; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// in place: hist -> exclusive bucket starts; small[0] = start of the transposed buckets
+__global__ void __launch_bounds__(1024) k_plan_scan(int* hist, long long* small) {
+  __shared__ int ws[32];
+  constexpr int PER = 2 * PLAN_NB / 1024;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int v[PER], acc = 0;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) { v[u] = hist[tid * PER + u]; acc += v[u]; }
+  int x = acc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(0xffffffffu, w, o); if (lane >= o) w += y; }
+    ws[lane] = w;
+  }
+  __syncthreads();
+  int run = (warp ? ws[warp - 1] : 0) + x - acc;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int b = tid * PER + u;
+    if (b == PLAN_NB) small[0] = run;
+    hist[b] = run;
+    run += v[u];
+  }
+}
+
+__global__ void k_plan_scatter(const int* __restrict__ bkt, const long long* __restrict__ words,
+                               long long np, int* starts, int* aux, long long* tw) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < np;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int pos = atomicAdd(&starts[bkt[k]], 1);
+    aux[pos] = (int)k;
+    tw[pos] = words[k];
+  }
+}
+
+__global__ void k_plan_total(const long long* tw, const long long* tdoff, long long np, long long* small) {
+  small[1] = tdoff[np - 1] + tw[np - 1];
+}
+
+// Fills c->d_aux (task -> pair) and c->d_tdoff (task -> word offset); returns the
+// first transposed task and the total words (one small device -> host copy).
+nw_status device_plan(nw_ctx* c, const int* d_pairs, const long long* d_offs, long long npairs,
+                      long long RS, long long maxlen, bool orient, long long* ntr0, long long* total) {
+  int lrs = 0;
+  while ((1LL << lrs) < RS) ++lrs;
+  const unsigned long long inv = ((unsigned long long)(PLAN_NB - 1) << 32) /
+                                 (unsigned long long)std::max(1LL, maxlen * maxlen);
+  size_t cub_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (const long long*)nullptr, (long long*)nullptr,
+                                (int)npairs, c->stream);
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t b_bkt = al(sizeof(int) * npairs), b_w = al(sizeof(long long) * npairs),
+               b_h = al(sizeof(int) * (2 * PLAN_NB + 1)), b_small = 256, b_tw = b_w;
+  nw_status st = grow(c, c->d_plan, c->plan_cap, b_bkt + b_w + b_h + b_small + b_tw + al(cub_bytes));
+  if (st) return st;
+  st = grow(c, c->d_aux, c->aux_cap, sizeof(int) * (size_t)npairs + 16);
+  if (st) return st;
+  st = grow(c, c->d_tdoff, c->tdoff_cap, sizeof(long long) * (size_t)npairs);
+  if (st) return st;
+  char* p = static_cast<char*>(c->d_plan);
+  int* bkt = reinterpret_cast<int*>(p); p += b_bkt;
+  long long* words = reinterpret_cast<long long*>(p); p += b_w;
+  int* hist = reinterpret_cast<int*>(p); p += b_h;
+  long long* small = reinterpret_cast<long long*>(p); p += b_small;
+  long long* tw = reinterpret_cast<long long*>(p); p += b_tw;
+  void* cub_tmp = p;
+  CUDA_TRY(c, cudaMemsetAsync(hist, 0, sizeof(int) * 2 * PLAN_NB, c->stream));
+  const int blocks = (int)std::min<long long>((npairs + 255) / 256, (long long)c->sm_count * 4);
+  k_plan_bucket<<<blocks, 256, 0, c->stream>>>(d_pairs, d_offs, npairs, lrs, inv, orient ? 1 : 0,
+                                                RS / 2, bkt, words, hist);
+  k_plan_scan<<<1, 1024, 0, c->stream>>>(hist, small);
+  k_plan_scatter<<<blocks, 256, 0, c->stream>>>(bkt, words, npairs, hist, static_cast<int*>(c->d_aux), tw);
+  CUDA_TRY(c, cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, tw, c->d_tdoff, (int)npairs, c->stream));
+  k_plan_total<<<1, 1, 0, c->stream>>>(tw, c->d_tdoff, npairs, small);
+  c->launches += 5;
+  CUDA_TRY(c, cudaGetLastError());
+  long long h[2] = {0, 0};
+  CUDA_TRY(c, cudaMemcpyAsync(h, small, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  *ntr0 = orient ? h[0] : npairs;
+  *total = h[1];
+  return NW_OK;
+}
+
 struct HostLaps {  // NW_HOST_PROFILE=1: host-side phase times of one call, to stderr
   bool on = getenv("NW_HOST_PROFILE") != nullptr;
   std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
@@ -1225,7 +1349,21 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   for (int x = 0; x < sc->K; ++x)
     for (int y = 0; y < x; ++y) sym = sym && score_of(sc, x, y) == score_of(sc, y, x);
   long long ntr0 = npairs;  // explicit-pair tasks [ntr0, npairs) are filled transposed
-  if (h_pairs) {
+  // the plan on the device for large explicit two-phase batches (C4: ~1.4 ms of host
+  // planning, all GPU idle, becomes a few tiny kernels and one small copy); used when
+  // the kept flag buffer already holds every pair's words (else the host plans waves)
+  bool dev_plan = false;
+  if (h_pairs && two_phase && npairs >= 4096 && c->tbdirs_cap > 0 && !getenv("NW_HOST_PLAN")) {
+    long long total = 0, nt = npairs;
+    st = device_plan(c, d_pairs, d_offs, npairs, RS, maxlen,
+                     sym && !getenv("NW_BATCH_NO_TRANSPOSE"), &nt, &total);
+    if (st) return st;
+    if ((size_t)total * 4 <= c->tbdirs_cap && !getenv("NW_BATCH_TB_BUDGET")) {
+      dev_plan = true;
+      ntr0 = nt;
+    }
+  }
+  if (h_pairs && !dev_plan) {
     // LPT order: counting sort on the cost quantised to NB levels (descending,
     // stable), O(npairs) -- a comparison sort of C4's 100k pairs took ~15 ms of host
     // time per call and left the GPU idle (tools/exp_c4.py). Two-phase traceback with
@@ -1271,12 +1409,15 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
     for (long long k = 0; k < npairs; ++k) aux[cnt[bk[k]]++] = (int)k;
   }
   hl.lap("LPT order + orientation");
-  st = grow(c, c->d_aux, c->aux_cap, sizeof(int) * aux.size() + 16);
-  if (st) return st;
+  if (!dev_plan) {
+    st = grow(c, c->d_aux, c->aux_cap, sizeof(int) * aux.size() + 16);
+    if (st) return st;
+  }
   std::vector<long long>& tdoff = c->h_tdoff;
   std::vector<long long> wave_end;
   tdoff.clear();
-  if (two_phase) {
+  if (dev_plan) wave_end.push_back(npairs);  // one wave: the kept buffer holds every pair's words
+  if (two_phase && !dev_plan) {
     const long long wpg = RS / 2;  // words per (strip, 8-step group): H packed rows x 32 lanes
     auto len = [&](int s) { return h_offs[s + 1] - h_offs[s]; };
     auto words_mn = [&](long long m, long long n) {
@@ -1328,7 +1469,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
     st = grow(c, c->d_tdoff, c->tdoff_cap, sizeof(long long) * (size_t)std::max(1LL, npairs));
     if (st) return st;
   }
-  {
+  if (!dev_plan) {
     const StagedCopy cp[2] = {{c->d_aux, aux.data(), sizeof(int) * aux.size()},
                               {c->d_tdoff, tdoff.data(), sizeof(long long) * tdoff.size()}};
     hl.lap("words, waves, grow");

@@ -472,3 +472,28 @@ def test_batch_caller_owned_outputs(ctx):
     assert s is s_out and s.tolist() == nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc).tolist()
     with pytest.raises(ValueError):
         nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc, out=s_out[:10])
+
+
+@pytest.mark.parametrize("host_plan", [False, True])
+def test_batch_traceback_device_plan(ctx, monkeypatch, host_plan):
+    """Large explicit traceback batches (>= 4,096 pairs) are planned on the device
+    (LPT buckets, orientation, word offsets) once the kept flag buffer is sized;
+    NW_HOST_PLAN forces the host planner. Results are identical either way and equal
+    the oracle's (scores of all pairs, paths of a sample)."""
+    if host_plan:
+        monkeypatch.setenv("NW_HOST_PLAN", "1")
+    ss = nwgen.random_set(91, 400, 0, 260, nwgen.PROTEIN)
+    rng = np.random.Generator(np.random.PCG64(91))
+    pairs = rng.integers(0, ss.nseq, size=(5000, 2)).astype(np.int32)
+    for tie in [(1, 2, 3), (3, 2, 1)]:
+        sc = nwgen.Scoring(match=0, mismatch=0, gap=-5, alphabet=nwgen.PROTEIN,
+                           subst=nwgen.BLOSUM62, tie=tie)
+        for _ in range(2):  # the first call sizes the buffer (host plan), the second may use the device
+            scores, *flat = nwb.nw_align_batch(ctx, ss.residues, ss.offs, pairs, sc, nwb.NW_TRACEBACK)
+        want = oracle.batch_score(ss.residues, ss.offs, pairs, sc)
+        assert scores.tolist() == want.tolist()
+        paths = nwb.batch_paths(*flat)
+        for k in rng.choice(len(pairs), 300, replace=False):
+            p, q = pairs[k]
+            ws, wops = oracle.align(ss.seq(p), ss.seq(q), sc)
+            assert paths[k].tolist() == wops.tolist(), (k, tie)
