@@ -513,6 +513,14 @@ def run_ours(args):
     tp = os.path.join(ROOT, "profiles", f"traffic_{wl}.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    walk = None  # C4's traceback walk: HBM bytes (ncu, per launch) over its live event time
+    wp = os.path.join(ROOT, "profiles", f"traffic_{wl}_walk.json")
+    if os.path.exists(wp) and tb_n:
+        wb = json.load(open(wp)).get("dram_bytes_per_launch")
+        w_ms = tb_ms / tb_n
+        walk = {"kernel": "k_batch_walk", "bound": "hbm latency (dependent loads)", "ms_per_launch": w_ms,
+                "dram_bytes_per_launch": wb, "achieved_GBps": wb / (w_ms / 1e3) / 1e9,
+                "peak_GBps": load_peaks().get("hbm_gbs"), "bytes_source": os.path.relpath(wp, ROOT)}
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (int32 lane-ops)",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "kernel": ("k_percell_fill" if wl in ("c1p", "c2p") else
@@ -522,7 +530,8 @@ def run_ours(args):
                 "kernel_launches_per_step": fill_launches_per_step,
                 "kernel_share_of_step": (fill_ms / total_ms) if total_ms else None,
                 "traceback_ms_per_step": tb_ms / max(args.steps, 1),
-                "peak_source": "tools/peaks_int.cu issue limit 128 lane-ops/clk/SM x 148 SMs x 1965 MHz"}
+                "peak_source": "tools/peaks_int.cu issue limit 128 lane-ops/clk/SM x 148 SMs x 1965 MHz",
+                **({"traceback_walk": walk} if walk else {})}
     out = {
         "metric": "GCUPS (cell updates/s)", "value": value, "unit": "GCUPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
