@@ -356,13 +356,14 @@ int choose_kr_shape(long long m, long long n, bool dirs);
 // KR 5 and 6 exist only with register profiles (K <= 4)
 int choose_kr(long long m, long long n, bool dirs, int K) {
   const int k = choose_kr_shape(m, n, dirs);
-  return (K > 4 && (k == 5 || k == 6)) ? 4 : k;
+  return (K > 4 && (k == 5 || k == 6)) ? 4 : (K > 4 && k > 8) ? 8 : k;
 }
 int choose_kr_shape(long long m, long long n, bool dirs) {
   const char* env = getenv("NW_KR");
   if (env) {
     const int k = atoi(env);
     if (k == 2 || k == 4 || k == 8 || k == 5 || k == 6) return k;  // 5, 6: register profiles only
+    if (k == 10 || k == 12) return dirs ? k : 8;  // direction fills only
   }
   (void)dirs;
   // Tall pairs (>= ~150 strips at KR = 8): the largest KR, the lag is amortised
@@ -371,7 +372,15 @@ int choose_kr_shape(long long m, long long n, bool dirs) {
   // the measured step cost c and strip-to-strip lag L (tools/exp_lag.py: c = 75,
   // 97.5, 150 and L = 9450, 9650, 12450 cycles at KR = 2, 4, 8): C2 -> 4,
   // C1 (1k x 1k) -> 4, 2k x 80k -> 2.
-  if (m >= 32LL * 8 * 150) return 8;
+  if (m >= 32LL * 8 * 150) {
+    // tall: the largest KR amortises the lag; with directions and register profiles,
+    // 10 or 12 rows per lane once 8 would put more than two strips per SM
+    // sub-partition (the lock-step pace of DESIGN.md §3.8; NW_TALL_KR8=1: always 8)
+    if (dirs && !getenv("NW_TALL_KR8"))
+      for (int k : {8, 10, 12})
+        if ((m + 32LL * k - 1) / (32LL * k) <= 8LL * 148) return k;  // 148 SMs (B200)
+    return 8;
+  }
   const int ks[3] = {2, 4, 8};
   const double c[3] = {75.0, 97.5, 150.0}, L[3] = {9450.0, 9650.0, 12450.0};
   int best = 2;
@@ -861,7 +870,7 @@ static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops, bool
     const int gw_bytes = (kr * 16 + 1) * 4;
     if (S >= 2) {
       auto kspec = kr == 2 ? k_tb_spec<2> : kr == 4 ? k_tb_spec<4> : kr == 5 ? k_tb_spec<5>
-                 : kr == 6 ? k_tb_spec<6> : k_tb_spec<8>;
+                 : kr == 6 ? k_tb_spec<6> : kr == 10 ? k_tb_spec<10> : kr == 12 ? k_tb_spec<12> : k_tb_spec<8>;
       const size_t win = (size_t)((32 * B.step + left_cols + 40) / 8 + 2) * gw_bytes;
       cudaFuncSetAttribute(kspec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win);
       kspec<<<(S - 1) * (B.nb / 32), 32, win, c->stream>>>(tb->dirs, tb->wpl, B, tb->tie[0],
@@ -870,7 +879,7 @@ static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops, bool
     }
     {
       auto kchain = kr == 2 ? k_tb_chain<2> : kr == 4 ? k_tb_chain<4> : kr == 5 ? k_tb_chain<5>
-                  : kr == 6 ? k_tb_chain<6> : k_tb_chain<8>;
+                  : kr == 6 ? k_tb_chain<6> : kr == 10 ? k_tb_chain<10> : kr == 12 ? k_tb_chain<12> : k_tb_chain<8>;
       // exact walks: windows of ~96 KB of decision bits left of the entry
       // a window of 2R + 256 columns left of the entry (re-staged further left
       // when a long gap leaves it): staging, not the walk, dominated at 96 KB
@@ -886,7 +895,8 @@ static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops, bool
     }
     const int smem_bytes = 96 * 1024;
     auto kseg = kr == 2 ? k_tb_segments<2> : kr == 4 ? k_tb_segments<4> : kr == 5 ? k_tb_segments<5>
-              : kr == 6 ? k_tb_segments<6> : k_tb_segments<8>;
+              : kr == 6 ? k_tb_segments<6> : kr == 10 ? k_tb_segments<10> : kr == 12 ? k_tb_segments<12>
+              : k_tb_segments<8>;
     cudaFuncSetAttribute(kseg, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     kseg<<<S, 32, smem_bytes, c->stream>>>(tb->dirs, tb->wpl, tb->m, tb->n, tb->tie[0],
                                            tb->tie[1], tb->tie[2], tb->cs, tb->seg, tb->segstride,

@@ -46,6 +46,10 @@ void launch_batch_t(const BatchArgs& B, int grid, size_t smem, cudaStream_t st) 
       launch_fill_t<5, true, true, PI>(A, grid, smem, st);                                    \
     } else if (kr == 6 && profreg) {                                                          \
       launch_fill_t<6, true, true, PI>(A, grid, smem, st);                                    \
+    } else if (kr == 10 && profreg) {                                                         \
+      launch_fill_t<10, true, true, PI>(A, grid, smem, st);                                   \
+    } else if (kr == 12 && profreg) {                                                         \
+      launch_fill_t<12, true, true, PI>(A, grid, smem, st);                                   \
     } else {                                                                                  \
       if (profreg) launch_fill_t<8, true, true, PI>(A, grid, smem, st);                       \
       else launch_fill_t<8, true, false, PI>(A, grid, smem, st);                              \

@@ -433,10 +433,11 @@ def test_batch_score_only_orientation(ctx, monkeypatch, sym):
     assert nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc).tolist() == want.tolist()
 
 
-@pytest.mark.parametrize("kr", [2, 4, 5, 6, 8])
+@pytest.mark.parametrize("kr", [2, 4, 5, 6, 8, 10, 12])
 def test_pair_every_rows_per_lane(ctx, monkeypatch, kr):
-    """The single-pair fill + strip traceback at every rows-per-lane setting (5 and 6:
-    strips of 160 / 192 rows, not powers of two), all tie orders on a tie-rich pair."""
+    """The single-pair fill + strip traceback at every rows-per-lane setting (5, 6, 10,
+    12: strips of 160 / 192 / 320 / 384 rows, not powers of two), all tie orders on a
+    tie-rich pair."""
     monkeypatch.setenv("NW_KR", str(kr))
     for k, (m, n) in enumerate([(32 * kr * 3 + 17, 1500), (2000, 700), (700, 2100), (5, 9)]):
         a, b = _pair(9300 + 11 * kr + k, m, n)
