@@ -246,8 +246,42 @@ nw_status nw_align_pair_percell_dev(nw_ctx *ctx, const uint8_t *d_a, int64_t m, 
                                     uint8_t *d_ops, int64_t *d_len);
 
 /* Wait for the context's stream and report any deferred device-side error
- * (alphabet violations, watchdog) raised by earlier _dev calls. */
+ * (alphabet violations, watchdog) raised by earlier _dev calls. The error flags
+ * are sticky: an error raised by any _dev call since the last synchronising call
+ * on ctx (this one, or any host-pointer entry point) is reported then, even if
+ * later calls succeeded; the first bad position among them is kept. Reporting
+ * clears the flags. */
 nw_status nw_ctx_sync(nw_ctx *ctx);
+
+/* ---- tuning and test options (explicit context state; nothing reads the environment) ----
+ * Every option defaults to 0 = the measured default. They select
+ * among kernels that all compute the same results (the parity tests run each
+ * setting against the oracle), or shape test-only behaviour. Values < 0 or an
+ * unknown option -> NW_E_INVAL. */
+enum {
+  NW_OPT_ROWS_PER_LANE = 0,    /* single-pair int32 fill: rows per lane 2,4,5,6,8 (10,12 with directions) */
+  NW_OPT_D16_FORCE = 1,        /* score-only pair: packed difference form at this many rows per lane */
+  NW_OPT_D16_KR = 2,           /* rows per lane of the tall-pair difference form (even, 12..32) */
+  NW_OPT_NO_D16 = 3,           /* 1: never use the packed difference forms */
+  NW_OPT_TALL_KR8 = 4,         /* 1: tall direction fills always at 8 rows per lane */
+  NW_OPT_POLL_NS = 5,          /* back-off (ns) between re-polls of a late boundary entry */
+  NW_OPT_TB_STEP = 6,          /* sampled-exit spacing in columns (power of two) */
+  NW_OPT_TB_BAND = 7,          /* sampled exits per strip (multiple of 32) */
+  NW_OPT_BATCH_KR16 = 8,       /* packed batch traceback strips: 8 or 16 rows per lane */
+  NW_OPT_BATCH_NO_TRANSPOSE = 9,  /* 1: batch pairs always filled in their own orientation */
+  NW_OPT_BATCH_TB_BUDGET = 10, /* bytes of kept decision words per batch wave (forces waves) */
+  NW_OPT_HOST_PLAN = 11,       /* 1: plan large traceback batches on the host, not the device */
+  NW_OPT_LINEAR_INT32 = 12,    /* 1: checkpoint pass of nw_align_pair_linear in int32 strips */
+  NW_OPT_CBLOCK_WARPS_PER_SM = 13, /* warps per SM of the column-block launch (default 8) */
+  NW_OPT_HOST_PROFILE = 14,    /* 1: print host-side phase times of batch calls to stderr */
+  NW_OPT_WATCHDOG_POLLS = 15,  /* re-polls of a late boundary entry before NW_E_DEADLOCK (0: 2^28) */
+  NW_OPT_TEST_WITHHOLD = 16,   /* test only: 1 + the strip whose bottom row is never published
+                                  (single-pair fills), so its consumer's watchdog must fire */
+  NW_OPT_COUNT_ = 17
+};
+nw_status nw_ctx_set_option(nw_ctx *ctx, int32_t option, int64_t value);
+/* Current value, or -1 for a NULL ctx / unknown option. */
+int64_t nw_ctx_get_option(const nw_ctx *ctx, int32_t option);
 
 /* Number of library kernels launched on this context so far (bench accounting). */
 int64_t nw_ctx_launches(const nw_ctx *ctx);

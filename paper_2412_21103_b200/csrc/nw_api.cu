@@ -42,7 +42,8 @@ struct nw_ctx {
   // workspace (grow-only)
   uint8_t* d_lut = nullptr;     // 256
   int8_t* d_prof = nullptr;     // 64*64
-  long long* d_bad = nullptr;   // 1 (+ spare)
+  long long* d_bad = nullptr;   // [0] first bad residue position, [1] watchdog flag (int): sticky
+  int* d_err = nullptr;         //   = (int*)(d_bad + 1); both cleared only by check_deferred
   int* d_ints = nullptr;        // small ints: [0] ticket [1] err [2] hm [5] slow traceback strips
   size_t ints_cap = 0;
   uint8_t* d_codes = nullptr;   // encoded inputs
@@ -75,6 +76,12 @@ struct nw_ctx {
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_open[2];
   std::vector<cudaEvent_t> ev_pool;
+  // tuning / test options (nw_ctx_set_option; 0 = the measured default)
+  long long opt[NW_OPT_COUNT_] = {0};
+  // live handles: nw_ctx_destroy releases their device memory and detaches them, so
+  // a handle freed after its context only deletes its host struct
+  std::vector<nw_tb*> live_tb;
+  std::vector<nw_msa*> live_msa;
   // last scoring uploaded (avoid re-uploading identical tables)
   bool have_tables = false;
   uint8_t lut_h[256];
@@ -82,14 +89,14 @@ struct nw_ctx {
 };
 
 struct nw_msa {
-  nw_ctx* ctx;
+  nw_ctx* ctx;               // null once the context was destroyed
   int nseq = 0, center = 0;
   long long W = 0;           // MSA columns
   uint8_t* d_rows = nullptr; // [nseq][W] gapped rows ('-' = gap), input order
 };
 
 struct nw_tb {
-  nw_ctx* ctx;
+  nw_ctx* ctx;        // null once the context was destroyed
   void* mem;          // one device allocation holding everything below
   uint16_t* dirs;     // [S][wpl][KR][32] decision-bit halfwords (nw_fill.cuh)
   long long wpl;      // 8-step groups per strip
@@ -100,6 +107,7 @@ struct nw_tb {
   long long segstride;
   int m, n, S;
   int kr;             // rows per lane of the fill that wrote `dirs`
+  int lstep, nb;      // sampled-exit spacing (log2) and samples per strip (k_tb_spec)
   uint8_t tie[3];
 };
 
@@ -273,18 +281,18 @@ int pi_code(const uint8_t tie[3]) { return tie[0] * 100 + tie[1] * 10 + tie[2]; 
 
 long long pad16(long long x) { return (x + 15) & ~15ll; }
 
-int env_int(const char* name, int dflt, int lo) {
-  const char* e = getenv(name);
-  const int k = e ? atoi(e) : 0;
-  return k >= lo ? k : dflt;
+// Sampled strip exits: spacing of the samples in columns (log2;
+// NW_OPT_TB_STEP rounds down to a power of two) and samples per strip (a multiple of 32).
+int tb_lstep(const nw_ctx* c) {
+  const long long k = c->opt[NW_OPT_TB_STEP] >= 1 ? c->opt[NW_OPT_TB_STEP] : 4;
+  int l = 0;
+  while ((2LL << l) <= k) ++l;
+  return l;
 }
-// Sampled strip exits: spacing of the samples in columns and
-// samples per strip (a multiple of 32), overridable for experiments.
-int tb_lstep() {  // log2 of the spacing (NW_TB_STEP rounds down to a power of two)
-  static int v = [] { int k = env_int("NW_TB_STEP", 4, 1), l = 0; while ((2 << l) <= k) ++l; return l; }();
-  return v;
+int tb_band(const nw_ctx* c) {
+  const long long k = c->opt[NW_OPT_TB_BAND] >= 32 ? std::min(c->opt[NW_OPT_TB_BAND], 4096LL) : 256;
+  return (int)((k + 31) / 32 * 32);
 }
-int tb_band() { static int v = (env_int("NW_TB_BAND", 256, 32) + 31) / 32 * 32; return v; }
 
 // Entries per boundary-ring slot (columns 0..n plus the sweep's overhang), 16-byte multiple.
 long long bnd_stride(long long n) { return (n + 1 + 64 + 1) & ~1ll; }
@@ -341,8 +349,8 @@ bool dispatch_fill(bool dirs, int pi, int kr, bool profreg, const FillArgs& A, i
 
 // Packed difference form (nw_fill_d16.cuh) applies to score-only DNA-size
 // alphabets with s - 2g >= 0 for every symbol pair.
-bool d16_ok(const nw_scoring* sc) {
-  if (sc->K > 4 || getenv("NW_NO_D16")) return false;
+bool d16_ok(const nw_ctx* c, const nw_scoring* sc) {
+  if (sc->K > 4 || c->opt[NW_OPT_NO_D16]) return false;
   for (int x = 0; x < sc->K; ++x)
     for (int y = 0; y < sc->K; ++y)
       if (score_of(sc, x, y) - 2 * sc->gap < 0) return false;
@@ -351,17 +359,16 @@ bool d16_ok(const nw_scoring* sc) {
 
 // Rows per lane for a single pair: the strip count m/(32 KR)
 // is the number of warps that can work at once; small KR buys parallelism at the
-// cost of a longer lane skew (m/KR steps). NW_KR overrides (2, 4 or 8).
-int choose_kr_shape(long long m, long long n, bool dirs);
+// cost of a longer lane skew (m/KR steps). NW_OPT_ROWS_PER_LANE overrides.
+int choose_kr_shape(const nw_ctx* c, long long m, long long n, bool dirs);
 // KR 5 and 6 exist only with register profiles (K <= 4)
-int choose_kr(long long m, long long n, bool dirs, int K) {
-  const int k = choose_kr_shape(m, n, dirs);
+int choose_kr(const nw_ctx* c, long long m, long long n, bool dirs, int K) {
+  const int k = choose_kr_shape(c, m, n, dirs);
   return (K > 4 && (k == 5 || k == 6)) ? 4 : (K > 4 && k > 8) ? 8 : k;
 }
-int choose_kr_shape(long long m, long long n, bool dirs) {
-  const char* env = getenv("NW_KR");
-  if (env) {
-    const int k = atoi(env);
+int choose_kr_shape(const nw_ctx* c, long long m, long long n, bool dirs) {
+  if (c->opt[NW_OPT_ROWS_PER_LANE]) {
+    const int k = (int)c->opt[NW_OPT_ROWS_PER_LANE];
     if (k == 2 || k == 4 || k == 8 || k == 5 || k == 6) return k;  // 5, 6: register profiles only
     if (k == 10 || k == 12) return dirs ? k : 8;  // direction fills only
   }
@@ -375,19 +382,19 @@ int choose_kr_shape(long long m, long long n, bool dirs) {
   if (m >= 32LL * 8 * 150) {
     // tall: the largest KR amortises the lag; with directions and register profiles,
     // 10 or 12 rows per lane once 8 would put more than two strips per SM
-    // sub-partition (the lock-step pace of DESIGN.md §3.8; NW_TALL_KR8=1: always 8)
-    if (dirs && !getenv("NW_TALL_KR8"))
+    // sub-partition (the lock-step pace of DESIGN.md §3.8; NW_OPT_TALL_KR8: always 8)
+    if (dirs && !c->opt[NW_OPT_TALL_KR8])
       for (int k : {8, 10, 12})
-        if ((m + 32LL * k - 1) / (32LL * k) <= 8LL * 148) return k;  // 148 SMs (B200)
+        if ((m + 32LL * k - 1) / (32LL * k) <= 8LL * c->sm_count) return k;
     return 8;
   }
   const int ks[3] = {2, 4, 8};
-  const double c[3] = {75.0, 97.5, 150.0}, L[3] = {9450.0, 9650.0, 12450.0};
+  const double cs[3] = {75.0, 97.5, 150.0}, L[3] = {9450.0, 9650.0, 12450.0};
   int best = 2;
   double tbest = 1e300;
   for (int i = 0; i < 3; ++i) {
     const double S = (double)((m + 32 * ks[i] - 1) / (32 * ks[i]));
-    const double t = c[i] * (double)(n + 31) + L[i] * (S - 1.0);
+    const double t = cs[i] * (double)(n + 31) + L[i] * (S - 1.0);
     if (t < tbest) { tbest = t; best = ks[i]; }
   }
   return best;
@@ -397,13 +404,13 @@ int choose_kr_shape(long long m, long long n, bool dirs) {
 // strips advance in lock-step, so the pair runs at the pace of the most loaded SM
 // sub-partition: the smallest even KR >= 16 that keeps the strip count within two
 // warps per sub-partition (1M^2: KR 28 = 1,117 strips, 6.5 TCUPS, vs KR 32 = 977
-// strips 6.2 and KR 26 = 1,202 strips 5.5; tools/exp_c5kr.py). NW_D16_KR overrides.
-int d16_kr(long long m, int sm_count) {
+// strips 6.2 and KR 26 = 1,202 strips 5.5; tools/exp_c5kr.py). NW_OPT_D16_KR overrides.
+int d16_kr(const nw_ctx* c, long long m) {
   int kd = 32;
   for (int k = 16; k <= 32; k += 2)
-    if ((m + 32LL * k - 1) / (32LL * k) <= 8LL * sm_count) { kd = k; break; }
-  const int k = env_int("NW_D16_KR", kd, 12);
-  return (k >= 12 && k <= 32 && k % 2 == 0) ? k : kd;
+    if ((m + 32LL * k - 1) / (32LL * k) <= 8LL * c->sm_count) { kd = k; break; }
+  const long long k = c->opt[NW_OPT_D16_KR];
+  return (k >= 12 && k <= 32 && k % 2 == 0) ? (int)k : kd;
 }
 
 bool dispatch_batch(bool dirs, int pi, bool profreg, bool u16, bool d16, int packed_kr,
@@ -442,7 +449,7 @@ nw_status init_small(nw_ctx* c, int nints, ZeroRanges zr = ZeroRanges{{nullptr, 
   long long work = nints;
   for (int r = 0; r < 4; ++r) work = std::max(work, zr.bytes[r] / 16);
   const int blocks = (int)std::min<long long>((long long)c->sm_count * 4, (work + 255) / 256 + 1);
-  k_init<<<blocks, 256, 0, c->stream>>>(c->d_ints, nints, c->d_bad, zr);
+  k_init<<<blocks, 256, 0, c->stream>>>(c->d_ints, nints, nullptr, zr);  // error flags are sticky
   LAUNCHED(c);
   return NW_OK;
 }
@@ -527,7 +534,7 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
   const bool dirs = tb != nullptr;
   nw_status st = NW_OK;
   int* ticket = c->d_ints;
-  int* errf = c->d_ints + 1;
+  int* errf = c->d_err;
   int* hm = c->d_ints + 2;
   const long long gmn = (long long)sc->gap * (m + n);
   if (m > 0 && n > 0) {
@@ -538,12 +545,18 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     A.dirs = dirs ? tb->dirs : nullptr;
     A.wpl = dirs ? tb->wpl : 0;
     A.hm = hm; A.err = errf;
-    A.poll_ns = (unsigned)env_int("NW_POLL_NS", 0, 1);
+    A.poll_ns = (unsigned)std::max(0LL, std::min(c->opt[NW_OPT_POLL_NS], 100000LL));
     A.ckpt = ckpt; A.ck_every = ck_every; A.ck_stride = ck_stride;
     A.top_row = top_row; A.top_tag = top_tag;
+    if (c->opt[NW_OPT_WATCHDOG_POLLS] > 0) A.watchdog = c->opt[NW_OPT_WATCHDOG_POLLS];
+    const long long wh = c->opt[NW_OPT_TEST_WITHHOLD];
+    if (wh > 0 && wh <= nstrips && c->bnd_cap >= sizeof(unsigned long long) * 3 * (size_t)bnd_stride(n)) {
+      A.withhold = (int)wh;  // test hook: that strip's bottom row goes to the ring's third slot
+      A.sink = c->d_bnd + 2 * bnd_stride(n);
+    }
     const bool profreg = sc->K <= 4;
     const size_t smem = profreg ? 0 : (size_t)sc->K * R;
-    const bool d16 = !dirs && (kr >= 12 || (!ckpt && getenv("NW_D16_FORCE") && d16_ok(sc)));
+    const bool d16 = !dirs && (kr >= 12 || (!ckpt && c->opt[NW_OPT_D16_FORCE] && d16_ok(c, sc)));
     // persistent grid: one warp per CTA, at most the resident capacity
     int per_sm = 16;
     int grid = std::min<long long>(nstrips, (long long)c->sm_count * per_sm);
@@ -563,12 +576,20 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
   return NW_OK;
 }
 
+// Reads (and clears) the sticky device error flags: the first bad residue
+// position (atomicMin over every call since the last check) and the watchdog
+// flag. A _dev call's error therefore surfaces at the next synchronising call on
+// the context, even when other calls were enqueued in between.
 nw_status check_deferred(nw_ctx* c) {
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  long long bad = 0;
-  int errf = 0;
-  CUDA_TRY(c, cudaMemcpy(&bad, c->d_bad, sizeof bad, cudaMemcpyDeviceToHost));
-  if (c->d_ints) CUDA_TRY(c, cudaMemcpy(&errf, c->d_ints + 1, sizeof errf, cudaMemcpyDeviceToHost));
+  long long flags[2] = {0, 0};
+  CUDA_TRY(c, cudaMemcpy(flags, c->d_bad, sizeof flags, cudaMemcpyDeviceToHost));
+  const long long bad = flags[0];
+  const int errf = (int)(flags[1] & 0xffffffff);
+  if (bad != 0x7fffffffffffffffll || errf) {
+    const long long clear[2] = {0x7fffffffffffffffll, 0};
+    CUDA_TRY(c, cudaMemcpy(c->d_bad, clear, sizeof clear, cudaMemcpyHostToDevice));
+  }
   if (bad != 0x7fffffffffffffffll) {
     c->bad_pos = bad;
     return fail(c, NW_E_ALPHABET, "residue at position %lld is not in the alphabet", bad);
@@ -607,6 +628,7 @@ nw_status new_tb(nw_ctx* c, long long m, long long n, const nw_scoring* sc, int 
   if (!tb) return fail(c, NW_E_NOMEM, "host allocation");
   memset(tb, 0, sizeof *tb);
   tb->ctx = c;
+  c->live_tb.push_back(tb);
   tb->m = (int)m;
   tb->n = (int)n;
   tb->kr = kr;
@@ -617,13 +639,16 @@ nw_status new_tb(nw_ctx* c, long long m, long long n, const nw_scoring* sc, int 
   tb->segstride = pad16(R + n + 1);
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t b_dirs = al((size_t)S * tb->wpl * kr * 32 * sizeof(uint16_t));
-  const size_t b_spec = al((size_t)S * tb_band() * sizeof(int));
+  tb->lstep = tb_lstep(c);
+  tb->nb = tb_band(c);
+  const size_t b_spec = al((size_t)S * tb->nb * sizeof(int));
   const size_t b_cs = al((size_t)S * sizeof(int)), b_len = b_cs;
   const size_t b_seg = al((size_t)S * tb->segstride);
   const size_t bytes = b_dirs + b_spec + b_cs + b_len + b_seg;
   if (m > 0 && n > 0) {
     cudaError_t e = cudaMallocAsync(&tb->mem, bytes, c->stream);
     if (e != cudaSuccess) {
+      c->live_tb.pop_back();
       delete tb;
       return fail(c, NW_E_NOMEM, "traceback buffers of %zu bytes: %s", bytes, cudaGetErrorString(e));
     }
@@ -653,21 +678,23 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
   // workspace: padded code buffers and the tagged 2-slot boundary ring
   constexpr long long R = R_MAX;
   const long long la = pad16(PAD + m + R + PAD), lb = pad16(PAD + n + R + PAD);
-  int kr = choose_kr(m, n, want_dirs, sc->K);
+  int kr = choose_kr(c, m, n, want_dirs, sc->K);
   // packed difference form (two rows per register) for tall score-only pairs: it
   // halves the ALU work per cell but doubles the lane skew, so it only pays when
   // there are enough 512-row strips to fill the GPU (measured: 1M^2 2.4 -> 5.9
   // TCUPS; 20k^2 1.44 -> 2.14 ms, slower)
   // and 28-32 rows per lane by the strip-count rule of d16_kr.
-  if (!want_dirs && d16_ok(sc) && m >= 32LL * 16 * 150) kr = d16_kr(m, c->sm_count);
-  // experiments: NW_D16_FORCE=<4|8|16|32> runs any score-only pair in the packed form
-  if (!want_dirs && d16_ok(sc) && getenv("NW_D16_FORCE")) {
-    const int f = env_int("NW_D16_FORCE", 16, 4);
+  if (!want_dirs && d16_ok(c, sc) && m >= 32LL * 16 * 150) kr = d16_kr(c, m);
+  // NW_OPT_D16_FORCE = <4|8|12..32 even> runs any score-only pair in the packed form
+  if (!want_dirs && d16_ok(c, sc) && c->opt[NW_OPT_D16_FORCE]) {
+    const int f = (int)std::max(4LL, std::min(c->opt[NW_OPT_D16_FORCE], 32LL));
     kr = (f >= 12 && f <= 32 && f % 2 == 0) ? f : (f >= 32 ? 32 : (f >= 16 ? 16 : (f >= 8 ? 8 : 4)));
   }
   st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
   if (st) return st;
-  const long long bbytes = (long long)sizeof(unsigned long long) * 2 * bnd_stride(n);
+  // two ring slots (+ a sink slot for the NW_OPT_TEST_WITHHOLD hook)
+  const long long bbytes = (long long)sizeof(unsigned long long) * (c->opt[NW_OPT_TEST_WITHHOLD] ? 3 : 2) *
+                           bnd_stride(n);
   st = grow(c, c->d_bnd, c->bnd_cap, (size_t)bbytes);
   if (st) return st;
   // one launch zeroes ticket/err/hm, the bad-position flag, the code
@@ -747,8 +774,9 @@ nw_status nw_ctx_create(int device, void* cuda_stream, nw_ctx** out) {
     nw_ctx_destroy(c);
     return NW_E_NOMEM;
   }
-  long long init_bad = 0x7fffffffffffffffll;
-  cudaMemcpy(c->d_bad, &init_bad, sizeof init_bad, cudaMemcpyHostToDevice);
+  const long long init_flags[4] = {0x7fffffffffffffffll, 0, 0, 0};
+  cudaMemcpy(c->d_bad, init_flags, sizeof init_flags, cudaMemcpyHostToDevice);
+  c->d_err = reinterpret_cast<int*>(c->d_bad + 1);
   // keep freed stream-ordered allocations in the pool (steady-state calls allocate nothing new)
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -763,6 +791,16 @@ void nw_ctx_destroy(nw_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  for (nw_tb* tb : c->live_tb) {  // detach: a later nw_tb_free only deletes the host struct
+    if (tb->mem) cudaFreeAsync(tb->mem, c->stream);
+    tb->mem = nullptr;
+    tb->ctx = nullptr;
+  }
+  for (nw_msa* h : c->live_msa) {
+    if (h->d_rows) cudaFreeAsync(h->d_rows, c->stream);
+    h->d_rows = nullptr;
+    h->ctx = nullptr;
+  }
   cudaFree(c->d_lut);
   cudaFree(c->d_prof);
   cudaFree(c->d_bad);
@@ -815,6 +853,18 @@ nw_status nw_ctx_kernel_time(nw_ctx* c, int cls, double* total_ms, int64_t* laun
   return NW_OK;
 }
 
+nw_status nw_ctx_set_option(nw_ctx* c, int32_t option, int64_t value) {
+  if (!c) return NW_E_INVAL;
+  if (option < 0 || option >= NW_OPT_COUNT_) return fail(c, NW_E_INVAL, "unknown option %d", option);
+  if (value < 0) return fail(c, NW_E_INVAL, "option %d: negative value", option);
+  c->opt[option] = value;
+  return NW_OK;
+}
+
+int64_t nw_ctx_get_option(const nw_ctx* c, int32_t option) {
+  return (c && option >= 0 && option < NW_OPT_COUNT_) ? c->opt[option] : -1;
+}
+
 nw_status nw_ctx_sync(nw_ctx* c) {
   if (!c) return NW_E_INVAL;
   CUDA_TRY(c, cudaSetDevice(c->device));
@@ -844,7 +894,11 @@ nw_status nw_align_pair_dev(nw_ctx* c, const uint8_t* d_a, int64_t m, const uint
 
 void nw_tb_free(nw_tb* tb) {
   if (!tb) return;
-  if (tb->mem) cudaFreeAsync(tb->mem, tb->ctx->stream);
+  if (nw_ctx* c = tb->ctx) {
+    if (tb->mem) cudaFreeAsync(tb->mem, c->stream);
+    auto& v = c->live_tb;
+    v.erase(std::remove(v.begin(), v.end(), tb), v.end());
+  }
   delete tb;
 }
 
@@ -863,7 +917,7 @@ static nw_status traceback_core(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops, bool
     // parallel), then the bottom-up chain over the brackets
     const int kr = tb->kr, R = 32 * kr;
     nwk::TbBand B;
-    B.m = tb->m; B.n = tb->n; B.lstep = tb_lstep(); B.step = 1 << B.lstep; B.nb = tb_band();
+    B.m = tb->m; B.n = tb->n; B.lstep = tb->lstep; B.step = 1 << B.lstep; B.nb = tb->nb;
     B.ratio = (float)tb->n / (float)tb->m;
     B.nq = (tb->n + B.step - 1) / B.step + 1;
     const int left_cols = R + 128;  // > one strip's drift on a near-diagonal path
@@ -927,11 +981,6 @@ nw_status nw_traceback(nw_ctx* c, const nw_tb* tb, uint8_t* ops, int64_t cap, in
   long long hl = 0;
   CUDA_TRY(c, cudaMemcpyAsync(&hl, c->d_len, sizeof hl, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  if (getenv("NW_TB_DEBUG")) {
-    int slow = 0;
-    cudaMemcpy(&slow, c->d_ints + 5, sizeof slow, cudaMemcpyDeviceToHost);
-    fprintf(stderr, "nw_traceback: %d strips, %d walked exactly (unresolved brackets)\n", tb->S, slow);
-  }
   *len = hl;
   if (cap < hl) {
     cudaFreeAsync(d_ops, c->stream);
@@ -995,13 +1044,13 @@ nw_status cblock_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* 
     A.rstride = S * (CB_R + 1);
     A.ticket = c->d_ints + 4;
     A.hm = c->d_ints + 2;
-    A.err = c->d_ints + 1;
+    A.err = c->d_err;
     A.rank0 = rank0;
     A.nranks_here = nhere;
     // every rank's warps must be resident together (they wait on each other);
     // NW_CBLOCK_WARPS_PER_SM caps this launch's share of the GPU
     int per_sm = 8;
-    if (const char* e = getenv("NW_CBLOCK_WARPS_PER_SM")) per_sm = std::max(1, atoi(e));
+    if (c->opt[NW_OPT_CBLOCK_WARPS_PER_SM] > 0) per_sm = (int)std::min(c->opt[NW_OPT_CBLOCK_WARPS_PER_SM], 64LL);
     const int grid = (int)std::min<long long>((long long)c->sm_count * per_sm, S * nhere);
     const int grid_r = std::max(nhere, grid - grid % nhere);
     {
@@ -1267,8 +1316,9 @@ nw_status device_plan(nw_ctx* c, const int* d_pairs, const long long* d_offs, lo
   return NW_OK;
 }
 
-struct HostLaps {  // NW_HOST_PROFILE=1: host-side phase times of one call, to stderr
-  bool on = getenv("NW_HOST_PROFILE") != nullptr;
+struct HostLaps {  // NW_OPT_HOST_PROFILE: host-side phase times of one call, to stderr
+  bool on;
+  explicit HostLaps(const nw_ctx* c) : on(c->opt[NW_OPT_HOST_PROFILE] != 0) {}
   std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
   void lap(const char* what) {
     if (!on) return;
@@ -1283,7 +1333,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
                      const int* h_pairs, long long npairs, const nw_scoring* sc, uint32_t flags,
                      int* d_scores, const long long* d_ops_off, uint8_t* d_ops, int* d_ops_len) {
   constexpr int R = 32 * KR_BATCH;
-  HostLaps hl;
+  HostLaps hl(c);
   const bool tbk = (flags & NW_TRACEBACK) != 0;
   const long long total = h_offs[nseq];
   long long maxlen = 0;
@@ -1320,13 +1370,13 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   const bool profreg = sc->K <= 4;
   // packed score-only sweeps: the H' form when every H' fits 16 bits (measured
   // faster on C3), else the difference form (any length); both need s - 2g >= 0
-  const bool packed = !tbk && profreg && d16_ok(sc);
+  const bool packed = !tbk && profreg && d16_ok(c, sc);
   int smax = 0;
   for (int x = 0; x < sc->K; ++x)
     for (int y = 0; y < sc->K; ++y) smax = std::max(smax, score_of(sc, x, y) - 2 * sc->gap);
   const bool u16 = packed && (long long)maxlen * smax <= 65535;
   bool d16 = packed && !u16;
-  if (tbk && !getenv("NW_NO_D16")) {  // traceback: difference form with decision flags
+  if (tbk && !c->opt[NW_OPT_NO_D16]) {  // traceback: difference form with decision flags
     int smin = 1 << 30;
     for (int x = 0; x < sc->K; ++x)
       for (int y = 0; y < sc->K; ++y) smin = std::min(smin, score_of(sc, x, y) - 2 * sc->gap);
@@ -1345,7 +1395,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
     }
     std::nth_element(rl.begin(), rl.begin() + rl.size() / 2, rl.end());
     if (!rl.empty() && rl[rl.size() / 2] <= 768) packed_kr = 8;
-    if (const char* e = getenv("NW_BATCH_KR16")) packed_kr = atoi(e) == 8 ? 8 : 16;
+    if (c->opt[NW_OPT_BATCH_KR16]) packed_kr = c->opt[NW_OPT_BATCH_KR16] == 8 ? 8 : 16;
   }
   const long long RS = packed_sweep ? 32 * (tbk && d16 ? packed_kr : 16) : R;
   // Two-phase traceback (explicit pairs, packed flags): the fill keeps
@@ -1363,12 +1413,12 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   // planning, all GPU idle, becomes a few tiny kernels and one small copy); used when
   // the kept flag buffer already holds every pair's words (else the host plans waves)
   bool dev_plan = false;
-  if (h_pairs && two_phase && npairs >= 4096 && c->tbdirs_cap > 0 && !getenv("NW_HOST_PLAN")) {
+  if (h_pairs && two_phase && npairs >= 4096 && c->tbdirs_cap > 0 && !c->opt[NW_OPT_HOST_PLAN]) {
     long long total = 0, nt = npairs;
     st = device_plan(c, d_pairs, d_offs, npairs, RS, maxlen,
-                     sym && !getenv("NW_BATCH_NO_TRANSPOSE"), &nt, &total);
+                     sym && !c->opt[NW_OPT_BATCH_NO_TRANSPOSE], &nt, &total);
     if (st) return st;
-    if ((size_t)total * 4 <= c->tbdirs_cap && !getenv("NW_BATCH_TB_BUDGET")) {
+    if ((size_t)total * 4 <= c->tbdirs_cap && !c->opt[NW_OPT_BATCH_TB_BUDGET]) {
       dev_plan = true;
       ntr0 = nt;
     }
@@ -1383,7 +1433,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
     // whose path is the pair's own with U and L exchanged (the oracle's mirror pin).
     // C4: 1.38x -> 1.29x the useful cells. Transposed tasks come after the others
     // (NB more buckets), each part in LPT order; each part is its own fill launch.
-    const bool orient = two_phase && sym && !getenv("NW_BATCH_NO_TRANSPOSE");
+    const bool orient = two_phase && sym && !c->opt[NW_OPT_BATCH_NO_TRANSPOSE];
     // one pass: bucket (cost quantised against maxlen^2, so no max pass), orientation
     // and the pair's flag words; a second pass scatters them into LPT order
     constexpr int NB = 4096;
@@ -1459,7 +1509,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
       CUDA_TRY(c, cudaMemGetInfo(&free_b, &tot_b));
       budget = (long long)((free_b + c->tbdirs_cap) / 2 / 4);
     }
-    if (const char* e = getenv("NW_BATCH_TB_BUDGET")) budget = std::max(1LL, atoll(e) / 4);
+    if (c->opt[NW_OPT_BATCH_TB_BUDGET] > 0) budget = std::max(1LL, c->opt[NW_OPT_BATCH_TB_BUDGET] / 4);
     tdoff.resize(npairs);
     long long acc = 0, maxwave = 0;
     for (long long t = 0; t < npairs; ++t) {
@@ -1491,8 +1541,11 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   const size_t smem = smem_prof;
   // 6 x 4 warps per SM (24 warps, 72 registers each): C4 2.11 -> 2.26 TCUPS, C3 6.73 -> 6.84
   // over 4 per SM; 8 no better (tools/exp_ctas.sh, profiles/r01_exp_ctas.txt)
-  int ctas_per_sm = env_int("NW_BATCH_CTAS", 6, 1);
-  const long long nwarps = (long long)c->sm_count * ctas_per_sm * warps_per_cta;
+  int ctas_per_sm = 6;
+  // no more warps than pairs: the int32 traceback path sizes its per-warp direction
+  // scratch (~maxlen^2/4 bytes) per launched warp
+  const long long nwarps = std::min<long long>((long long)c->sm_count * ctas_per_sm * warps_per_cta,
+                                               (npairs + warps_per_cta - 1) / warps_per_cta * warps_per_cta);
   const long long bstride = maxlen + 1 + 64;
   // direction scratch per warp, in halfwords: int32 sweep = halfword per (group,
   // row, lane); packed sweep = 32-bit word per (group, packed row, lane)
@@ -1517,7 +1570,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   B.K = sc->K;
   B.g = sc->gap;
   B.ticket = c->d_ints;
-  B.err = c->d_ints + 1;
+  B.err = c->d_err;
   B.scores = d_scores;
   char* base = static_cast<char*>(c->d_scratch);
   B.wbnd = reinterpret_cast<int*>(base);
@@ -1529,7 +1582,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   B.ops_off = d_ops_off;
   B.ops = d_ops;
   B.ops_len = d_ops_len;
-  B.transpose_ok = (!tbk && sym && !getenv("NW_BATCH_NO_TRANSPOSE")) ? 1 : 0;
+  B.transpose_ok = (!tbk && sym && !c->opt[NW_OPT_BATCH_NO_TRANSPOSE]) ? 1 : 0;
   B.transposed = 0;
   B.ntr0 = ntr0;
   B.tdirs = two_phase ? static_cast<uint32_t*>(c->d_tbdirs) : nullptr;
@@ -1633,6 +1686,10 @@ nw_status nw_align_batch(nw_ctx* c, const uint8_t* seqs, const int64_t* offs, in
   nw_status st = batch_check(c, h_offs, nseq, pairs, npairs, sc, flags);
   if (st) return st;
   const bool tbk = flags & NW_TRACEBACK;
+  if (npairs == 0) {  // nothing to align: outputs may be NULL; ops_off[0] = 0 if given
+    if (tbk && ops_off) ops_off[0] = 0;
+    return NW_OK;
+  }
   if (!scores || (h_offs[nseq] > 0 && !seqs) || (tbk && (!ops_off || !ops || !ops_len)))
     return fail(c, NW_E_INVAL, "NULL argument");
   CUDA_TRY(c, cudaSetDevice(c->device));
@@ -1642,7 +1699,6 @@ nw_status nw_align_batch(nw_ctx* c, const uint8_t* seqs, const int64_t* offs, in
     st = nw_batch_ops_offsets(offs, nseq, pairs, npairs, ops_off);
     if (st) return fail(c, st, "ops offsets");
   }
-  if (npairs == 0) return NW_OK;
   const long long total = h_offs[nseq];
   // device staging: raw residues, offs, pairs, scores, (ops_off, ops, ops_len)
   const size_t b_raw = (size_t)total + 16, b_offs = sizeof(long long) * (nseq + 1),
@@ -1687,13 +1743,13 @@ nw_status nw_align_batch_dev(nw_ctx* c, const uint8_t* d_seqs, const int64_t* d_
   nw_status st = batch_check(c, ho, nseq, h_pairs, npairs, sc, flags);
   if (st) return st;
   const bool tbk = flags & NW_TRACEBACK;
+  if (npairs == 0) return NW_OK;  // nothing to align: outputs may be NULL
   if (!d_scores || !d_offs || (ho[nseq] > 0 && !d_seqs) || (d_pairs && !h_pairs) ||
       (!d_pairs && h_pairs) || (tbk && (!d_ops_off || !d_ops || !d_ops_len)))
     return fail(c, NW_E_INVAL, "NULL argument");
   CUDA_TRY(c, cudaSetDevice(c->device));
   st = upload_tables(c, sc);
   if (st) return st;
-  if (npairs == 0) return NW_OK;
   return batch_core(c, d_seqs, false, reinterpret_cast<const long long*>(d_offs), ho, nseq, d_pairs,
                     h_pairs, npairs, sc, flags, d_scores, reinterpret_cast<const long long*>(d_ops_off),
                     d_ops, d_ops_len);
@@ -1782,9 +1838,11 @@ nw_status msa_core(nw_ctx* c, const uint8_t* d_seqs, const long long* d_offs,
   nw_msa* h = new (std::nothrow) nw_msa;
   if (!h) return bail(fail(c, NW_E_NOMEM, "msa handle"));
   h->ctx = c; h->nseq = nseq; h->center = center; h->W = W;
+  c->live_msa.push_back(h);
   if (W > 0 && (size_t)nseq * (size_t)W > 0) {
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&h->d_rows), (size_t)nseq * W, c->stream);
     if (e != cudaSuccess) {
+      c->live_msa.pop_back();
       delete h;
       return bail(fail(c, NW_E_NOMEM, "msa rows of %lld bytes: %s", (long long)nseq * W, cudaGetErrorString(e)));
     }
@@ -1880,7 +1938,11 @@ nw_status nw_msa_rows(nw_ctx* c, const nw_msa* h, uint8_t* rows, int64_t row_str
 
 void nw_msa_free(nw_msa* h) {
   if (!h) return;
-  if (h->d_rows) cudaFreeAsync(h->d_rows, h->ctx->stream);
+  if (nw_ctx* c = h->ctx) {
+    if (h->d_rows) cudaFreeAsync(h->d_rows, c->stream);
+    auto& v = c->live_msa;
+    v.erase(std::remove(v.begin(), v.end(), h), v.end());
+  }
   delete h;
 }
 
@@ -2016,8 +2078,8 @@ nw_status linear_core(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b
   // segment height: directions take (n + 38) / 4 bytes per row
   // the checkpoint pass is score-only: the packed difference form when it applies
   // (its rows carry V; k_ckpt_prefix turns them into H' for the refills)
-  const bool ck_d16 = d16_ok(sc) && m >= 32LL * 16 * 150 && !getenv("NW_LINEAR_INT32");
-  const int kr_ck = ck_d16 ? d16_kr(m, c->sm_count) : choose_kr(m, n, false, sc->K);
+  const bool ck_d16 = d16_ok(c, sc) && m >= 32LL * 16 * 150 && !c->opt[NW_OPT_LINEAR_INT32];
+  const int kr_ck = ck_d16 ? d16_kr(c, m) : choose_kr(c, m, n, false, sc->K);
   const long long Rck = 32LL * kr_ck;
   const long long rows_max = std::max<long long>(1, budget / ((n + 38) / 4 + 1));
   const long long K = std::max<long long>(1, rows_max / Rck);
@@ -2053,7 +2115,7 @@ nw_status linear_core(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b
     ZeroRanges zb{{c->d_bnd, nullptr, nullptr, nullptr}, {bbytes, 0, 0, 0}};
     st = init_small(c, 8, zb);  // fresh ticket, error flag and ring tags for this fill
     if (st) break;
-    const int kr = choose_kr(mm, col, true, sc->K);
+    const int kr = choose_kr(c, mm, col, true, sc->K);
     nw_tb* tb = nullptr;
     st = new_tb(c, mm, col, sc, kr, &tb);
     if (st) break;

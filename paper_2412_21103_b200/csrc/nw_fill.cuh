@@ -56,6 +56,9 @@ struct FillArgs {
   const unsigned long long* top_row;  // tagged H' of the row above strip 0 (null: zeros),
   unsigned top_tag;                   //   tagged top_tag (the checkpoint writer's s+1)
   unsigned poll_ns = 0;               // back-off between re-polls of a boundary chunk (0: spin)
+  long long watchdog = 1LL << 28;     // re-polls of a late boundary chunk before *err is raised
+  int withhold = 0;                   // test only (NW_OPT_TEST_WITHHOLD): strip withhold-1 writes its
+  void* sink = nullptr;               //   bottom row to `sink` instead, so its consumer never sees it
 };
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
@@ -111,6 +114,7 @@ struct StripCtx {
   int* err;
   int* hm;
   unsigned poll_ns;
+  long long watchdog;
   int n, s, lane;
   int hm_lane, hm_r, hm_t;  // where H'(m, n) lives in this strip (hm_lane < 0: not here)
 };
@@ -154,7 +158,7 @@ __device__ __forceinline__ int chunk_verify(const StripCtx& C, int c0, unsigned 
       ok = (unsigned)(v >> 32) == tag;
     }
     if (__all_sync(FULL, ok)) break;
-    if (it > (1ll << 28)) {  // watchdog: report and stop waiting (results invalid)
+    if (it > C.watchdog) {  // watchdog: report and stop waiting (results invalid)
       if (C.lane == 0) atomicExch(C.err, 8);
       break;
     }
@@ -287,9 +291,11 @@ __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, 
     if ((s + 1) % A.ck_every == 0) C.bnd_out = A.ckpt + (long long)((s + 1) / A.ck_every - 1) * A.ck_stride;
     if (s > 0 && s % A.ck_every == 0) C.bnd_in = A.ckpt + (long long)(s / A.ck_every - 1) * A.ck_stride;
   }
+  if (MULTIWARP && s + 1 == A.withhold) C.bnd_out = A.sink;
   C.dir_base = DIRS ? A.dirs + (long long)s * A.wpl * (KR * 32) + lane : nullptr;
   C.err = A.err;
   C.poll_ns = A.poll_ns;
+  C.watchdog = A.watchdog;
   C.hm = A.hm;
   C.n = n;
   C.s = s;

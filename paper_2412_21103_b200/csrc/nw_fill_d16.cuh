@@ -142,9 +142,11 @@ __device__ __forceinline__ void strip_sweep_d16(const FillArgs& A, int s, int la
     if ((s + 1) % A.ck_every == 0) C.bnd_out = A.ckpt + (long long)((s + 1) / A.ck_every - 1) * A.ck_stride;
     if (s > 0 && s % A.ck_every == 0) C.bnd_in = A.ckpt + (long long)(s / A.ck_every - 1) * A.ck_stride;
   }
+  if (MULTIWARP && s + 1 == A.withhold) C.bnd_out = A.sink;
   C.dir_base = nullptr;
   C.err = A.err;
   C.poll_ns = A.poll_ns;
+  C.watchdog = A.watchdog;
   C.hm = A.hm;
   C.n = n;
   C.s = s;

@@ -9,6 +9,7 @@ nw_align_batch (+ the _dev variants on device pointers / torch CUDA tensors).
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 
@@ -21,6 +22,11 @@ NW_OK, NW_E_INVAL, NW_E_ALPHABET, NW_E_OVERFLOW, NW_E_NOMEM, NW_E_CUDA, NW_E_TRU
     NW_E_STATE, NW_E_DEADLOCK, NW_E_COMM = range(10)
 NW_DIAG, NW_UP, NW_LEFT = 1, 2, 3
 NW_SCORE_ONLY, NW_TRACEBACK = 0, 1
+# nw_ctx_set_option (include/nw.h): tuning / test options, 0 = the measured default
+OPTIONS = {"rows_per_lane": 0, "d16_force": 1, "d16_kr": 2, "no_d16": 3, "tall_kr8": 4,
+           "poll_ns": 5, "tb_step": 6, "tb_band": 7, "batch_kr16": 8, "batch_no_transpose": 9,
+           "batch_tb_budget": 10, "host_plan": 11, "linear_int32": 12, "cblock_warps_per_sm": 13,
+           "host_profile": 14, "watchdog_polls": 15, "test_withhold": 16}
 
 
 class NWError(RuntimeError):
@@ -56,6 +62,8 @@ def lib() -> ctypes.CDLL:
         "nw_last_error": ([vp], ctypes.c_char_p),
         "nw_last_bad_pos": ([vp], i64),
         "nw_ctx_sync": ([vp], ctypes.c_int),
+        "nw_ctx_set_option": ([vp, i32, i64], ctypes.c_int),
+        "nw_ctx_get_option": ([vp, i32], i64),
         "nw_ctx_launches": ([vp], i64),
         "nw_ctx_set_timing": ([vp, ctypes.c_int], ctypes.c_int),
         "nw_ctx_kernel_time": ([vp, ctypes.c_int, P(ctypes.c_double), P(i64)], ctypes.c_int),
@@ -101,7 +109,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = ("nw_ctx_create", "nw_ctx_destroy", "nw_strerror", "nw_last_error", "nw_last_bad_pos",
-            "nw_ctx_sync", "nw_ctx_launches", "nw_ctx_set_timing", "nw_ctx_kernel_time", "nw_score_only", "nw_score_only_dev",
+            "nw_ctx_sync", "nw_ctx_set_option", "nw_ctx_get_option", "nw_ctx_launches", "nw_ctx_set_timing", "nw_ctx_kernel_time", "nw_score_only", "nw_score_only_dev",
             "nw_align_pair", "nw_align_pair_dev", "nw_traceback", "nw_traceback_dev",
             "nw_tb_free", "nw_align_batch", "nw_align_batch_dev", "nw_batch_ops_offsets",
             "nw_score_only_cblock", "nw_cblock_recv_bytes", "nw_score_only_cblock_rank_dev",
@@ -176,6 +184,25 @@ class Context:
 
     def sync(self):
         self._check(lib().nw_ctx_sync(self._h))
+
+    def set_option(self, name: str, value: int):
+        """nw_ctx_set_option by name (OPTIONS); 0 restores the default."""
+        self._check(lib().nw_ctx_set_option(self._h, OPTIONS[name], int(value)))
+
+    def get_option(self, name: str) -> int:
+        return int(lib().nw_ctx_get_option(self._h, OPTIONS[name]))
+
+    @contextlib.contextmanager
+    def options(self, **kw):
+        """Set options for the duration of a with-block, then restore them."""
+        old = {k: self.get_option(k) for k in kw}
+        try:
+            for k, v in kw.items():
+                self.set_option(k, v)
+            yield self
+        finally:
+            for k, v in old.items():
+                self.set_option(k, v)
 
     def close(self):
         if self._h:

@@ -25,3 +25,18 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture
+def opts(request):
+    """opts(ctx, name, value): nw_ctx_set_option for this test only (reset to the
+    default, 0, when the test ends)."""
+    undo = []
+
+    def set_(ctx, name, value):
+        ctx.set_option(name, value)
+        undo.append((ctx, name))
+
+    yield set_
+    for ctx, name in reversed(undo):
+        ctx.set_option(name, 0)

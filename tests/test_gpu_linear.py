@@ -89,13 +89,13 @@ def test_c5_scale_closed_forms(ctx):
 @pytest.mark.parametrize("m,n,budget", [(80_000, 400, 1), (80_000, 400, 2_000_000),
                                         (100_000, 1_500, 9_000_000)])
 @pytest.mark.parametrize("int32", [False, True])
-def test_tall_packed_checkpoint_pass(ctx, monkeypatch, m, n, budget, int32):
+def test_tall_packed_checkpoint_pass(ctx, opts, m, n, budget, int32):
     """Tall pairs (>= 76,800 rows): the checkpoint pass runs the packed difference
     form, whose checkpoint rows carry V and are prefix-summed into H' for the
     refills (k_ckpt_prefix); NW_LINEAR_INT32 forces the int32 pass. Both must give
     the oracle's score and canonical path, many segments down to one strip each."""
     if int32:
-        monkeypatch.setenv("NW_LINEAR_INT32", "1")
+        opts(ctx, "linear_int32", 1)
     a, b = nwgen.random_pair(m + n, m, n)
     for tie in [(1, 2, 3), (3, 2, 1)]:
         _check(ctx, a, b, nwgen.Scoring(tie=tie), budget)

@@ -309,10 +309,10 @@ def test_score_only_tall_difference_form(ctx, m, n):
 
 
 @pytest.mark.parametrize("kr", [4, 8, 12, 14, 16, 18, 20, 22, 24, 26, 28, 30, 32])
-def test_score_only_difference_form_every_kr(ctx, monkeypatch, kr):
+def test_score_only_difference_form_every_kr(ctx, opts, kr):
     """The packed score-only sweep at every rows-per-lane setting the library can pick
     (strip heights 128..1,024 rows, ragged last strips, one-strip pairs)."""
-    monkeypatch.setenv("NW_D16_FORCE", str(kr))
+    opts(ctx, "d16_force", kr)
     for k, (m, n) in enumerate([(2500, 700), (32 * kr * 3 + 17, 333), (5, 900), (1, 1)]):
         a, b = _pair(9100 + 37 * kr + k, m, n)
         for sc in (nwgen.PAPER_DNA, nwgen.Scoring(match=2, mismatch=-1, gap=-3)):
@@ -329,16 +329,17 @@ def test_c5_default_strip_choice(ctx):
 
 
 @pytest.mark.parametrize("G,w", [(2, 0), (3, 700)])
-def test_cblock_rank_api_concurrent_streams(ctx, monkeypatch, G, w):
+def test_cblock_rank_api_concurrent_streams(ctx, opts, G, w):
     """The per-rank (real multi-GPU) entry point, with the G ranks as concurrent
     launches on G streams of one GPU and plain device buffers as 'peer' memory."""
     import torch
-    monkeypatch.setenv("NW_CBLOCK_WARPS_PER_SM", "4")
     m, n = 5000, 9000
     a, b = _pair(9100 + G, m, n)
     sc = nwgen.PAPER_DNA
     streams = [torch.cuda.Stream() for _ in range(G)]
     ctxs = [nwb.Context(0, s.cuda_stream) for s in streams]
+    for c in ctxs:  # every rank's warps must be resident at once: share the GPU
+        c.set_option("cblock_warps_per_sm", 4)
     da = torch.frombuffer(bytearray(a), dtype=torch.uint8).cuda()
     db = torch.frombuffer(bytearray(b), dtype=torch.uint8).cuda()
     nbytes = nwb.nw_cblock_recv_bytes(m)
@@ -378,7 +379,7 @@ def test_batch_traceback_paths_all_orders(ctx, tie, scname):
 
 
 @pytest.mark.parametrize("mode", ["waves", "kr16", "implicit", "notranspose", "asymmetric"])
-def test_batch_traceback_two_phase_modes(ctx, monkeypatch, mode):
+def test_batch_traceback_two_phase_modes(ctx, opts, mode):
     """Two-phase batch traceback (the fill keeps every pair's flags, k_batch_walk walks
     them, one thread per pair; pairs whose last strip would waste more lanes are
     filled transposed under the mirrored tie order): split into many waves by a tiny
@@ -388,15 +389,15 @@ def test_batch_traceback_two_phase_modes(ctx, monkeypatch, mode):
     across strip edges."""
     subst = nwgen.BLOSUM62
     if mode == "kr16":
-        monkeypatch.setenv("NW_BATCH_KR16", "16")
+        opts(ctx, "batch_kr16", 16)
     elif mode == "notranspose":
-        monkeypatch.setenv("NW_BATCH_NO_TRANSPOSE", "1")
+        opts(ctx, "batch_no_transpose", 1)
     elif mode == "asymmetric":  # s(x,y) != s(y,x): never filled transposed
         subst = np.array(nwgen.BLOSUM62, dtype=np.int32).copy()
         subst[0, 1] += 2
         subst[5, 9] -= 1
     else:
-        monkeypatch.setenv("NW_BATCH_TB_BUDGET", str(300_000))
+        opts(ctx, "batch_tb_budget", 300_000)
     ss = nwgen.random_set(61, 30 if mode != "implicit" else 14, 0, 1300, nwgen.PROTEIN)
     rng = np.random.Generator(np.random.PCG64(61))
     pairs = rng.integers(0, ss.nseq, size=(120, 2)).astype(np.int32)
@@ -414,7 +415,7 @@ def test_batch_traceback_two_phase_modes(ctx, monkeypatch, mode):
 
 
 @pytest.mark.parametrize("sym", [True, False])
-def test_batch_score_only_orientation(ctx, monkeypatch, sym):
+def test_batch_score_only_orientation(ctx, opts, sym):
     """Score-only batches fill each pair in the orientation that wastes fewer strip
     rows when s is symmetric (Score(a,b) = Score(b,a)); an asymmetric s must keep
     a on the rows. Lengths straddle the 512-row strip edges in both directions."""
@@ -429,16 +430,16 @@ def test_batch_score_only_orientation(ctx, monkeypatch, sym):
     rev = pairs[:, ::-1].copy()
     assert nwb.nw_align_batch(ctx, ss.residues, ss.offs, rev, sc).tolist() == \
         oracle.batch_score(ss.residues, ss.offs, rev, sc).tolist()
-    monkeypatch.setenv("NW_BATCH_NO_TRANSPOSE", "1")
+    opts(ctx, "batch_no_transpose", 1)
     assert nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc).tolist() == want.tolist()
 
 
 @pytest.mark.parametrize("kr", [2, 4, 5, 6, 8, 10, 12])
-def test_pair_every_rows_per_lane(ctx, monkeypatch, kr):
+def test_pair_every_rows_per_lane(ctx, opts, kr):
     """The single-pair fill + strip traceback at every rows-per-lane setting (5, 6, 10,
     12: strips of 160 / 192 / 320 / 384 rows, not powers of two), all tie orders on a
     tie-rich pair."""
-    monkeypatch.setenv("NW_KR", str(kr))
+    opts(ctx, "rows_per_lane", kr)
     for k, (m, n) in enumerate([(32 * kr * 3 + 17, 1500), (2000, 700), (700, 2100), (5, 9)]):
         a, b = _pair(9300 + 11 * kr + k, m, n)
         check_pair(ctx, a, b, nwgen.PAPER_DNA)
@@ -476,13 +477,13 @@ def test_batch_caller_owned_outputs(ctx):
 
 
 @pytest.mark.parametrize("host_plan", [False, True])
-def test_batch_traceback_device_plan(ctx, monkeypatch, host_plan):
+def test_batch_traceback_device_plan(ctx, opts, host_plan):
     """Large explicit traceback batches (>= 4,096 pairs) are planned on the device
     (LPT buckets, orientation, word offsets) once the kept flag buffer is sized;
     NW_HOST_PLAN forces the host planner. Results are identical either way and equal
     the oracle's (scores of all pairs, paths of a sample)."""
     if host_plan:
-        monkeypatch.setenv("NW_HOST_PLAN", "1")
+        opts(ctx, "host_plan", 1)
     ss = nwgen.random_set(91, 400, 0, 260, nwgen.PROTEIN)
     rng = np.random.Generator(np.random.PCG64(91))
     pairs = rng.integers(0, ss.nseq, size=(5000, 2)).astype(np.int32)
