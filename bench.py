@@ -1,12 +1,15 @@
 """GCUPS benchmark of the B200 NW hot path (BASELINE.json metric).
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                [--workload c2|c1|c3|c4|c5]
+                [--workload c3|c1|c2|c4|c5|...]
 
-Default workload = BASELINE.json configs[1] (C2): one DNA pair 20,000 x 20,000,
-+1/-1/-1, fill + 2-bit packed directions + traceback. One step = one pass of the
-whole hot path: nw_align_pair_dev (encode + fill + directions) and
-nw_traceback_dev (walk + reverse) on inputs resident in HBM.
+Default workload = C3 (BASELINE.json configs[2]), the configuration the metric's
+1/2/4/8-GPU scaling is quoted on: all 2,096,128 pairs of 2,048 DNA sequences of
+500-2,000 bp, score-only. One step = one nw_align_batch_dev call on inputs
+resident in HBM: encode, the all-pairs batch fill and, with N ranks, the gather
+of every rank's scores (each rank aligns its cost-balanced range).
+--gpus N without a torchrun environment spawns the N ranks itself (one process
+per GPU, NCCL); under torchrun the environment's ranks are used.
 
 value   : GCUPS = m*n cells / device time per step (CUDA events on the context
           stream, per step, L2 flushed between steps), whole job over N ranks.
@@ -17,8 +20,11 @@ roofline: the fill kernel's integer-op rate vs the issue-limited lane-op peak
           (DESIGN.md §5).
 cpu_baseline: the oracle (plain C, 1 core) on a bounded sample of the workload.
 --impl reference: the oracle timed on the host as the reference arm.
-Multi-GPU (torchrun): C2 is one pair (no exchange step): N independent
-replicas, weak scaling. c3 shards pairs across ranks and all-gathers scores.
+Multi-GPU: C3/C4 shard pairs across ranks (dist context) and gather every
+score on every rank: "scaling": "strong" (the total work is fixed). C1/C2 are one
+pair with no exchange step: N independent replicas, weak scaling.
+check   : after the timed loop, a sample of the timed outputs is compared with the
+          oracle (outside the timed region).
 """
 from __future__ import annotations
 
@@ -40,9 +46,16 @@ import nwgen  # noqa: E402
 
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 ALU_ISSUE_LANES_PER_CLK_PER_SM = 128  # 4 SMSPs x 32 lanes x 1 warp-instr/clk (tools/peaks_int.cu)
+ALU_PIPE_LANES_PER_CLK_PER_SM = 64    # VIMNMX3/VIADDMNMX/IADD3/PRMT/SHF: the half-rate ALU pipe (measured)
 SM_COUNT = 148
 SM_MAX_MHZ = 1965.0
-OPS_PER_CELL = {"dirs": 6, "score": 3}  # SURVEY.md §8(d) algorithmic op floors
+# SURVEY.md §8(d) algorithmic op floors per cell, by the arithmetic form of the fill:
+# int32 with directions 6, int32 score-only 3, two 16-bit cells per register (H' half
+# rows, C3) 1.5, the packed difference form (C5: PRMT + VIMNMX3.U16x2 + 2 IADD per two
+# cells) 2, packed with decision flags (C4) 2 (SURVEY's "u16x2 + direction")
+OPS_PER_CELL = {"dirs": 6, "score": 3, "u16": 1.5, "d16": 2, "d16dir": 2}
+FORM = {"c1": "dirs", "c2": "dirs", "c1p": "dirs", "c2p": "dirs", "c1co": "dirs", "c2co": "dirs",
+        "c3": "u16", "c4": "d16dir", "c5": "d16", "c5tb": "d16", "msa": "u16"}
 WORKLOADS = {
     "c1": "C1: single DNA pair 1,000 x 1,000, +1/-1/-1, score + full traceback",
     "c2": "C2: single DNA pair 20,000 x 20,000, +1/-1/-1, score + 2-bit packed traceback",
@@ -243,8 +256,6 @@ class PairWorkload:
         self.d_ops = torch.zeros(self.m + self.n, dtype=torch.uint8, device="cuda")
         self.d_len = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.cells = self.m * self.n
-        # C5 with several ranks: one pair split over the ranks (strong scaling), not replicas
-        self.pipeline = workload == "c5" and int(os.environ.get("WORLD_SIZE", "1")) > 1
 
     def step(self):
         if self.coopt:  # host-pointer API (synchronous)
@@ -258,10 +269,6 @@ class PairWorkload:
             tb = self.nwb.nw_align_pair_dev(self.ctx, self.da, self.db, self.sc, self.d_score)
             self.nwb.nw_traceback_dev(self.ctx, tb, self.d_ops, self.d_len)
             tb.free()
-        elif self.pipeline:
-            # C5 on N GPUs: one pair, column blocks pipelined across ranks (a10)
-            from paper_2412_21103_b200 import dist as nwdist
-            nwdist.cblock_score(self.ctx, self.da, self.db, self.sc)
         else:
             self.nwb.nw_score_only_dev(self.ctx, self.da, self.db, self.sc, self.d_score)
 
@@ -288,9 +295,28 @@ class PairWorkload:
     def h2d_bytes(self):
         return self.m + self.n
 
+    def check(self):
+        """The last timed step's outputs vs the oracle (outside the timed region)."""
+        import oracle
+        if self.coopt or self.linear:
+            return {"against": "none", "what": "not checked here (see tests/)"}
+        got = int(self.d_score.item())
+        if self.workload == "c5":  # oracle score of the seeded pair: tools/oracle_digests.py
+            dp = os.path.join(ROOT, "tests", "golden", "digests.json")
+            want = json.load(open(dp)).get("c5", {}).get("score") if os.path.exists(dp) else None
+            return {"against": "oracle (tests/golden/digests.json)", "what": "score", "sample": 1,
+                    "mismatches": None if want is None else int(got != want)}
+        ws, wops = oracle.align(self.a, self.b, self.sc)
+        ln = int(self.d_len.item())
+        ops = self.d_ops[:ln].cpu().numpy()
+        return {"against": "oracle", "what": "score and path", "sample": 1,
+                "mismatches": int(got != ws or ops.tolist() != wops.tolist())}
+
 
 class BatchWorkload:
-    """C3 (all pairs, score-only, sharded by rank) and C4 (protein, traceback)."""
+    """C3 (all pairs, score-only) and C4 (protein pairs, traceback). With N ranks the
+    context is a dist context (include/nw.h): every rank passes the full inputs,
+    aligns its cost-balanced range and receives every rank's outputs."""
 
     def __init__(self, ctx, torch, workload: str, rank: int, world: int):
         import paper_2412_21103_b200 as nwb
@@ -301,35 +327,29 @@ class BatchWorkload:
             pairs = nwgen.all_pairs(ss.nseq)
             self.sc = nwgen.PAPER_DNA
             self.flags = nwb.NW_SCORE_ONLY
+            self.h_pairs = None  # implicit all pairs
         else:
             ss = nwgen.config_c4()
             pairs = nwgen.consecutive_pairs(ss.nseq // 2)
             self.sc = nwgen.PROTEIN_BLOSUM62
             self.flags = nwb.NW_TRACEBACK
-        from paper_2412_21103_b200 import dist as nwdist
-        self.nwdist = nwdist
-        lens = ss.lengths()
-        cost = nwdist.pair_costs(lens, pairs)
-        self.total_cells = int(cost.sum())
-        self.npairs_total = len(pairs)
-        # cost-balanced shard of the pair list over ranks (reading R18)
+            self.h_pairs = pairs
+        lens = ss.lengths().astype(np.int64)
+        self.all_pairs = pairs
+        self.total_cells = self.cells = int((lens[pairs[:, 0]] * lens[pairs[:, 1]]).sum())
+        self.npairs = len(pairs)
         if world > 1:
-            self.shard = nwdist.partition_pairs(cost, world)[rank]
-            pairs_r = pairs[self.shard]
-        else:
-            self.shard = None
-            pairs_r = pairs if workload == "c4" else None
+            from paper_2412_21103_b200 import dist as nwdist
+            b = nwdist.partition(ss.offs, self.h_pairs, world)
+            self.range = (int(b[rank]), int(b[rank + 1]))
         self.ss = ss
-        self.h_pairs = pairs_r
-        self.npairs = len(pairs) if pairs_r is None else len(pairs_r)
-        self.cells = int(cost.sum()) if pairs_r is None else int(
-            (lens[pairs_r[:, 0]].astype(np.int64) * lens[pairs_r[:, 1]]).sum())
         self.d_seqs = torch.from_numpy(ss.residues).cuda()
         self.d_offs = torch.from_numpy(ss.offs).cuda()
-        self.d_pairs = None if pairs_r is None else torch.from_numpy(pairs_r).cuda()
+        self.d_pairs = None if self.h_pairs is None else torch.from_numpy(self.h_pairs).cuda()
         self.d_scores = torch.zeros(max(self.npairs, 1), dtype=torch.int32, device="cuda")
         if self.flags:
-            oo = nwb.nw_batch_ops_offsets(ss.offs, pairs_r)
+            oo = nwb.nw_batch_ops_offsets(ss.offs, self.h_pairs)
+            self.oo = oo
             self.d_ops_off = torch.from_numpy(oo).cuda()
             self.d_ops = torch.zeros(int(oo[-1]) + 1, dtype=torch.uint8, device="cuda")
             self.d_ops_len = torch.zeros(self.npairs, dtype=torch.int32, device="cuda")
@@ -339,7 +359,7 @@ class BatchWorkload:
         # host memory (the copies inside the timed region then run at DMA speed)
         self.h_res = _pinned(torch, ss.residues)
         self.h_offs = _pinned(torch, ss.offs)
-        self.h_pairs_pin = None if pairs_r is None else _pinned(torch, pairs_r)
+        self.h_pairs_pin = None if self.h_pairs is None else _pinned(torch, self.h_pairs)
         if self.flags:
             self.h_out = (_pinned(torch, np.empty(self.npairs, np.int32)),
                           _pinned(torch, np.empty(int(oo[-1]) + 1, np.uint8)),
@@ -348,15 +368,10 @@ class BatchWorkload:
         else:
             self.h_out = _pinned(torch, np.empty(self.npairs, np.int32))
 
-
     def step(self):
         self.nwb.nw_align_batch_dev(self.ctx, self.d_seqs, self.d_offs, self.ss.offs, self.d_pairs,
                                     self.h_pairs, self.npairs, self.sc, self.flags, self.d_scores,
                                     self.d_ops_off, self.d_ops, self.d_ops_len)
-        if self.world > 1:
-            # P:131 "gathered back in the main process": every rank gets every shard's scores
-            self.full = self.nwdist.gather_scores(self.d_scores, self.shard, self.npairs_total,
-                                                  self.world)
 
     def step_host(self):
         r = self.nwb.nw_align_batch(self.ctx, self.h_res, self.h_offs, self.h_pairs_pin, self.sc,
@@ -365,6 +380,28 @@ class BatchWorkload:
             scores, ops, ops_off, ops_len = r
             return scores.nbytes + ops.nbytes + ops_len.nbytes
         return r.nbytes
+
+    def check(self, k: int = 48):
+        """Compare a seeded sample of the last timed step's outputs (every rank's, as
+        gathered) with the oracle: scores, and paths with NW_TRACEBACK."""
+        import oracle
+        rng = np.random.Generator(np.random.PCG64(12345))
+        idx = np.sort(rng.choice(self.npairs, size=min(k, self.npairs), replace=False))
+        scores = self.d_scores.cpu().numpy()
+        pairs = self.all_pairs[idx]
+        bad = 0
+        if self.flags:
+            ops, ln = self.d_ops.cpu().numpy(), self.d_ops_len.cpu().numpy()
+            for i, (p, q) in zip(idx, pairs):
+                ws, wops = oracle.align(self.ss.seq(p), self.ss.seq(q), self.sc)
+                got = ops[self.oo[i]:self.oo[i] + ln[i]]
+                bad += int(scores[i] != ws or got.tolist() != wops.tolist())
+            what = "scores and paths"
+        else:
+            want = oracle.batch_score(self.ss.residues, self.ss.offs, pairs, self.sc)
+            bad = int((scores[idx] != want).sum())
+            what = "scores"
+        return {"against": "oracle", "what": what, "sample": int(len(idx)), "mismatches": bad}
 
     @property
     def h2d_bytes(self):
@@ -416,6 +453,10 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     ctx = nwb.Context(local, stream.cuda_stream)
     wl = args.workload
+    sharded = wl in ("c3", "c4") and world > 1
+    if sharded:  # the library's own NCCL communicator (nw_ctx_set_dist), id shared by rank 0
+        from paper_2412_21103_b200 import dist as nwdist
+        nwdist.init_dist_context(ctx)
     if wl in ("c1", "c2", "c5", "c1p", "c2p", "c5tb", "c1co", "c2co"):
         W = PairWorkload(ctx, torch, wl, rank)
     elif wl == "msa":
@@ -462,12 +503,10 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    if wl in ("c1", "c2", "msa", "c1p", "c2p", "c5tb", "c1co", "c2co") or (wl == "c5" and world == 1):
-        cells_all = W.cells * world  # replicas: every rank aligns its own pair / set
-    elif wl == "c5":
-        cells_all = W.cells          # one pair pipelined across the ranks
+    if sharded or wl in ("c3", "c4"):
+        cells_all = W.total_cells    # one batch split over the ranks, gathered on every rank
     else:
-        cells_all = W.total_cells
+        cells_all = W.cells * world  # replicas: every rank aligns its own pair / set
     value = cells_all / (ms_per_step / 1e3) / 1e9
     # ---- e2e through the host-pointer ABI
     torch.cuda.synchronize()
@@ -492,7 +531,7 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (the fill)
     fill_avg_ms = fill_ms / max(fill_n, 1)
     fill_launches_per_step = fill_n / max(args.steps, 1)
-    mode = "dirs" if (wl in ("c1", "c2", "c4", "c1p", "c2p", "c5tb", "c1co", "c2co")) else "score"
+    mode = FORM[wl]
     ops = OPS_PER_CELL[mode]
     # the step's cells over the fill time of the whole step (C4 fills in two launches:
     # the pairs kept in their orientation, then the transposed ones)
@@ -500,15 +539,16 @@ def run_ours(args):
     achieved = W.cells * ops / (fill_step_ms / 1e3) / 1e12 if fill_n else None
     if wl == "c5tb":  # one score-only pass + the direction refills of every segment
         fill_avg_ms = fill_ms / max(args.steps, 1)
-        ops = f"{OPS_PER_CELL['score']} (checkpoint pass; refill ops not counted: a lower bound)"
-        achieved = W.cells * OPS_PER_CELL["score"] / (fill_avg_ms / 1e3) / 1e12 if fill_n else None
+        ops = f"{OPS_PER_CELL['d16']} (checkpoint pass; refill ops not counted: a lower bound)"
+        achieved = W.cells * OPS_PER_CELL["d16"] / (fill_avg_ms / 1e3) / 1e12 if fill_n else None
     if wl == "msa":  # two batch launches per step: all pairs score-only, center pairs + dirs
-        ops = f"{OPS_PER_CELL['score']} (all pairs) / {OPS_PER_CELL['dirs']} (center alignments)"
+        ops = f"{OPS_PER_CELL['u16']} (all pairs) / {OPS_PER_CELL['d16dir']} (center alignments)"
         fill_step_ms = fill_ms / max(args.steps, 1)
-        achieved = (W.cells_pairs * OPS_PER_CELL["score"] + W.cells_center * OPS_PER_CELL["dirs"]) / (
+        achieved = (W.cells_pairs * OPS_PER_CELL["u16"] + W.cells_center * OPS_PER_CELL["d16dir"]) / (
             fill_step_ms / 1e3) / 1e12 if fill_n else None
         fill_avg_ms = fill_step_ms
-    peak = ALU_ISSUE_LANES_PER_CLK_PER_SM * SM_COUNT * SM_MAX_MHZ * 1e6 / 1e12
+    peak_issue = ALU_ISSUE_LANES_PER_CLK_PER_SM * SM_COUNT * SM_MAX_MHZ * 1e6 / 1e12
+    peak = ALU_PIPE_LANES_PER_CLK_PER_SM * SM_COUNT * SM_MAX_MHZ * 1e6 / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{wl}.json")
     if os.path.exists(tp):
@@ -523,6 +563,7 @@ def run_ours(args):
                 "peak_GBps": load_peaks().get("hbm_gbs"), "bytes_source": os.path.relpath(wp, ROOT)}
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (int32 lane-ops)",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "peak_issue": peak_issue, "frac_issue": (achieved / peak_issue) if achieved else None,
                 "kernel": ("k_percell_fill" if wl in ("c1p", "c2p") else
                            "k_fill_pair" if wl in ("c1", "c2", "c5", "c5tb") else "k_batch"),
                 **({"kernel_ms_is": "both k_batch launches of one step"} if wl == "msa" else {}),
@@ -530,22 +571,29 @@ def run_ours(args):
                 "kernel_launches_per_step": fill_launches_per_step,
                 "kernel_share_of_step": (fill_ms / total_ms) if total_ms else None,
                 "traceback_ms_per_step": tb_ms / max(args.steps, 1),
-                "peak_source": "tools/peaks_int.cu issue limit 128 lane-ops/clk/SM x 148 SMs x 1965 MHz",
+                "peak_source": ("tools/peaks_int.cu (profiles/r02_peaks_int.json): the ALU pipe's 64 "
+                                "lane-ops/clk/SM for the 3-input / add-max / packed-16-bit ops the fills issue "
+                                "(VIMNMX3, VIADDMNMX, IADD3, PRMT, SHF) x 148 SMs x 1965 MHz; peak_issue: the "
+                                "128 lane-ops/clk/SM warp-issue limit (2-input VIMNMX). MEASURED_PEAKS.json "
+                                "has no INT32 entry"),
+                "form": mode,
                 **({"traceback_walk": walk} if walk else {})}
     out = {
         "metric": "GCUPS (cell updates/s)", "value": value, "unit": "GCUPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong" if (wl == "c5" and world > 1) else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if wl in ("c3", "c4") else "weak", "vs_baseline": None,
         # arithmetic of the fill kernel in use: int32 strips, or two 16-bit cells per register
         "dtype": "int32" if wl in ("c1", "c2", "c1p", "c2p", "c5tb", "c1co", "c2co") else "u16x2",
         **({"msa": {"center": W.center, "width": W.width}} if wl == "msa" else {}),
         "data": "synthetic (nwgen seeded, SURVEY.md §8(d) recipe)",
         "config": {"workload": WORKLOADS[wl], "cells_per_step": cells_all,
-                   "parallelism": (f"replicas{world}" if wl in ("c1", "c2", "msa", "c1p", "c2p", "c5tb", "c1co", "c2co") or (wl == "c5" and world == 1)
-                                   else f"column-blocks{world}" if wl == "c5" else f"pairs-sharded{world}"),
+                   "parallelism": (f"pairs-sharded{world} (cost-balanced ranges, NCCL in-place broadcasts)"
+                                   if wl in ("c3", "c4") else f"replicas{world}"),
                    "l2": "flushed between steps (256 MB write)"},
         "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roofline,
     }
+    if rank == 0 and hasattr(W, "check") and not args.no_check:
+        out["check"] = W.check()  # a sample of the timed outputs vs the oracle (untimed)
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_oracle_sample(wl)
     if rank == 0:
@@ -588,13 +636,18 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-check", action="store_true", help="skip the oracle spot check")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # no torchrun environment: one process per GPU, spawned here (rank 0 prints)
+        from paper_2412_21103_b200 import dist as nwdist
+        nwdist.launch(args.gpus, run_ours, (args,))
     else:
         run_ours(args)
 

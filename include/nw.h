@@ -50,7 +50,8 @@ typedef enum {
   NW_E_TRUNC = 6,     /* ops buffer too small: *len holds the required length */
   NW_E_STATE = 7,     /* traceback handle belongs to another context or holds no directions */
   NW_E_DEADLOCK = 8,  /* an inter-warp dependency wait exceeded its watchdog */
-  NW_E_COMM = 9       /* reserved for the multi-GPU path */
+  NW_E_COMM = 9       /* NCCL could not be loaded, or a collective / communicator failed
+                         (dist contexts, nw_ctx_set_dist) */
 } nw_status;
 
 enum { NW_DIAG = 1, NW_UP = 2, NW_LEFT = 3 }; /* 1 diagonal, 2 vertical, 3 horizontal */
@@ -152,6 +153,35 @@ nw_status nw_align_batch_dev(nw_ctx *ctx, const uint8_t *d_seqs, const int64_t *
 /* Host helper: ops_off[0..npairs] worst-case offsets for NW_TRACEBACK (see above). */
 nw_status nw_batch_ops_offsets(const int64_t *h_offs, int32_t nseq, const int32_t *h_pairs,
                                int64_t npairs, int64_t *ops_off);
+
+/* ---- distributed context: one process per GPU ----
+ * "the total number of alignments is divided by the number of ranks ... the
+ * data is then sent to each rank ... gathered back in the main process".
+ * nw_dist_unique_id: rank 0 creates the 128-byte NCCL id; the caller hands it to every
+ *   rank (any channel: torch.distributed, a file, MPI). NW_E_COMM if NCCL (libnccl.so.2,
+ *   loaded at run time) is unavailable. Needs no GPU.
+ * nw_ctx_set_dist: collective over the `world` ranks (each calls it with its rank on
+ *   its own device's ctx); replaces an earlier communicator. world = 1 is legal (the
+ *   collectives then move nothing). NW_E_COMM on NCCL failure.
+ * On a dist ctx, nw_align_batch / nw_align_batch_dev take the SAME inputs on every rank
+ *   and return the FULL outputs on every rank: each rank aligns the contiguous,
+ *   cost-balanced range nw_batch_partition gives it (explicit pairs: pair-index ranges;
+ *   pairs = NULL score-only: ranges of the length-descending rank space), then one group
+ *   of in-place NCCL broadcasts gathers every range (scores, and with NW_TRACEBACK the
+ *   path lengths and ops bytes). Results are identical to a single-GPU call (reading
+ *   R18: the partition never changes a result). Asynchronous NCCL failures surface as
+ *   NW_E_COMM at the next synchronising call. */
+nw_status nw_dist_unique_id(uint8_t id[128]);
+nw_status nw_ctx_set_dist(nw_ctx *ctx, int32_t rank, int32_t world, const uint8_t id[128]);
+/* This ctx's rank and world (0 / 1 without nw_ctx_set_dist). */
+nw_status nw_ctx_dist_info(const nw_ctx *ctx, int32_t *rank, int32_t *world);
+/* Host helper (no GPU): bounds[0..world] of the dist batch partition, bounds[r] = the first
+ * task of rank r. Tasks are the pairs in pair order, or (pairs == NULL) k_batch's rank
+ * space: all p' < q' over the sequences sorted by length descending (stable), row-major.
+ * bounds[r] is the first task whose cost prefix (sum of m*n over earlier tasks) reaches
+ * r/world of the total, so every range is within one task's cost of total/world. */
+nw_status nw_batch_partition(const int64_t *offs, int32_t nseq, const int32_t *pairs,
+                             int64_t npairs, int32_t world, int64_t *bounds);
 
 /* ---- column-block wavefront (giant pair across ranks) ----
  * Score-only H(m,n) computed as the multi-GPU pipeline computes it: columns cut
@@ -277,7 +307,11 @@ enum {
   NW_OPT_WATCHDOG_POLLS = 15,  /* re-polls of a late boundary entry before NW_E_DEADLOCK (0: 2^28) */
   NW_OPT_TEST_WITHHOLD = 16,   /* test only: 1 + the strip whose bottom row is never published
                                   (single-pair fills), so its consumer's watchdog must fire */
-  NW_OPT_COUNT_ = 17
+  NW_OPT_DIST_VIRTUAL_WORLD = 17, /* test only, ctx without nw_ctx_set_dist: batch calls align only
+                                     rank DIST_VIRTUAL_RANK's range of a world of this size and
+                                     gather nothing (G sequential calls replay G ranks on one GPU) */
+  NW_OPT_DIST_VIRTUAL_RANK = 18,
+  NW_OPT_COUNT_ = 19
 };
 nw_status nw_ctx_set_option(nw_ctx *ctx, int32_t option, int64_t value);
 /* Current value, or -1 for a NULL ctx / unknown option. */

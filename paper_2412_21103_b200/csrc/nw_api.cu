@@ -22,6 +22,7 @@
 #include "nw_msa.cuh"
 #include "nw_percell.cuh"
 #include "nw_coopt.cuh"
+#include "nw_dist.cuh"
 
 using namespace nwk;
 
@@ -78,6 +79,15 @@ struct nw_ctx {
   std::vector<cudaEvent_t> ev_pool;
   // tuning / test options (nw_ctx_set_option; 0 = the measured default)
   long long opt[NW_OPT_COUNT_] = {0};
+  // distributed context (nw_ctx_set_dist): one process per GPU, NCCL communicator
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  int* d_rs = nullptr;          // implicit dist batches: every rank-space task's score
+  size_t rs_cap = 0;
+  int* d_pmat = nullptr;        // implicit dist traceback batches: materialised lex pairs
+  size_t pmat_cap = 0;
+  std::vector<long long> h_bounds, h_oo;
+  std::vector<int> h_pmat;
   // live handles: nw_ctx_destroy releases their device memory and detaches them, so
   // a handle freed after its context only deletes its host struct
   std::vector<nw_tb*> live_tb;
@@ -595,6 +605,11 @@ nw_status check_deferred(nw_ctx* c) {
     return fail(c, NW_E_ALPHABET, "residue at position %lld is not in the alphabet", bad);
   }
   if (errf) return fail(c, NW_E_DEADLOCK, "inter-warp dependency watchdog fired");
+  if (c->comm) {
+    ncclResult_t ar = ncclSuccess;
+    if (nwd::nccl().CommGetAsyncError(c->comm, &ar) != ncclSuccess || ar != ncclSuccess)
+      return fail(c, NW_E_COMM, "NCCL communicator error: %s", nwd::nccl().GetErrorString(ar));
+  }
   return NW_OK;
 }
 
@@ -817,11 +832,14 @@ void nw_ctx_destroy(nw_ctx* c) {
   if (c->stage_ev) { cudaEventSynchronize(c->stage_ev); cudaEventDestroy(c->stage_ev); }
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->d_tbdirs) cudaFreeAsync(c->d_tbdirs, c->stream);
+  if (c->d_rs) cudaFreeAsync(c->d_rs, c->stream);
+  if (c->d_pmat) cudaFreeAsync(c->d_pmat, c->stream);
   if (c->d_tdoff) cudaFreeAsync(c->d_tdoff, c->stream);
   cudaStreamSynchronize(c->stream);
   for (auto& v : c->ev_open)
     for (auto& pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->comm) nwd::nccl().CommDestroy(c->comm);
   delete c;
 }
 
@@ -850,6 +868,57 @@ nw_status nw_ctx_kernel_time(nw_ctx* c, int cls, double* total_ms, int64_t* laun
   *launches = (int64_t)c->ev_open[cls].size();
   c->ev_open[cls].clear();
   *total_ms = tot;
+  return NW_OK;
+}
+
+nw_status nw_dist_unique_id(uint8_t* id) {
+  if (!id) return NW_E_INVAL;
+  const nwd::NcclApi& api = nwd::nccl();
+  if (!api.ok) return NW_E_COMM;
+  ncclUniqueId u;
+  if (api.GetUniqueId(&u) != ncclSuccess) return NW_E_COMM;
+  memcpy(id, &u, sizeof u);
+  return NW_OK;
+}
+
+nw_status nw_ctx_set_dist(nw_ctx* c, int32_t rank, int32_t world, const uint8_t* id) {
+  if (!c) return NW_E_INVAL;
+  if (world < 1 || rank < 0 || rank >= world || !id)
+    return fail(c, NW_E_INVAL, "rank %d / world %d / id", rank, world);
+  const nwd::NcclApi& api = nwd::nccl();
+  if (!api.ok) return fail(c, NW_E_COMM, "%s", api.why);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (c->comm) {
+    api.CommDestroy(c->comm);
+    c->comm = nullptr;
+  }
+  ncclUniqueId u;
+  memcpy(&u, id, sizeof u);
+  ncclComm_t comm = nullptr;
+  const ncclResult_t r = api.CommInitRank(&comm, world, u, rank);
+  if (r != ncclSuccess) return fail(c, NW_E_COMM, "ncclCommInitRank: %s", api.GetErrorString(r));
+  c->comm = comm;
+  c->rank = rank;
+  c->world = world;
+  return NW_OK;
+}
+
+nw_status nw_ctx_dist_info(const nw_ctx* c, int32_t* rank, int32_t* world) {
+  if (!c || !rank || !world) return NW_E_INVAL;
+  *rank = c->rank;
+  *world = c->comm ? c->world : 1;
+  return NW_OK;
+}
+
+nw_status nw_batch_partition(const int64_t* offs, int32_t nseq, const int32_t* pairs, int64_t npairs,
+                             int32_t world, int64_t* bounds) {
+  if (!offs || !bounds || nseq < 0 || npairs < 0 || world < 1) return NW_E_INVAL;
+  if (!pairs && npairs != (int64_t)nseq * (nseq - 1) / 2) return NW_E_INVAL;
+  for (int64_t k = 0; pairs && k < 2 * npairs; ++k)
+    if (pairs[k] < 0 || pairs[k] >= nseq) return NW_E_INVAL;
+  nwd::partition_bounds(reinterpret_cast<const long long*>(offs), nseq, pairs, npairs, world,
+                        reinterpret_cast<long long*>(bounds));
   return NW_OK;
 }
 
@@ -1328,10 +1397,16 @@ struct HostLaps {  // NW_OPT_HOST_PROFILE: host-side phase times of one call, to
   }
 };
 
+// Implicit all-pairs on a dist context: this rank's rank-space tasks
+// [tbase, tbase + ntasks), scores written compactly (d_scores[task]).
+struct DistRange { long long tbase, ntasks; };
+
 nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool already_coded,
                      const long long* d_offs, const long long* h_offs, int nseq, const int* d_pairs,
                      const int* h_pairs, long long npairs, const nw_scoring* sc, uint32_t flags,
-                     int* d_scores, const long long* d_ops_off, uint8_t* d_ops, int* d_ops_len) {
+                     int* d_scores, const long long* d_ops_off, uint8_t* d_ops, int* d_ops_len,
+                     const DistRange* dr = nullptr) {
+  const long long ntasks = (dr && !h_pairs) ? dr->ntasks : npairs;
   constexpr int R = 32 * KR_BATCH;
   HostLaps hl(c);
   const bool tbk = (flags & NW_TRACEBACK) != 0;
@@ -1545,7 +1620,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   // no more warps than pairs: the int32 traceback path sizes its per-warp direction
   // scratch (~maxlen^2/4 bytes) per launched warp
   const long long nwarps = std::min<long long>((long long)c->sm_count * ctas_per_sm * warps_per_cta,
-                                               (npairs + warps_per_cta - 1) / warps_per_cta * warps_per_cta);
+                                               (ntasks + warps_per_cta - 1) / warps_per_cta * warps_per_cta);
   const long long bstride = maxlen + 1 + 64;
   // direction scratch per warp, in halfwords: int32 sweep = halfword per (group,
   // row, lane); packed sweep = 32-bit word per (group, packed row, lane)
@@ -1588,7 +1663,11 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   B.tdirs = two_phase ? static_cast<uint32_t*>(c->d_tbdirs) : nullptr;
   B.tdir_off = two_phase ? c->d_tdoff : nullptr;
   B.task0 = 0;
-  B.task1 = npairs;
+  B.task1 = ntasks;
+  if (dr && !h_pairs) {
+    B.tbase = dr->tbase;
+    B.compact = 1;
+  }
   B.X = sc->tie[0];
   B.Y = sc->tie[1];
   B.Z = sc->tie[2];
@@ -1673,6 +1752,111 @@ nw_status batch_check(nw_ctx* c, const long long* h_offs, int nseq, const int* h
   return NW_OK;
 }
 
+#define NCCL_TRY(c, x)                                                                    \
+  do {                                                                                    \
+    ncclResult_t r_ = (x);                                                                \
+    if (r_ != ncclSuccess)                                                                \
+      return fail((c), NW_E_COMM, "%s: %s", #x, nwd::nccl().GetErrorString(r_));          \
+  } while (0)
+
+// nw_align_batch(_dev) on a dist context: every rank passes
+// the same inputs, aligns the cost-balanced contiguous share partition_bounds gives
+// it, and one group of in-place broadcasts (an all-gather of variable-size ranges)
+// leaves every output on every rank. No index travels: the ranges follow from the
+// inputs. Explicit pairs: pair-index ranges, outputs written in place (scores,
+// path lengths, and the ops bytes [ops_off[lo], ops_off[hi])). Implicit all-pairs,
+// score-only: ranges of k_batch's rank space (longest sequences first), scores
+// gathered in rank-space order and scattered to pair order by k_rs_scatter.
+// Implicit with traceback: the lexicographic pairs are materialised (explicit).
+nw_status batch_dist(nw_ctx* c, const uint8_t* d_raw, const long long* d_offs, const long long* h_offs,
+                     int nseq, const int* d_pairs, const int* h_pairs, long long npairs,
+                     const nw_scoring* sc, uint32_t flags, int* d_scores, const long long* d_ops_off,
+                     const long long* h_ops_off, uint8_t* d_ops, int* d_ops_len) {
+  const nwd::NcclApi& api = nwd::nccl();
+  const bool tbk = (flags & NW_TRACEBACK) != 0;
+  // NW_OPT_DIST_VIRTUAL_WORLD / _RANK (test only, no communicator): run one rank's range
+  // of the partition and skip the gather, so G sequential calls on one GPU replay G ranks
+  const bool virt = c->comm == nullptr;
+  const int G = virt ? (int)c->opt[NW_OPT_DIST_VIRTUAL_WORLD] : c->world;
+  const int me = virt ? (int)std::min<long long>(c->opt[NW_OPT_DIST_VIRTUAL_RANK], G - 1) : c->rank;
+  nw_status st = NW_OK;
+  if (!h_pairs && tbk) {  // materialise the lexicographic pairs
+    c->h_pmat.resize(2 * (size_t)npairs);
+    long long k = 0;
+    for (int p = 0; p < nseq; ++p)
+      for (int q = p + 1; q < nseq; ++q, ++k) { c->h_pmat[2 * k] = p; c->h_pmat[2 * k + 1] = q; }
+    st = grow(c, c->d_pmat, c->pmat_cap, sizeof(int) * 2 * (size_t)npairs);
+    if (st) return st;
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_pmat, c->h_pmat.data(), sizeof(int) * 2 * (size_t)npairs,
+                                cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // h_pmat is reused by the next call
+    h_pairs = c->h_pmat.data();
+    d_pairs = c->d_pmat;
+  }
+  std::vector<long long>& bd = c->h_bounds;
+  bd.assign(G + 1, 0);
+  nwd::partition_bounds(h_offs, nseq, h_pairs, npairs, G, bd.data());
+  const long long lo = bd[me], hi = bd[me + 1];
+  if (!h_pairs) {  // implicit, score-only
+    st = grow(c, c->d_rs, c->rs_cap, sizeof(int) * (size_t)std::max(1LL, npairs));
+    if (st) return st;
+    const DistRange dr{lo, hi - lo};
+    if (hi > lo) {
+      st = batch_core(c, d_raw, false, d_offs, h_offs, nseq, nullptr, nullptr, npairs, sc, flags,
+                      c->d_rs + lo, nullptr, nullptr, nullptr, &dr);
+      if (st) return st;
+    } else {  // no tasks here: the permutation k_rs_scatter needs still comes from batch_core
+      std::vector<int> perm;
+      nwd::length_perm(h_offs, nseq, perm);
+      st = grow(c, c->d_aux, c->aux_cap, sizeof(int) * perm.size() + 16);
+      if (st) return st;
+      const StagedCopy cp[1] = {{c->d_aux, perm.data(), sizeof(int) * perm.size()}};
+      st = upload_staged(c, cp, 1);
+      if (st) return st;
+    }
+    if (!virt) NCCL_TRY(c, api.GroupStart());
+    for (int g = 0; g < G && !virt; ++g)
+      if (bd[g + 1] > bd[g])
+        NCCL_TRY(c, api.Broadcast(c->d_rs + bd[g], c->d_rs + bd[g], (size_t)(bd[g + 1] - bd[g]),
+                                  ncclInt32, g, c->comm, c->stream));
+    if (!virt) NCCL_TRY(c, api.GroupEnd());
+    const int blocks = (int)std::min<long long>((npairs + 255) / 256, (long long)c->sm_count * 8);
+    nwk::k_rs_scatter<<<std::max(blocks, 1), 256, 0, c->stream>>>(c->d_rs, npairs, static_cast<const int*>(c->d_aux),
+                                                                  nseq, d_scores);
+    LAUNCHED(c);
+    CUDA_TRY(c, cudaGetLastError());
+    return NW_OK;
+  }
+  if (hi > lo) {
+    st = batch_core(c, d_raw, false, d_offs, h_offs, nseq, d_pairs + 2 * lo, h_pairs + 2 * lo, hi - lo, sc,
+                    flags, d_scores + lo, tbk ? d_ops_off + lo : nullptr, d_ops, tbk ? d_ops_len + lo : nullptr);
+    if (st) return st;
+  }
+  const long long* oo = h_ops_off;
+  if (tbk && !oo) {
+    c->h_oo.resize(npairs + 1);
+    st = nw_batch_ops_offsets(reinterpret_cast<const int64_t*>(h_offs), nseq, h_pairs, npairs,
+                              reinterpret_cast<int64_t*>(c->h_oo.data()));
+    if (st) return fail(c, st, "ops offsets");
+    oo = c->h_oo.data();
+  }
+  if (virt) return NW_OK;
+  NCCL_TRY(c, api.GroupStart());
+  for (int g = 0; g < G; ++g) {
+    const long long a = bd[g], b = bd[g + 1];
+    if (b <= a) continue;
+    NCCL_TRY(c, api.Broadcast(d_scores + a, d_scores + a, (size_t)(b - a), ncclInt32, g, c->comm, c->stream));
+    if (tbk) {
+      NCCL_TRY(c, api.Broadcast(d_ops_len + a, d_ops_len + a, (size_t)(b - a), ncclInt32, g, c->comm, c->stream));
+      if (oo[b] > oo[a])
+        NCCL_TRY(c, api.Broadcast(d_ops + oo[a], d_ops + oo[a], (size_t)(oo[b] - oo[a]), ncclUint8, g, c->comm,
+                                  c->stream));
+    }
+  }
+  NCCL_TRY(c, api.GroupEnd());
+  return NW_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1721,8 +1905,10 @@ nw_status nw_align_batch(nw_ctx* c, const uint8_t* seqs, const int64_t* offs, in
   CUDA_TRY(c, cudaMemcpyAsync(d_offs, offs, b_offs, cudaMemcpyHostToDevice, c->stream));
   if (pairs) CUDA_TRY(c, cudaMemcpyAsync(d_pairs, pairs, b_pairs, cudaMemcpyHostToDevice, c->stream));
   if (tbk) CUDA_TRY(c, cudaMemcpyAsync(d_oo, ops_off, b_oo, cudaMemcpyHostToDevice, c->stream));
-  st = batch_core(c, d_raw, false, d_offs, h_offs, nseq, d_pairs, pairs, npairs, sc, flags, d_scores,
-                  d_oo, d_ops, d_ol);
+  st = (c->comm || c->opt[NW_OPT_DIST_VIRTUAL_WORLD] > 0) ? batch_dist(c, d_raw, d_offs, h_offs, nseq, d_pairs, pairs, npairs, sc, flags, d_scores,
+                            d_oo, reinterpret_cast<const long long*>(ops_off), d_ops, d_ol)
+               : batch_core(c, d_raw, false, d_offs, h_offs, nseq, d_pairs, pairs, npairs, sc, flags, d_scores,
+                            d_oo, d_ops, d_ol);
   if (st) { cudaFreeAsync(d, c->stream); return st; }
   CUDA_TRY(c, cudaMemcpyAsync(scores, d_scores, b_sc, cudaMemcpyDeviceToHost, c->stream));
   if (tbk) {
@@ -1750,6 +1936,10 @@ nw_status nw_align_batch_dev(nw_ctx* c, const uint8_t* d_seqs, const int64_t* d_
   CUDA_TRY(c, cudaSetDevice(c->device));
   st = upload_tables(c, sc);
   if (st) return st;
+  if (c->comm || c->opt[NW_OPT_DIST_VIRTUAL_WORLD] > 0)
+    return batch_dist(c, d_seqs, reinterpret_cast<const long long*>(d_offs), ho, nseq, d_pairs, h_pairs, npairs,
+                      sc, flags, d_scores, reinterpret_cast<const long long*>(d_ops_off), nullptr, d_ops,
+                      d_ops_len);
   return batch_core(c, d_seqs, false, reinterpret_cast<const long long*>(d_offs), ho, nseq, d_pairs,
                     h_pairs, npairs, sc, flags, d_scores, reinterpret_cast<const long long*>(d_ops_off),
                     d_ops, d_ops_len);

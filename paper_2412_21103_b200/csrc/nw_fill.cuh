@@ -85,6 +85,20 @@ struct Tie {
   static constexpr int X = PI / 100, Y = (PI / 10) % 10, Z = PI % 10;
 };
 
+// max through inline PTX: opaque to the LLVM optimiser, which would otherwise fold the
+// prefix-form maxima below back into the serial chain max(c_r, H'(r-1)) (it did:
+// same SASS as the chain form).
+__device__ __forceinline__ int max_opq(int a, int b) {
+  int d;
+  asm("max.s32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ int max3_opq(int a, int b, int c) {
+  int d;
+  asm("max.s32 %0, %1, %2;\n\tmax.s32 %0, %0, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 template <int CODE>
 __device__ __forceinline__ int pick(int cD, int cU, int cL) {
   return CODE == 1 ? cD : (CODE == 2 ? cU : cL);
@@ -191,27 +205,36 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
       static_assert(KR == 2, "shared-memory profile: KR must be 2, 4 or 8");
       pw.x = *reinterpret_cast<const uint16_t*>(C.sprof + bc * R + lane * KR);
     }
+    // Prefix form of the vertical chain: with c_r = max(cD_r, cL_r) (no dependence on the
+    // lane above), H'(r) = max(c_r, H'(r-1)) = max(P_r, up) for P_r = max(c_0..c_r). The
+    // P_r chain runs while the shuffle bringing `up` is in flight; once it lands, every
+    // row is one independent max, so the lane-to-lane critical path per step is
+    // SHFL + SEL + one max instead of SHFL + KR dependent maxima.
+    int S[KR], cD[KR], P[KR];
+#pragma unroll
+    for (int r = 0; r < KR; ++r) {
+      S[r] = cell_score<KR, PROFREG>(st, r, sel, pw);
+      cD[r] = (r == 0 ? st.diag : st.Hl[r - 1]) + S[r];
+      P[r] = (r == 0) ? max_opq(cD[0], st.Hl[0]) : max3_opq(cD[r], st.Hl[r], P[r - 1]);
+    }
     // up = H'(top-1, j): lane 0 from the boundary row (0 for strip 0), others from lane-1
     const int recv = __shfl_up_sync(FULL, st.send, 1);
     const int bval = __shfl_sync(FULL, st.chunk_cur, q);  // strip 0: chunks hold H'(0, j) = 0
     const int up = (lane == 0) ? bval : recv;
-    int hd = st.diag, hu = up;
+    int hu = up;
 #pragma unroll
     for (int r = 0; r < KR; ++r) {
-      const int S = cell_score<KR, PROFREG>(st, r, sel, pw);
-      const int cD = hd + S, cU = hu, cL = st.Hl[r];
-      // the up candidate arrives last (vertical chain): fold diag and left first
-      int h = max(max(cD, cL), cU);
+      int h = max_opq(P[r], up);
       if (DIRS) {
-        const int cX = pick<T::X>(cD, cU, cL);
-        const int cY = pick<T::Y>(cD, cU, cL);
+        const int cU = hu, cL = st.Hl[r];
+        const int cX = pick<T::X>(cD[r], cU, cL);
+        const int cY = pick<T::Y>(cD[r], cU, cL);
         const int dX = cX - h;  // 0 iff X is maximal, else < 0  (bit nbX = sign)
         const int dY = cY - h;  // 0 iff Y is maximal, else < 0  (bit nbY = sign)
         st.acc[r] = __funnelshift_l((uint32_t)dX, st.acc[r], 1);
         st.acc[r] = __funnelshift_l((uint32_t)dY, st.acc[r], 1);
       }
       if (MASKED) h = (j >= 1) ? h : 0;  // border column H'(i, 0) = 0 until the lane starts
-      hd = st.Hl[r];
       hu = h;
       st.Hl[r] = h;
     }

@@ -469,6 +469,11 @@ struct BatchArgs {
   int transposed;          // this fill launch sweeps its pairs transposed (b on the rows;
                            // the kernel's tie order is the mirrored one)
   long long ntr0;          // the walk: tasks >= ntr0 were filled transposed
+  // Distributed all-pairs (nw_ctx_set_dist, implicit mode): this rank's tasks are the
+  // rank-space tasks [tbase + task0, tbase + task1); compact = scores go to scores[task]
+  // (rank-space order, gathered and scattered to pair order by k_rs_scatter).
+  long long tbase = 0;
+  int compact = 0;
 };
 
 // flat rank-space index k -> (p', q'), p' < q', lexicographic over N items
@@ -495,11 +500,11 @@ __device__ __forceinline__ void task_pair(const BatchArgs& B, long long task, in
     q = B.pairs[2 * outk + 1];
   } else {
     int pr, qr;
-    unrank_pair(task, B.nseq, pr, qr);
+    unrank_pair(B.tbase + task, B.nseq, pr, qr);
     const int x = B.perm[pr], y = B.perm[qr];
     p = min(x, y);
     q = max(x, y);
-    outk = (long long)p * B.nseq - (long long)p * (p + 1) / 2 + (q - p - 1);
+    outk = B.compact ? task : (long long)p * B.nseq - (long long)p * (p + 1) / 2 + (q - p - 1);
   }
 }
 
@@ -676,6 +681,22 @@ __device__ __forceinline__ void walk_lanes(const BatchArgs& B, long long task, b
     }
   }
 }
+
+#ifdef NW_COMMON_KERNELS  // one TU
+// Distributed all-pairs: rs[t] holds the score of rank-space task t (every rank's
+// range, gathered); write it to its lexicographic pair index.
+__global__ void k_rs_scatter(const int* __restrict__ rs, long long P, const int* __restrict__ perm,
+                             int N, int* __restrict__ scores) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < P;
+       t += (long long)gridDim.x * blockDim.x) {
+    int pr, qr;
+    unrank_pair(t, N, pr, qr);
+    const int x = perm[pr], y = perm[qr];
+    const int p = min(x, y), q = max(x, y);
+    scores[(long long)p * N - (long long)p * (p + 1) / 2 + (q - p - 1)] = rs[t];
+  }
+}
+#endif
 
 // The walk as its own launch after the fill: one thread per task.
 template <int KR16>

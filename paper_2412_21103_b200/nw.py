@@ -26,7 +26,8 @@ NW_SCORE_ONLY, NW_TRACEBACK = 0, 1
 OPTIONS = {"rows_per_lane": 0, "d16_force": 1, "d16_kr": 2, "no_d16": 3, "tall_kr8": 4,
            "poll_ns": 5, "tb_step": 6, "tb_band": 7, "batch_kr16": 8, "batch_no_transpose": 9,
            "batch_tb_budget": 10, "host_plan": 11, "linear_int32": 12, "cblock_warps_per_sm": 13,
-           "host_profile": 14, "watchdog_polls": 15, "test_withhold": 16}
+           "host_profile": 14, "watchdog_polls": 15, "test_withhold": 16,
+           "dist_virtual_world": 17, "dist_virtual_rank": 18}
 
 
 class NWError(RuntimeError):
@@ -63,6 +64,10 @@ def lib() -> ctypes.CDLL:
         "nw_last_bad_pos": ([vp], i64),
         "nw_ctx_sync": ([vp], ctypes.c_int),
         "nw_ctx_set_option": ([vp, i32, i64], ctypes.c_int),
+        "nw_dist_unique_id": ([vp], ctypes.c_int),
+        "nw_ctx_set_dist": ([vp, i32, i32, vp], ctypes.c_int),
+        "nw_ctx_dist_info": ([vp, P(i32), P(i32)], ctypes.c_int),
+        "nw_batch_partition": ([vp, i32, vp, i64, i32, vp], ctypes.c_int),
         "nw_ctx_get_option": ([vp, i32], i64),
         "nw_ctx_launches": ([vp], i64),
         "nw_ctx_set_timing": ([vp, ctypes.c_int], ctypes.c_int),
@@ -109,7 +114,8 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = ("nw_ctx_create", "nw_ctx_destroy", "nw_strerror", "nw_last_error", "nw_last_bad_pos",
-            "nw_ctx_sync", "nw_ctx_set_option", "nw_ctx_get_option", "nw_ctx_launches", "nw_ctx_set_timing", "nw_ctx_kernel_time", "nw_score_only", "nw_score_only_dev",
+            "nw_ctx_sync", "nw_ctx_set_option", "nw_ctx_get_option",
+            "nw_dist_unique_id", "nw_ctx_set_dist", "nw_ctx_dist_info", "nw_batch_partition", "nw_ctx_launches", "nw_ctx_set_timing", "nw_ctx_kernel_time", "nw_score_only", "nw_score_only_dev",
             "nw_align_pair", "nw_align_pair_dev", "nw_traceback", "nw_traceback_dev",
             "nw_tb_free", "nw_align_batch", "nw_align_batch_dev", "nw_batch_ops_offsets",
             "nw_score_only_cblock", "nw_cblock_recv_bytes", "nw_score_only_cblock_rank_dev",
@@ -189,6 +195,19 @@ class Context:
         """nw_ctx_set_option by name (OPTIONS); 0 restores the default."""
         self._check(lib().nw_ctx_set_option(self._h, OPTIONS[name], int(value)))
 
+    def set_dist(self, rank: int, world: int, uid: bytes):
+        """nw_ctx_set_dist: join the `world`-rank NCCL communicator named by uid
+        (from nw_dist_unique_id on rank 0). Collective."""
+        if len(uid) != 128:
+            raise ValueError("uid must be 128 bytes")
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        self._check(lib().nw_ctx_set_dist(self._h, int(rank), int(world), buf))
+
+    def dist_info(self) -> tuple[int, int]:
+        r, w = ctypes.c_int32(), ctypes.c_int32()
+        self._check(lib().nw_ctx_dist_info(self._h, ctypes.byref(r), ctypes.byref(w)))
+        return r.value, w.value
+
     def get_option(self, name: str) -> int:
         return int(lib().nw_ctx_get_option(self._h, OPTIONS[name]))
 
@@ -238,6 +257,31 @@ class Traceback:
             self.free()
         except Exception:
             pass
+
+
+def nw_dist_unique_id() -> bytes:
+    """128-byte NCCL id for Context.set_dist (no GPU needed)."""
+    buf = ctypes.create_string_buffer(128)
+    st = lib().nw_dist_unique_id(buf)
+    if st != NW_OK:
+        raise NWError(st, "nw_dist_unique_id: NCCL unavailable")
+    return buf.raw
+
+
+def nw_batch_partition(offs, pairs, world: int) -> np.ndarray:
+    """bounds[0..world] of the dist batch partition (see include/nw.h)."""
+    offs = np.ascontiguousarray(offs, dtype=np.int64)
+    nseq = len(offs) - 1
+    if pairs is None:
+        npairs = nseq * (nseq - 1) // 2
+    else:
+        pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+        npairs = len(pairs)
+    out = np.zeros(world + 1, dtype=np.int64)
+    st = lib().nw_batch_partition(offs.ctypes.data, nseq, _ptr(pairs), npairs, world, out.ctypes.data)
+    if st != NW_OK:
+        raise NWError(st, "nw_batch_partition")
+    return out
 
 
 def nw_score_only(ctx: Context, a, b, sc) -> int:

@@ -12,7 +12,7 @@ n = 20000
 res = {}
 krs = [int(k) for k in os.environ.get("NW_EXP_KR", "2,4,8").split(",")]
 for kr in krs:
-    os.environ["NW_KR"] = str(kr)
+    ctx.set_option("rows_per_lane", kr)
     R = 32 * kr
     for S in [int(x) for x in os.environ.get("NW_EXP_S", "1,2,4,16,64,148").split(",")]:
         m = R * S

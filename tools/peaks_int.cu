@@ -30,13 +30,15 @@
 #define OP_vibmax_u16x2    { bool p_, q_; a = __vibmax_u16x2(a, b, &p_, &q_); c ^= (p_ ? 1u : 0u); }
 #define OP_vadd2           a = __vadd2(a, b)
 #define OP_iadd3           a = a + b + c
-#define OP_lop3            a = (a & b) ^ c
+// volatile PTX: a plain (a & b) ^ c chain was folded across statements (round 1 reported
+// an impossible 453 lane-ops/clk/SM, above the 128 issue limit)
+#define OP_lop3            asm volatile("lop3.b32 %0, %0, %1, %2, 0x6a;" : "+r"(a) : "r"(b), "r"(c))
 #define OP_prmt            a = __byte_perm(a, b, c)
 #define OP_shf             a = __funnelshift_r(a, b, c)
 #define OP_imad            a = a * b + c
 #define OP_shfl            a = __shfl_xor_sync(0xffffffffu, a, 1) + b
 #define OP_mix_viaddmax_imad   a = __viaddmax_s32(a, b, c); a = a * b + c
-#define OP_mix_viaddmax_lop3   a = __viaddmax_s32(a, b, c); a = (a & b) ^ c
+#define OP_mix_viaddmax_lop3   a = __viaddmax_s32(a, b, c); asm volatile("lop3.b32 %0, %0, %1, %2, 0x6a;" : "+r"(a) : "r"(b), "r"(c))
 #define OP_mix_viaddmax_prmt   a = __viaddmax_s32(a, b, c); a = __byte_perm(a, b, c)
 #define OP_mix_u16x2_imad      a = __viaddmax_u16x2(a, b, c); a = a * b + c
 
