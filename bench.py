@@ -453,8 +453,9 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     ctx = nwb.Context(local, stream.cuda_stream)
     wl = args.workload
-    sharded = wl in ("c3", "c4") and world > 1
+    sharded = wl in ("c3", "c4", "c5") and world > 1
     if sharded:  # the library's own NCCL communicator (nw_ctx_set_dist), id shared by rank 0
+        # (C3/C4: pair ranges + gather; C5: the column-block pipeline across the GPUs)
         from paper_2412_21103_b200 import dist as nwdist
         nwdist.init_dist_context(ctx)
     if wl in ("c1", "c2", "c5", "c1p", "c2p", "c5tb", "c1co", "c2co"):
@@ -503,7 +504,9 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    if sharded or wl in ("c3", "c4"):
+    if wl == "c5" and sharded:
+        cells_all = W.cells          # one pair, its column blocks pipelined across the ranks
+    elif sharded or wl in ("c3", "c4"):
         cells_all = W.total_cells    # one batch split over the ranks, gathered on every rank
     else:
         cells_all = W.cells * world  # replicas: every rank aligns its own pair / set
@@ -581,14 +584,17 @@ def run_ours(args):
     out = {
         "metric": "GCUPS (cell updates/s)", "value": value, "unit": "GCUPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong" if wl in ("c3", "c4") else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if (wl in ("c3", "c4") or (wl == "c5" and sharded)) else "weak",
+        "vs_baseline": None,
         # arithmetic of the fill kernel in use: int32 strips, or two 16-bit cells per register
         "dtype": "int32" if wl in ("c1", "c2", "c1p", "c2p", "c5tb", "c1co", "c2co") else "u16x2",
         **({"msa": {"center": W.center, "width": W.width}} if wl == "msa" else {}),
         "data": "synthetic (nwgen seeded, SURVEY.md §8(d) recipe)",
         "config": {"workload": WORKLOADS[wl], "cells_per_step": cells_all,
                    "parallelism": (f"pairs-sharded{world} (cost-balanced ranges, NCCL in-place broadcasts)"
-                                   if wl in ("c3", "c4") else f"replicas{world}"),
+                                   if wl in ("c3", "c4") else
+                                   f"column-blocks{world} (peer-memory pipeline, CUDA IPC + NVLink)"
+                                   if (wl == "c5" and sharded) else f"replicas{world}"),
                    "l2": "flushed between steps (256 MB write)"},
         "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roofline,
     }

@@ -183,30 +183,45 @@ nw_status nw_ctx_dist_info(const nw_ctx *ctx, int32_t *rank, int32_t *world);
 nw_status nw_batch_partition(const int64_t *offs, int32_t nseq, const int32_t *pairs,
                              int64_t npairs, int32_t world, int64_t *bounds);
 
-/* ---- column-block wavefront (giant pair across ranks, SURVEY.md §8 a10) ----
- * Score-only H(m,n) computed as the multi-GPU pipeline computes it: columns cut
- * into blocks of block_cols (0 = automatic), block b owned by rank b % ranks,
- * strips handed down within a rank and each strip's right boundary column handed
- * to the next rank as tagged 64-bit entries. Here all `ranks` are virtual ranks
- * on this context's device (one launch, all warps resident); the result equals
- * nw_score_only's. Host pointers, synchronous. DNA-size alphabets (K <= 4). */
+/* ---- column-block wavefront (giant pair across ranks, SURVEY.md §8 a10; P:197) ----
+ * Score-only H(m,n) computed as the multi-GPU pipeline computes it: rows in strips,
+ * columns cut into blocks of block_cols (0 = automatic), block b owned by rank b % ranks,
+ * strips handed down within a rank and each strip's right boundary column handed to the
+ * next rank as tagged 64-bit entries. DNA-size alphabets (K <= 4).
+ * With s - 2g >= 0 for every symbol pair the packed difference form runs (U crosses
+ * the block edge, V the strip edge; nw_fill_d16.cuh), else int32 H'. Every call tags
+ * its entries afresh (a per-context counter), so receive buffers are zeroed once, when
+ * allocated, and never between calls; every rank must make the same sequence of
+ * column-block calls on its context.
+ * nw_score_only_cblock: all `ranks` are virtual ranks on this context's device (one
+ *   launch, all warps resident); the result equals nw_score_only's. Host pointers,
+ *   synchronous.
+ * On a dist context (nw_ctx_set_dist) with world > 1, nw_score_only / nw_score_only_dev
+ *   of a pair of >= 2^34 cells run this pipeline across the ranks' GPUs (receive buffers
+ *   exchanged once through CUDA IPC, entries stored over NVLink with .sys scope), and one
+ *   all-reduce gives every rank H(m,n) (NW_OPT_DIST_PIPELINE overrides the rule). */
 nw_status nw_score_only_cblock(nw_ctx *ctx, const uint8_t *a, int64_t m, const uint8_t *b,
                                int64_t n, const nw_scoring *sc, int32_t ranks,
                                int32_t block_cols, int64_t *score);
 
-/* One real rank of the same pipeline (one process per GPU). recv_self: this rank's
- * receive buffer of nw_cblock_recv_bytes(m) bytes, device memory the previous rank
- * can write (e.g. a symmetric-memory / CUDA-IPC peer mapping); recv_next: the next
- * rank's receive buffer as mapped on this device. Every rank's recv_self must be
- * zeroed, and that zeroing complete on all ranks, before any rank calls this.
- * d_a, d_b, d_score device pointers; async on ctx's stream. *d_score receives
- * H(m,n) on the rank owning the last column block and 0 elsewhere (sum across
- * ranks = the score). */
+/* One real rank of the same pipeline (one process per GPU), for callers that manage the
+ * peer memory themselves. recv_self: this rank's receive buffer of nw_cblock_recv_bytes(m)
+ * bytes, device memory the previous rank can write (a CUDA-IPC / symmetric-memory
+ * mapping), zeroed on every rank before the first call; recv_next: the next rank's
+ * receive buffer as mapped here. recv_self = NULL uses the buffers of
+ * nw_cblock_ipc_export / nw_cblock_ipc_import (NW_E_STATE if there are none).
+ * d_a, d_b, d_score device pointers; async on ctx's stream. *d_score receives H(m,n) on
+ * the rank owning the last column block and 0 elsewhere (sum across ranks = the score). */
 int64_t nw_cblock_recv_bytes(int64_t m);
 nw_status nw_score_only_cblock_rank_dev(nw_ctx *ctx, const uint8_t *d_a, int64_t m,
                                         const uint8_t *d_b, int64_t n, const nw_scoring *sc,
                                         int32_t rank, int32_t ranks, int32_t block_cols,
                                         void *recv_self, void *recv_next, int64_t *d_score);
+/* CUDA IPC plumbing for the rank entry point: export allocates (once, zeroed) this
+ * context's receive buffer for m rows and returns its 64-byte cudaIpcMemHandle; import
+ * opens the next rank's handle (kept until replaced or the context is destroyed). */
+nw_status nw_cblock_ipc_export(nw_ctx *ctx, int64_t m, uint8_t handle[64]);
+nw_status nw_cblock_ipc_import(nw_ctx *ctx, const uint8_t handle[64]);
 
 /* ---- center-star multiple alignment ----
  * The paper's use of the batch path: scores of all n(n-1)/2 pairs (Eq. 2), the
@@ -311,7 +326,9 @@ enum {
                                      rank DIST_VIRTUAL_RANK's range of a world of this size and
                                      gather nothing (G sequential calls replay G ranks on one GPU) */
   NW_OPT_DIST_VIRTUAL_RANK = 18,
-  NW_OPT_COUNT_ = 19
+  NW_OPT_DIST_PIPELINE = 19,  /* dist ctx score-only pairs: 0 = column-block pipeline across the
+                                 ranks when world > 1 and m*n >= 2^34; 1 = always; 2 = never */
+  NW_OPT_COUNT_ = 20
 };
 nw_status nw_ctx_set_option(nw_ctx *ctx, int32_t option, int64_t value);
 /* Current value, or -1 for a NULL ctx / unknown option. */

@@ -88,6 +88,17 @@ struct nw_ctx {
   size_t pmat_cap = 0;
   std::vector<long long> h_bounds, h_oo;
   std::vector<int> h_pmat;
+  // column-block pipeline (a10): per-call tags, buffers zeroed once (nw_cblock.cuh)
+  unsigned cb_tag_next = 1;
+  void* d_cb_ring = nullptr;    // [ranks here][2][n + 66] tagged top/bottom rows
+  size_t cb_ring_cap = 0;
+  void* d_cb_recv = nullptr;    // this rank's receive buffer (cudaMalloc: IPC-exportable)
+  size_t cb_recv_cap = 0;
+  void* cb_next = nullptr;      // the next rank's receive buffer, IPC-opened
+  void* d_cb_vrecv = nullptr;   // virtual ranks' receive buffers
+  size_t cb_vrecv_cap = 0;
+  void* d_cb_tab = nullptr;     // receive-buffer pointer table
+  size_t cb_tab_cap = 0;
   // live handles: nw_ctx_destroy releases their device memory and detaches them, so
   // a handle freed after its context only deletes its host struct
   std::vector<nw_tb*> live_tb;
@@ -140,6 +151,13 @@ nw_status fail(nw_ctx* c, nw_status st, const char* fmt, ...) {
       return fail((c), e_ == cudaErrorMemoryAllocation ? NW_E_NOMEM : NW_E_CUDA,          \
                   "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__);      \
     }                                                                                     \
+  } while (0)
+
+#define NCCL_TRY(c, x)                                                                    \
+  do {                                                                                    \
+    ncclResult_t r_ = (x);                                                                \
+    if (r_ != ncclSuccess)                                                                \
+      return fail((c), NW_E_COMM, "%s: %s", #x, nwd::nccl().GetErrorString(r_));          \
   } while (0)
 
 #define LAUNCHED(c) ((c)->launches++)
@@ -471,6 +489,10 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
                     unsigned long long* ckpt = nullptr, int ck_every = 0, long long ck_stride = 0,
                     const unsigned long long* top_row = nullptr, unsigned top_tag = 0);
 
+bool cblock_dist_applies(const nw_ctx* c, long long m, long long n, const nw_scoring* sc);
+nw_status cblock_dist(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b, long long n,
+                      const nw_scoring* sc, bool host, long long* d_score);
+
 }  // namespace
 
 // ---- kernels for tiny bookkeeping ----
@@ -688,6 +710,16 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
   st = check_bounds(c, sc, m, n);
   if (st) return st;
   CUDA_TRY(c, cudaSetDevice(c->device));
+  if (!want_dirs && cblock_dist_applies(c, m, n, sc)) {  // C5 across the ranks of a dist ctx
+    long long* d_score = host ? c->d_score : score_out;
+    st = cblock_dist(c, a, m, b, n, sc, host, d_score);
+    if (st) return st;
+    if (host) {
+      CUDA_TRY(c, cudaMemcpyAsync(score_out, c->d_score, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+      return check_deferred(c);
+    }
+    return NW_OK;
+  }
   st = upload_tables(c, sc);
   if (st) return st;
   // workspace: padded code buffers and the tagged 2-slot boundary ring
@@ -833,6 +865,12 @@ void nw_ctx_destroy(nw_ctx* c) {
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->d_tbdirs) cudaFreeAsync(c->d_tbdirs, c->stream);
   if (c->d_rs) cudaFreeAsync(c->d_rs, c->stream);
+  if (c->d_cb_tab) cudaFreeAsync(c->d_cb_tab, c->stream);
+  cudaStreamSynchronize(c->stream);
+  if (c->cb_next) cudaIpcCloseMemHandle(c->cb_next);
+  if (c->d_cb_ring) cudaFree(c->d_cb_ring);
+  if (c->d_cb_recv) cudaFree(c->d_cb_recv);
+  if (c->d_cb_vrecv) cudaFree(c->d_cb_vrecv);
   if (c->d_pmat) cudaFreeAsync(c->d_pmat, c->stream);
   if (c->d_tdoff) cudaFreeAsync(c->d_tdoff, c->stream);
   cudaStreamSynchronize(c->stream);
@@ -1083,65 +1121,135 @@ nw_status nw_traceback_dev(nw_ctx* c, const nw_tb* tb, uint8_t* d_ops, int64_t c
 
 namespace {
 
-constexpr int CB_KR = 8, CB_R = 32 * CB_KR;
+// ---- column-block wavefront (a10) ----
+// Geometry of one column-block call: arithmetic form, strip height, blocks, messages.
+struct CbGeom {
+  bool d16;             // packed difference form (s - 2g >= 0), else int32 H'
+  int KR, R, S, W, nblocks;
+  long long mstride;    // entries per left-column message: R (d16) or R + 1 (int32)
+  long long rstride;    // entries per receive slot: S * mstride
+  size_t recv_bytes;    // one rank's receive buffer: 2 slots
+};
 
-long long cblock_strips(long long m) { return std::max<long long>((m + CB_R - 1) / CB_R, 1); }
+constexpr int CB_KR32 = 8;
 
-// Shared body of the column-block entry points: ranks [rank0, rank0 + nhere) run
-// in this launch; recv_tab (device, G entries) points at every rank's receive
-// buffer (virtual ranks: all local; a real rank: its own and the next rank's).
+// Receive-buffer bound for any form and strip height (m rows in strips of >= 256 rows,
+// <= R + 1 entries per strip, two slots).
+long long cb_recv_bound(long long m) { return 16LL * (m + m / 256 + 1 + 1025); }
+
+CbGeom cb_geom(const nw_ctx* c, long long m, long long n, const nw_scoring* sc, int G, int block_cols) {
+  CbGeom g;
+  g.d16 = d16_ok(c, sc);
+  g.KR = g.d16 ? d16_kr(c, std::max(m, 1LL)) : CB_KR32;
+  g.R = 32 * g.KR;
+  g.S = (int)std::max<long long>((m + g.R - 1) / g.R, 1);
+  if (block_cols > 0) g.W = block_cols;
+  else if (G == 1) g.W = (int)std::max<long long>(n, 1);
+  else g.W = (int)std::max<long long>(1024, (n + 32LL * G - 1) / (32LL * G));  // ~32 rounds
+  g.nblocks = (int)std::max<long long>((n + g.W - 1) / g.W, 1);
+  g.mstride = g.d16 ? g.R : g.R + 1;
+  g.rstride = (long long)g.S * g.mstride;
+  g.recv_bytes = sizeof(unsigned long long) * 2 * (size_t)g.rstride;
+  return g;
+}
+
+// Buffers the column-block kernels poll carry per-call tags (nw_cblock.cuh): they are
+// zeroed once, when allocated. cudaMalloc (not the stream pool): the receive buffer of
+// a real rank is exported through CUDA IPC.
+nw_status grow_zeroed(nw_ctx* c, void*& p, size_t& cap, size_t need) {
+  if (need <= cap && p) return NW_OK;
+  if (p) {
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  const size_t bytes = std::max<size_t>(need, 256);
+  CUDA_TRY(c, cudaMalloc(&p, bytes));
+  CUDA_TRY(c, cudaMemsetAsync(p, 0, bytes, c->stream));
+  cap = bytes;
+  return NW_OK;
+}
+
+// Tags of one call: [base, base + nblocks*S + 1). A per-context counter, identical on
+// every rank that makes the same sequence of calls; wrapping (after ~2^32 / (nblocks*S)
+// calls) re-zeroes this context's buffers (rank callers must then re-synchronise).
+unsigned cb_tags(nw_ctx* c, const CbGeom& g, bool* wrapped) {
+  const unsigned long long span = (unsigned long long)g.nblocks * g.S + 2;
+  *wrapped = (unsigned long long)c->cb_tag_next + span >= 0xffffffffull;
+  if (*wrapped) c->cb_tag_next = 1;
+  const unsigned base = c->cb_tag_next;
+  c->cb_tag_next += (unsigned)span;
+  return base;
+}
+
+// Shared body: ranks [rank0, rank0 + nhere) run in this launch; recv_tab (device, G
+// entries) points at every rank's receive buffer (virtual ranks: all local; a real rank:
+// its own and the next rank's). d_score receives this launch's H(m,n) share.
 nw_status cblock_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb, long long n,
-                      const nw_scoring* sc, int G, int W, int rank0, int nhere,
-                      unsigned long long* const* recv_tab, long long* d_score, bool owner_adds_gap) {
-  const long long S = cblock_strips(m);
-  const long long nblocks = std::max<long long>((n + W - 1) / W, 1);
+                      const nw_scoring* sc, const CbGeom& g, int G, int rank0, int nhere,
+                      unsigned long long* const* recv_tab, long long* d_score, bool owner_adds_gap,
+                      bool sys, unsigned tag_base) {
   const long long bstride = bnd_stride(n);
-  const size_t b_bnd = sizeof(unsigned long long) * (size_t)nhere * 2 * bstride;
-  void* ring = nullptr;
-  CUDA_TRY(c, cudaMallocAsync(&ring, b_bnd + 16, c->stream));
-  ZeroRanges zr{{ring, nullptr, nullptr, nullptr}, {(long long)((b_bnd + 15) & ~size_t(15)), 0, 0, 0}};
-  nw_status st = init_small(c, 4 + nhere, zr);
-  if (st) { cudaFreeAsync(ring, c->stream); return st; }
-  const int last_owner = (int)((nblocks - 1) % G);
+  nw_status st = grow_zeroed(c, c->d_cb_ring, c->cb_ring_cap, sizeof(unsigned long long) * (size_t)nhere * 2 * bstride);
+  if (st) return st;
+  st = init_small(c, 4 + nhere);  // [2] hm, [4..] tickets
+  if (st) return st;
+  const int last_owner = (g.nblocks - 1) % G;
   if (m > 0 && n > 0) {
     CBlockArgs A;
     A.a = ca; A.b = cb; A.prof = c->d_prof; A.K = sc->K; A.m = (int)m; A.n = (int)n;
-    A.W = W; A.G = G; A.S = (int)S; A.nblocks = (int)nblocks;
-    A.bnd = static_cast<unsigned long long*>(ring);
+    A.W = g.W; A.G = G; A.S = g.S; A.nblocks = g.nblocks;
+    A.bnd = static_cast<unsigned long long*>(c->d_cb_ring);
     A.bstride = bstride;
     A.recv_tab = recv_tab;
-    A.rstride = S * (CB_R + 1);
+    A.rstride = g.rstride;
+    A.mstride = g.mstride;
+    A.tag_base = tag_base;
     A.ticket = c->d_ints + 4;
     A.hm = c->d_ints + 2;
     A.err = c->d_err;
+    A.watchdog = c->opt[NW_OPT_WATCHDOG_POLLS] > 0 ? c->opt[NW_OPT_WATCHDOG_POLLS] : (1LL << 28);
     A.rank0 = rank0;
     A.nranks_here = nhere;
     // every rank's warps must be resident together (they wait on each other);
-    // NW_CBLOCK_WARPS_PER_SM caps this launch's share of the GPU
+    // NW_OPT_CBLOCK_WARPS_PER_SM caps this launch's share of the GPU
     int per_sm = 8;
-    if (c->opt[NW_OPT_CBLOCK_WARPS_PER_SM] > 0) per_sm = (int)std::min(c->opt[NW_OPT_CBLOCK_WARPS_PER_SM], 64LL);
-    const int grid = (int)std::min<long long>((long long)c->sm_count * per_sm, S * nhere);
+    if (c->opt[NW_OPT_CBLOCK_WARPS_PER_SM] > 0) per_sm = (int)std::min(c->opt[NW_OPT_CBLOCK_WARPS_PER_SM], 16LL);
+    const long long want = (long long)g.S * nhere;
+    const int grid = (int)std::min<long long>((long long)c->sm_count * per_sm, want);
     const int grid_r = std::max(nhere, grid - grid % nhere);
     {
       KernelTimer kt(c, 0);
-      k_fill_cblock<CB_KR><<<grid_r, 32, 0, c->stream>>>(A);
+      if (g.d16) {
+        switch (g.KR) {
+#define NW_CB_CASE(K)                                                                 \
+  case K:                                                                             \
+    if (sys) k_fill_cblock_d16<K, true><<<grid_r, 32, 0, c->stream>>>(A);            \
+    else k_fill_cblock_d16<K, false><<<grid_r, 32, 0, c->stream>>>(A);               \
+    break;
+          NW_CB_CASE(16) NW_CB_CASE(18) NW_CB_CASE(20) NW_CB_CASE(22) NW_CB_CASE(24)
+          NW_CB_CASE(26) NW_CB_CASE(28) NW_CB_CASE(30) NW_CB_CASE(32)
+#undef NW_CB_CASE
+          default: return fail(c, NW_E_INVAL, "column-block rows per lane %d", g.KR);
+        }
+      } else if (sys) {
+        k_fill_cblock<CB_KR32, true><<<grid_r, 32, 0, c->stream>>>(A);
+      } else {
+        k_fill_cblock<CB_KR32, false><<<grid_r, 32, 0, c->stream>>>(A);
+      }
     }
     LAUNCHED(c);
     CUDA_TRY(c, cudaGetLastError());
   }
   const bool owner = rank0 <= last_owner && last_owner < rank0 + nhere;
   // the owner of the last block reports H(m,n); other real ranks report 0
-  const long long gmn = owner || !owner_adds_gap ? (long long)sc->gap * (m + n) : 0;
+  const bool here = owner || !owner_adds_gap;
+  const long long gmn = here ? (long long)sc->gap * (m + n) : 0;
   k_finish_score<<<1, 1, 0, c->stream>>>(c->d_ints + 2, gmn, d_score, (m == 0 || n == 0) ? 1 : 0);
   LAUNCHED(c);
-  cudaFreeAsync(ring, c->stream);
   CUDA_TRY(c, cudaGetLastError());
   return NW_OK;
-}
-
-int cblock_width(long long n, int G, int block_cols) {
-  if (block_cols > 0) return block_cols;
-  return (int)std::max<long long>(256, (n + 4LL * G - 1) / (4LL * G));
 }
 
 nw_status cblock_check(nw_ctx* c, long long m, long long n, const nw_scoring* sc, int G) {
@@ -1151,7 +1259,129 @@ nw_status cblock_check(nw_ctx* c, long long m, long long n, const nw_scoring* sc
   if (st) return st;
   if (sc->K > 4) return fail(c, NW_E_INVAL, "column-block path supports K <= 4");
   if (G < 1 || G > 64) return fail(c, NW_E_INVAL, "ranks %d outside [1,64]", G);
-  if (cblock_strips(m) >= (1 << 20)) return fail(c, NW_E_OVERFLOW, "too many strips for the tags");
+  return NW_OK;
+}
+
+// Codes of a (device or host) pair into the context's padded code buffers.
+nw_status cb_stage(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b, long long n, bool host,
+                   const nw_scoring* sc, uint8_t** ca, uint8_t** cbp) {
+  nw_status st = upload_tables(c, sc);
+  if (st) return st;
+  const long long la = pad16(PAD + m + R_MAX + PAD), lb = pad16(PAD + n + R_MAX + PAD);
+  st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
+  if (st) return st;
+  CUDA_TRY(c, cudaMemsetAsync(c->d_codes, 0, (size_t)(la + lb), c->stream));
+  return stage_pair(c, a, m, b, n, host, ca, cbp);
+}
+
+// This rank's share of the pipeline on a real rank (own receive buffer + the next
+// rank's, peer-mapped): async on ctx's stream.
+nw_status cblock_rank(nw_ctx* c, const uint8_t* d_a, long long m, const uint8_t* d_b, long long n,
+                      const nw_scoring* sc, int rank, int ranks, int block_cols, void* recv_self,
+                      void* recv_next, long long* d_score) {
+  const CbGeom g = cb_geom(c, m, n, sc, ranks, block_cols);
+  if (g.recv_bytes > (size_t)cb_recv_bound(m)) return fail(c, NW_E_INVAL, "receive buffer bound");
+  uint8_t *ca, *cb;
+  nw_status st = cb_stage(c, d_a, m, d_b, n, false, sc, &ca, &cb);
+  if (st) return st;
+  std::vector<unsigned long long*> tab(ranks, nullptr);
+  tab[rank] = static_cast<unsigned long long*>(recv_self);
+  tab[(rank + 1) % ranks] = static_cast<unsigned long long*>(ranks > 1 ? recv_next : recv_self);
+  st = grow(c, c->d_cb_tab, c->cb_tab_cap, sizeof(void*) * (size_t)ranks);
+  if (st) return st;
+  const StagedCopy cp[1] = {{c->d_cb_tab, tab.data(), sizeof(void*) * (size_t)ranks}};
+  st = upload_staged(c, cp, 1);
+  if (st) return st;
+  bool wrapped = false;
+  const unsigned base = cb_tags(c, g, &wrapped);
+  if (wrapped) {
+    CUDA_TRY(c, cudaMemsetAsync(recv_self, 0, g.recv_bytes, c->stream));
+    if (c->d_cb_ring) CUDA_TRY(c, cudaMemsetAsync(c->d_cb_ring, 0, c->cb_ring_cap, c->stream));
+  }
+  return cblock_core(c, ca, m, cb, n, sc, g, ranks, rank, 1,
+                     static_cast<unsigned long long* const*>(c->d_cb_tab), d_score, true, ranks > 1, base);
+}
+
+// Dist ctx: the receive buffer is allocated (zeroed) once per size and its CUDA IPC
+// handle all-gathered over the communicator; the next rank's buffer is opened once.
+nw_status cblock_dist_buffers(nw_ctx* c, size_t need) {
+  if (need <= c->cb_recv_cap && c->d_cb_recv && (c->world == 1 || c->cb_next)) return NW_OK;
+  const nwd::NcclApi& api = nwd::nccl();
+  nw_status st = grow_zeroed(c, c->d_cb_recv, c->cb_recv_cap, need);
+  if (st) return st;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (c->cb_next) {
+    cudaIpcCloseMemHandle(c->cb_next);
+    c->cb_next = nullptr;
+  }
+  if (c->world == 1) return NW_OK;
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(c, cudaIpcGetMemHandle(&h, c->d_cb_recv));
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  char* d = nullptr;
+  CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&d), hb * (size_t)(c->world + 1), c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(d + hb * c->world, &h, hb, cudaMemcpyHostToDevice, c->stream));
+  const ncclResult_t r = api.AllGather(d + hb * c->world, d, hb, ncclUint8, c->comm, c->stream);
+  if (r != ncclSuccess) {
+    cudaFreeAsync(d, c->stream);
+    return fail(c, NW_E_COMM, "handle all-gather: %s", api.GetErrorString(r));
+  }
+  std::vector<cudaIpcMemHandle_t> all(c->world);
+  CUDA_TRY(c, cudaMemcpyAsync(all.data(), d, hb * (size_t)c->world, cudaMemcpyDeviceToHost, c->stream));
+  cudaFreeAsync(d, c->stream);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  CUDA_TRY(c, cudaIpcOpenMemHandle(&c->cb_next, all[(c->rank + 1) % c->world],
+                                   cudaIpcMemLazyEnablePeerAccess));
+  // every rank's buffer is zero before any rank's kernel can write into it
+  long long* one = nullptr;
+  CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&one), sizeof(long long), c->stream));
+  const ncclResult_t r2 = api.AllReduce(one, one, 1, ncclInt64, ncclSum, c->comm, c->stream);
+  cudaFreeAsync(one, c->stream);
+  if (r2 != ncclSuccess) return fail(c, NW_E_COMM, "barrier: %s", api.GetErrorString(r2));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return NW_OK;
+}
+
+// Score-only pairs on a dist ctx take the pipeline when there are several ranks (or
+// NW_OPT_DIST_PIPELINE = 1) and the pair is large (>= 2^34 cells; DNA-size alphabets).
+bool cblock_dist_applies(const nw_ctx* c, long long m, long long n, const nw_scoring* sc) {
+  if (!c->comm || sc->K > 4 || m <= 0 || n <= 0) return false;
+  const long long mode = c->opt[NW_OPT_DIST_PIPELINE];
+  if (mode == 2) return false;
+  if (mode == 1) return true;
+  return c->world > 1 && (double)m * (double)n >= 17179869184.0;
+}
+
+// nw_score_only(_dev) on a dist ctx with world > 1: the C5 pipeline across the ranks,
+// then one all-reduce (sum of the owner's H(m,n) and everyone else's 0).
+nw_status cblock_dist(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b, long long n,
+                      const nw_scoring* sc, bool host, long long* d_score) {
+  const CbGeom g = cb_geom(c, m, n, sc, c->world, 0);
+  nw_status st = cblock_dist_buffers(c, (size_t)cb_recv_bound(m));
+  if (st) return st;
+  uint8_t *ca, *cb;
+  st = cb_stage(c, a, m, b, n, host, sc, &ca, &cb);
+  if (st) return st;
+  const int G = c->world;
+  std::vector<unsigned long long*> tab(G, nullptr);
+  tab[(c->rank + 1) % G] = static_cast<unsigned long long*>(c->cb_next);
+  tab[c->rank] = static_cast<unsigned long long*>(c->d_cb_recv);  // (G = 1: the same entry)
+  st = grow(c, c->d_cb_tab, c->cb_tab_cap, sizeof(void*) * (size_t)G);
+  if (st) return st;
+  const StagedCopy cp[1] = {{c->d_cb_tab, tab.data(), sizeof(void*) * (size_t)G}};
+  st = upload_staged(c, cp, 1);
+  if (st) return st;
+  bool wrapped = false;
+  const unsigned base = cb_tags(c, g, &wrapped);
+  if (wrapped) {  // re-zero every rank's buffers, then a barrier (rare: ~2^32 tags)
+    CUDA_TRY(c, cudaMemsetAsync(c->d_cb_recv, 0, c->cb_recv_cap, c->stream));
+    if (c->d_cb_ring) CUDA_TRY(c, cudaMemsetAsync(c->d_cb_ring, 0, c->cb_ring_cap, c->stream));
+    NCCL_TRY(c, nwd::nccl().AllReduce(d_score, d_score, 1, ncclInt64, ncclMax, c->comm, c->stream));
+  }
+  st = cblock_core(c, ca, m, cb, n, sc, g, G, c->rank, 1, static_cast<unsigned long long* const*>(c->d_cb_tab),
+                   d_score, true, true, base);
+  if (st) return st;
+  NCCL_TRY(c, nwd::nccl().AllReduce(d_score, d_score, 1, ncclInt64, ncclSum, c->comm, c->stream));
   return NW_OK;
 }
 
@@ -1159,9 +1389,7 @@ nw_status cblock_check(nw_ctx* c, long long m, long long n, const nw_scoring* sc
 
 extern "C" {
 
-int64_t nw_cblock_recv_bytes(int64_t m) {
-  return (int64_t)sizeof(unsigned long long) * 2 * cblock_strips(m) * (CB_R + 1);
-}
+int64_t nw_cblock_recv_bytes(int64_t m) { return cb_recv_bound(m); }
 
 nw_status nw_score_only_cblock(nw_ctx* c, const uint8_t* a, int64_t m, const uint8_t* b,
                                int64_t n, const nw_scoring* sc, int32_t ranks,
@@ -1171,32 +1399,32 @@ nw_status nw_score_only_cblock(nw_ctx* c, const uint8_t* a, int64_t m, const uin
   nw_status st = cblock_check(c, m, n, sc, ranks);
   if (st) return st;
   CUDA_TRY(c, cudaSetDevice(c->device));
-  st = upload_tables(c, sc);
+  const CbGeom g = cb_geom(c, m, n, sc, ranks, block_cols);
+  uint8_t *ca, *cb;
+  st = cb_stage(c, a, m, b, n, true, sc, &ca, &cb);
   if (st) return st;
-  const long long la = pad16(PAD + m + R_MAX + PAD), lb = pad16(PAD + n + R_MAX + PAD);
-  st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
+  // virtual ranks: all receive buffers in one kept allocation (zeroed once) + the table
+  const size_t per = (g.recv_bytes + 255) & ~size_t(255);
+  st = grow_zeroed(c, c->d_cb_vrecv, c->cb_vrecv_cap, per * (size_t)ranks);
   if (st) return st;
-  // virtual ranks: all receive buffers + the pointer table in one allocation
-  const size_t b_recv = (size_t)ranks * (size_t)nw_cblock_recv_bytes(m);
-  const size_t b_tab = sizeof(void*) * (size_t)ranks;
-  char* buf = nullptr;
-  CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&buf), b_recv + b_tab + 16, c->stream));
   std::vector<unsigned long long*> tab(ranks);
   for (int r = 0; r < ranks; ++r)
-    tab[r] = reinterpret_cast<unsigned long long*>(buf + (size_t)r * nw_cblock_recv_bytes(m));
-  CUDA_TRY(c, cudaMemcpyAsync(buf + b_recv, tab.data(), b_tab, cudaMemcpyHostToDevice, c->stream));
-  ZeroRanges zr{{c->d_codes, buf, nullptr, nullptr}, {la + lb, (long long)((b_recv + 15) & ~size_t(15)), 0, 0}};
-  st = init_small(c, 4, zr);
-  if (st) { cudaFreeAsync(buf, c->stream); return st; }
-  uint8_t *ca, *cb;
-  st = stage_pair(c, a, m, b, n, true, &ca, &cb);
-  if (st) { cudaFreeAsync(buf, c->stream); return st; }
-  st = cblock_core(c, ca, m, cb, n, sc, ranks, cblock_width(n, ranks, block_cols), 0, ranks,
-                   reinterpret_cast<unsigned long long* const*>(buf + b_recv), c->d_score, false);
-  if (st) { cudaFreeAsync(buf, c->stream); return st; }
-  CUDA_TRY(c, cudaMemcpyAsync(score, c->d_score, sizeof(long long), cudaMemcpyDeviceToHost,
-                              c->stream));
-  cudaFreeAsync(buf, c->stream);
+    tab[r] = reinterpret_cast<unsigned long long*>(static_cast<char*>(c->d_cb_vrecv) + (size_t)r * per);
+  st = grow(c, c->d_cb_tab, c->cb_tab_cap, sizeof(void*) * (size_t)ranks);
+  if (st) return st;
+  const StagedCopy cp[1] = {{c->d_cb_tab, tab.data(), sizeof(void*) * (size_t)ranks}};
+  st = upload_staged(c, cp, 1);
+  if (st) return st;
+  bool wrapped = false;
+  const unsigned base = cb_tags(c, g, &wrapped);
+  if (wrapped) {
+    CUDA_TRY(c, cudaMemsetAsync(c->d_cb_vrecv, 0, c->cb_vrecv_cap, c->stream));
+    if (c->d_cb_ring) CUDA_TRY(c, cudaMemsetAsync(c->d_cb_ring, 0, c->cb_ring_cap, c->stream));
+  }
+  st = cblock_core(c, ca, m, cb, n, sc, g, ranks, 0, ranks, static_cast<unsigned long long* const*>(c->d_cb_tab),
+                   c->d_score, false, false, base);
+  if (st) return st;
+  CUDA_TRY(c, cudaMemcpyAsync(score, c->d_score, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   return check_deferred(c);
 }
 
@@ -1205,35 +1433,45 @@ nw_status nw_score_only_cblock_rank_dev(nw_ctx* c, const uint8_t* d_a, int64_t m
                                         int32_t rank, int32_t ranks, int32_t block_cols,
                                         void* recv_self, void* recv_next, int64_t* d_score) {
   if (!c) return NW_E_INVAL;
-  if ((m > 0 && !d_a) || (n > 0 && !d_b) || !d_score || !recv_self || (ranks > 1 && !recv_next))
+  if (!recv_self) {  // the buffers of nw_cblock_ipc_export / nw_cblock_ipc_import
+    recv_self = c->d_cb_recv;
+    recv_next = c->cb_next;
+    if (!recv_self || (size_t)nw_cblock_recv_bytes(m) > c->cb_recv_cap || (ranks > 1 && !recv_next))
+      return fail(c, NW_E_STATE, "no exported/imported receive buffers for m=%lld", (long long)m);
+  }
+  if ((m > 0 && !d_a) || (n > 0 && !d_b) || !d_score || (ranks > 1 && !recv_next))
     return fail(c, NW_E_INVAL, "NULL argument");
   nw_status st = cblock_check(c, m, n, sc, ranks);
   if (st) return st;
   if (rank < 0 || rank >= ranks) return fail(c, NW_E_INVAL, "rank %d outside [0,%d)", rank, ranks);
   CUDA_TRY(c, cudaSetDevice(c->device));
-  st = upload_tables(c, sc);
+  return cblock_rank(c, d_a, m, d_b, n, sc, rank, ranks, block_cols, recv_self, recv_next,
+                     reinterpret_cast<long long*>(d_score));
+}
+
+nw_status nw_cblock_ipc_export(nw_ctx* c, int64_t m, uint8_t* handle) {
+  if (!c || !handle || m < 0) return c ? fail(c, NW_E_INVAL, "NULL argument") : NW_E_INVAL;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  nw_status st = grow_zeroed(c, c->d_cb_recv, c->cb_recv_cap, (size_t)nw_cblock_recv_bytes(m));
   if (st) return st;
-  const long long la = pad16(PAD + m + R_MAX + PAD), lb = pad16(PAD + n + R_MAX + PAD);
-  st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
-  if (st) return st;
-  // pointer table: own and next rank's receive buffers (the rest are never read)
-  std::vector<unsigned long long*> tab(ranks, nullptr);
-  tab[rank] = static_cast<unsigned long long*>(recv_self);
-  tab[(rank + 1) % ranks] = static_cast<unsigned long long*>(ranks > 1 ? recv_next : recv_self);
-  unsigned long long** d_tab = nullptr;
-  CUDA_TRY(c, cudaMallocAsync(reinterpret_cast<void**>(&d_tab), sizeof(void*) * ranks, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(d_tab, tab.data(), sizeof(void*) * ranks, cudaMemcpyHostToDevice,
-                              c->stream));
-  ZeroRanges zr{{c->d_codes, nullptr, nullptr, nullptr}, {la + lb, 0, 0, 0}};
-  st = init_small(c, 4, zr);
-  if (st) { cudaFreeAsync(d_tab, c->stream); return st; }
-  uint8_t *ca, *cb;
-  st = stage_pair(c, d_a, m, d_b, n, false, &ca, &cb);
-  if (st) { cudaFreeAsync(d_tab, c->stream); return st; }
-  st = cblock_core(c, ca, m, cb, n, sc, ranks, cblock_width(n, ranks, block_cols), rank, 1,
-                   d_tab, reinterpret_cast<long long*>(d_score), true);
-  cudaFreeAsync(d_tab, c->stream);
-  return st;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(c, cudaIpcGetMemHandle(&h, c->d_cb_recv));
+  memcpy(handle, &h, sizeof h);
+  return NW_OK;
+}
+
+nw_status nw_cblock_ipc_import(nw_ctx* c, const uint8_t* handle) {
+  if (!c || !handle) return c ? fail(c, NW_E_INVAL, "NULL argument") : NW_E_INVAL;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (c->cb_next) {
+    cudaIpcCloseMemHandle(c->cb_next);
+    c->cb_next = nullptr;
+  }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  CUDA_TRY(c, cudaIpcOpenMemHandle(&c->cb_next, h, cudaIpcMemLazyEnablePeerAccess));
+  return NW_OK;
 }
 
 nw_status nw_batch_ops_offsets(const int64_t* h_offs, int32_t nseq, const int32_t* h_pairs,
@@ -1752,12 +1990,6 @@ nw_status batch_check(nw_ctx* c, const long long* h_offs, int nseq, const int* h
   return NW_OK;
 }
 
-#define NCCL_TRY(c, x)                                                                    \
-  do {                                                                                    \
-    ncclResult_t r_ = (x);                                                                \
-    if (r_ != ncclSuccess)                                                                \
-      return fail((c), NW_E_COMM, "%s: %s", #x, nwd::nccl().GetErrorString(r_));          \
-  } while (0)
 
 // nw_align_batch(_dev) on a dist context: every rank passes
 // the same inputs, aligns the cost-balanced contiguous share partition_bounds gives

@@ -123,6 +123,7 @@ struct StripCtx {
   const int8_t* sprof;              // shared profile [K][R] (not PROFREG)
   const void* bnd_in;               // boundary row read (strip s-1's bottom), null for s == 0
   unsigned tag_in;                  // tag the bnd_in entries carry (strip s-1 wrote s)
+  unsigned tag_out;                 // tag this sweep writes (column-block sweeps; others use s+1)
   void* bnd_out;                    // boundary row written (this strip's bottom)
   uint16_t* dir_base;               // this lane's decision-bit halfwords
   int* err;

@@ -27,7 +27,8 @@ OPTIONS = {"rows_per_lane": 0, "d16_force": 1, "d16_kr": 2, "no_d16": 3, "tall_k
            "poll_ns": 5, "tb_step": 6, "tb_band": 7, "batch_kr16": 8, "batch_no_transpose": 9,
            "batch_tb_budget": 10, "host_plan": 11, "linear_int32": 12, "cblock_warps_per_sm": 13,
            "host_profile": 14, "watchdog_polls": 15, "test_withhold": 16,
-           "dist_virtual_world": 17, "dist_virtual_rank": 18}
+           "dist_virtual_world": 17, "dist_virtual_rank": 18,
+           "dist_pipeline": 19}
 
 
 class NWError(RuntimeError):
@@ -89,6 +90,8 @@ def lib() -> ctypes.CDLL:
         "nw_cblock_recv_bytes": ([i64], i64),
         "nw_score_only_cblock_rank_dev": ([vp, vp, i64, vp, i64, P(_Scoring), i32, i32, i32, vp,
                                            vp, vp], ctypes.c_int),
+        "nw_cblock_ipc_export": ([vp, i64, vp], ctypes.c_int),
+        "nw_cblock_ipc_import": ([vp, vp], ctypes.c_int),
         "nw_msa_center_star": ([vp, vp, vp, i32, P(_Scoring), P(vp)], ctypes.c_int),
         "nw_msa_center_star_dev": ([vp, vp, vp, vp, i32, P(_Scoring), P(vp)], ctypes.c_int),
         "nw_msa_info": ([vp, P(i32), P(i64)], ctypes.c_int),
@@ -119,6 +122,7 @@ EXPORTED = ("nw_ctx_create", "nw_ctx_destroy", "nw_strerror", "nw_last_error", "
             "nw_align_pair", "nw_align_pair_dev", "nw_traceback", "nw_traceback_dev",
             "nw_tb_free", "nw_align_batch", "nw_align_batch_dev", "nw_batch_ops_offsets",
             "nw_score_only_cblock", "nw_cblock_recv_bytes", "nw_score_only_cblock_rank_dev",
+            "nw_cblock_ipc_export", "nw_cblock_ipc_import",
             "nw_msa_center_star", "nw_msa_center_star_dev", "nw_msa_info", "nw_msa_rows",
             "nw_msa_rows_dev", "nw_msa_free", "nw_align_pair_percell", "nw_align_pair_percell_dev",
             "nw_align_pair_linear", "nw_cooptimal")
@@ -422,14 +426,27 @@ def nw_cblock_recv_bytes(m: int) -> int:
     return int(lib().nw_cblock_recv_bytes(m))
 
 
+def nw_cblock_ipc_export(ctx: Context, m: int) -> bytes:
+    """Allocate this context's receive buffer for m rows; its 64-byte CUDA IPC handle."""
+    buf = ctypes.create_string_buffer(64)
+    ctx._check(lib().nw_cblock_ipc_export(ctx.handle, int(m), buf))
+    return buf.raw
+
+
+def nw_cblock_ipc_import(ctx: Context, handle: bytes) -> None:
+    """Open the next rank's receive buffer (its nw_cblock_ipc_export handle)."""
+    ctx._check(lib().nw_cblock_ipc_import(ctx.handle, ctypes.create_string_buffer(bytes(handle), 64)))
+
+
 def nw_score_only_cblock_rank_dev(ctx: Context, d_a, d_b, sc, rank: int, ranks: int,
                                   block_cols: int, recv_self, recv_next, d_score) -> None:
-    """One rank of the column-block pipeline (see include/nw.h). Async."""
+    """One rank of the column-block pipeline (see include/nw.h). recv_self = None: the
+    context's exported/imported IPC buffers. Async."""
     s, keep = _scoring(sc)
     nxt = None if recv_next is None else _ptr(recv_next)
     ctx._check(lib().nw_score_only_cblock_rank_dev(ctx.handle, _ptr(d_a), d_a.numel(), _ptr(d_b),
                                                    d_b.numel(), ctypes.byref(s), rank, ranks,
-                                                   block_cols, _ptr(recv_self), nxt,
+                                                   block_cols, None if recv_self is None else _ptr(recv_self), nxt,
                                                    _ptr(d_score)))
 
 

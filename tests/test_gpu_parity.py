@@ -281,12 +281,20 @@ def test_score_only_prefix_and_closed_forms_c5(ctx):
 
 # ---------------------------------------------------------------- column blocks (a10)
 
-@pytest.mark.parametrize("m,n", [(1, 1), (300, 500), (1000, 5000), (3000, 700), (513, 2049)])
-@pytest.mark.parametrize("ranks,w", [(1, 0), (2, 64), (3, 1000), (8, 0), (5, 257)])
-def test_cblock_virtual_ranks(ctx, m, n, ranks, w):
-    """Column-block wavefront across virtual ranks == oracle score (SURVEY §8(e) C5 path)."""
+CB_SCORINGS = {"d16": nwgen.PAPER_DNA,                                  # difference form
+               "d16b": nwgen.Scoring(match=2, mismatch=-1, gap=-3),
+               "int32": nwgen.Scoring(match=2, mismatch=-4, gap=-1)}     # s - 2g < 0: int32 H'
+
+
+@pytest.mark.parametrize("form", sorted(CB_SCORINGS))
+@pytest.mark.parametrize("m,n", [(1, 1), (300, 500), (1000, 5000), (3000, 700), (513, 2049), (2000, 7)])
+@pytest.mark.parametrize("ranks,w", [(1, 0), (2, 64), (3, 1000), (8, 0), (5, 257), (4, 1)])
+def test_cblock_virtual_ranks(ctx, form, m, n, ranks, w):
+    """Column-block wavefront across virtual ranks == oracle score (SURVEY §8(e) C5 path),
+    both arithmetic forms, blocks down to one column, many calls on one context (the
+    per-call tags of nw_cblock.cuh: buffers are never re-zeroed between calls)."""
     a, b = _pair(7000 + m + n, m, n)
-    sc = nwgen.PAPER_DNA
+    sc = CB_SCORINGS[form]
     assert nwb.nw_score_only_cblock(ctx, a, b, sc, ranks, w) == oracle.score(a, b, sc)
 
 
@@ -346,6 +354,15 @@ def test_cblock_rank_api_concurrent_streams(ctx, opts, G, w):
     bufs = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(G)]
     parts = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(G)]
     torch.cuda.synchronize()
+    for r in range(G):
+        nwb.nw_score_only_cblock_rank_dev(ctxs[r], da, db, sc, r, G, w, bufs[r], bufs[(r + 1) % G],
+                                          parts[r])
+    for c in ctxs:
+        c.sync()
+    assert sum(int(p.item()) for p in parts) == oracle.score(a, b, sc)
+    # a second round on the same contexts and buffers (fresh tags, no re-zeroing)
+    for p in parts:
+        p.zero_()
     for r in range(G):
         nwb.nw_score_only_cblock_rank_dev(ctxs[r], da, db, sc, r, G, w, bufs[r], bufs[(r + 1) % G],
                                           parts[r])
