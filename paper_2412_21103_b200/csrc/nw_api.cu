@@ -57,6 +57,8 @@ struct nw_ctx {
   size_t rev_cap = 0;
   long long* d_len = nullptr;   // traceback length
   long long* d_score = nullptr; // score staging
+  uint16_t* d_sel16 = nullptr;  // batch: selector table of the packed sweeps (FillArgs::sel)
+  size_t sel16_cap = 0;
   void* d_scratch = nullptr;    // batch per-warp scratch
   size_t scratch_cap = 0;
   void* d_aux = nullptr;        // batch perm/order/offs/pairs staging
@@ -339,21 +341,29 @@ void launch_score(const FillArgs& A, bool profreg, int grid, size_t smem, cudaSt
 }
 
 bool dispatch_fill(bool dirs, int pi, int kr, bool profreg, const FillArgs& A, int grid,
-                   size_t smem, cudaStream_t st, bool d16 = false) {
+                   size_t smem, cudaStream_t st, bool d16 = false, bool two_chains = false) {
+  if (!dirs && d16 && two_chains && kr % 4 == 0 && kr >= 16) {  // two chains per lane
+    if (kr == 28) launch_fill_t<28, false, true, 123, 2>(A, grid, smem, st);
+    else if (kr == 32) launch_fill_t<32, false, true, 123, 2>(A, grid, smem, st);
+    else if (kr == 24) launch_fill_t<24, false, true, 123, 2>(A, grid, smem, st);
+    else if (kr == 20) launch_fill_t<20, false, true, 123, 2>(A, grid, smem, st);
+    else launch_fill_t<16, false, true, 123, 2>(A, grid, smem, st);
+    return true;
+  }
   if (!dirs && d16) {  // packed difference form, KR rows per lane (2 per register)
-    if (kr == 32) launch_fill_t<32, false, true, 123, true>(A, grid, smem, st);
-    else if (kr == 30) launch_fill_t<30, false, true, 123, true>(A, grid, smem, st);
-    else if (kr == 28) launch_fill_t<28, false, true, 123, true>(A, grid, smem, st);
-    else if (kr == 26) launch_fill_t<26, false, true, 123, true>(A, grid, smem, st);
-    else if (kr == 24) launch_fill_t<24, false, true, 123, true>(A, grid, smem, st);
-    else if (kr == 22) launch_fill_t<22, false, true, 123, true>(A, grid, smem, st);
-    else if (kr == 20) launch_fill_t<20, false, true, 123, true>(A, grid, smem, st);
-    else if (kr == 18) launch_fill_t<18, false, true, 123, true>(A, grid, smem, st);
-    else if (kr == 14) launch_fill_t<14, false, true, 123, true>(A, grid, smem, st);
-    else if (kr == 12) launch_fill_t<12, false, true, 123, true>(A, grid, smem, st);
-    else if (kr == 16) launch_fill_t<16, false, true, 123, true>(A, grid, smem, st);
-    else if (kr == 8) launch_fill_t<8, false, true, 123, true>(A, grid, smem, st);
-    else launch_fill_t<4, false, true, 123, true>(A, grid, smem, st);
+    if (kr == 32) launch_fill_t<32, false, true, 123, 1>(A, grid, smem, st);
+    else if (kr == 30) launch_fill_t<30, false, true, 123, 1>(A, grid, smem, st);
+    else if (kr == 28) launch_fill_t<28, false, true, 123, 1>(A, grid, smem, st);
+    else if (kr == 26) launch_fill_t<26, false, true, 123, 1>(A, grid, smem, st);
+    else if (kr == 24) launch_fill_t<24, false, true, 123, 1>(A, grid, smem, st);
+    else if (kr == 22) launch_fill_t<22, false, true, 123, 1>(A, grid, smem, st);
+    else if (kr == 20) launch_fill_t<20, false, true, 123, 1>(A, grid, smem, st);
+    else if (kr == 18) launch_fill_t<18, false, true, 123, 1>(A, grid, smem, st);
+    else if (kr == 14) launch_fill_t<14, false, true, 123, 1>(A, grid, smem, st);
+    else if (kr == 12) launch_fill_t<12, false, true, 123, 1>(A, grid, smem, st);
+    else if (kr == 16) launch_fill_t<16, false, true, 123, 1>(A, grid, smem, st);
+    else if (kr == 8) launch_fill_t<8, false, true, 123, 1>(A, grid, smem, st);
+    else launch_fill_t<4, false, true, 123, 1>(A, grid, smem, st);
     return true;
   }
   if (!dirs) {
@@ -596,7 +606,8 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     bool ok;
     {
       KernelTimer kt(c, 0);
-      ok = dispatch_fill(dirs, pi, kr, profreg, A, grid, smem, c->stream, d16);
+      ok = dispatch_fill(dirs, pi, kr, profreg, A, grid, smem, c->stream, d16,
+                         c->opt[NW_OPT_D16_CHAINS] != 1 && !ckpt);
     }
     if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
     LAUNCHED(c);
@@ -859,6 +870,7 @@ void nw_ctx_destroy(nw_ctx* c) {
   if (c->d_bnd) cudaFreeAsync(c->d_bnd, c->stream);
   if (c->d_rev) cudaFreeAsync(c->d_rev, c->stream);
   if (c->d_scratch) cudaFreeAsync(c->d_scratch, c->stream);
+  if (c->d_sel16) cudaFreeAsync(c->d_sel16, c->stream);
   if (c->d_aux) cudaFreeAsync(c->d_aux, c->stream);
   if (c->d_plan) cudaFreeAsync(c->d_plan, c->stream);
   if (c->stage_ev) { cudaEventSynchronize(c->stage_ev); cudaEventDestroy(c->stage_ev); }
@@ -1664,6 +1676,14 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   uint8_t* codes = c->d_codes + PAD;
   (void)already_coded;
   launch_encode(c, d_codes_raw_or_codes, total, codes, 0);
+  // selector table of the packed DNA sweeps (FillArgs::sel), aligned with the codes
+  st = grow(c, c->d_sel16, c->sel16_cap, sizeof(uint16_t) * (size_t)lc);
+  if (st) return st;
+  {
+    const int blocks = (int)std::min<long long>((lc - 1 + 255) / 256, (long long)c->sm_count * 8);
+    k_sel16<<<std::max(blocks, 1), 256, 0, c->stream>>>(c->d_codes + 1, lc - 1, c->d_sel16 + 1);
+    LAUNCHED(c);
+  }
   hl.lap("bounds, memset, encode");
   // order: implicit all-pairs -> perm of sequences by length (descending);
   // explicit pairs -> LPT order by m*n (descending), bucketed.
@@ -1885,6 +1905,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   B.ticket = c->d_ints;
   B.err = c->d_err;
   B.scores = d_scores;
+  B.sel16 = c->d_sel16 + PAD;
   char* base = static_cast<char*>(c->d_scratch);
   B.wbnd = reinterpret_cast<int*>(base);
   B.bstride = bstride;

@@ -32,7 +32,7 @@
 namespace nwk {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int PAD = 64;  // code buffers carry PAD readable bytes before and after
+constexpr int PAD = 128;  // code buffers carry PAD readable bytes before and after (lane skews up to 4 x 31)
 
 struct FillArgs {
   const uint8_t* a;    // row codes, a[-PAD .. m+PAD) readable
@@ -56,6 +56,8 @@ struct FillArgs {
   const unsigned long long* top_row;  // tagged H' of the row above strip 0 (null: zeros),
   unsigned top_tag;                   //   tagged top_tag (the checkpoint writer's s+1)
   unsigned poll_ns = 0;               // back-off between re-polls of a boundary chunk (0: spin)
+  const uint16_t* sel = nullptr;      // packed sweeps (batch): selector table aligned with b, sel[i] =
+                                      //   (17 b[i] + 128) | (17 b[i-1] + 196) << 8 (prmt2 of PA/PB)
   long long watchdog = 1LL << 28;     // re-polls of a late boundary chunk before *err is raised
   int withhold = 0;                   // test only (NW_OPT_TEST_WITHHOLD): strip withhold-1 writes its
   void* sink = nullptr;               //   bottom row to `sink` instead, so its consumer never sees it

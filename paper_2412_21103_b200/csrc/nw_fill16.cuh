@@ -31,7 +31,6 @@ __device__ __forceinline__ uint32_t prmt2(uint32_t x, uint32_t y, uint32_t sel) 
 struct U16State {
   uint32_t up0_prev;  // up(0) of the previous step (diag of packed 0)
   uint32_t send;      // packed h-1 (its high half = this lane's bottom row at jB)
-  uint32_t xT_prev;   // 17 * b code at the previous step's jT (this step's jB)
   int chunk;          // boundary values, lane q holds column t0+1+q
 };
 
@@ -44,18 +43,17 @@ __device__ __forceinline__ void u16_block(U16State& st, uint32_t (&PA)[KR / 2],
                                           int hm_lane, int hm_k, int hm_hi, int hm_t) {
   constexpr int H = KR / 2;
   const int n = A.n;
-  const uint8_t* bp = A.b + (t0 - 2 * lane);  // b code at jT - 1 for step t0
+  // s' selector of step t: nibbles (bT, bT|8, 4+bB, 12+bB) -> byte bT of PA zero-extended
+  // into the low half, byte bB of PB into the high half (s' >= 0: sign replication =
+  // 0x00); (c | (c|8)<<4) = 17c + 128 and (4+c | (12+c)<<4) = 17c + 196 for c < 4. Read
+  // from the host-built table A.sel (one 16-bit load per step, no ALU work): entry
+  // jT - 1 holds (17 b[jT-1] + 128) | (17 b[jT-2] + 196) << 8, bB = b at column jT - 1.
+  const uint16_t* sp16 = A.sel + (t0 - 2 * lane);
   int* op = bnd_out + (t0 - 62);             // lane 31's bottom row column jB = t - 62
 #pragma unroll 8
   for (int q = 0; q < 32; ++q) {
     const int t = t0 + q;
-    const uint32_t bT = bp[q];
-    // s' selector: nibbles (bT, bT|8, 4+bB, 12+bB) -> byte bT of PA zero-extended into
-    // the low half, byte bB of PB into the high half (s' >= 0: sign replication = 0x00);
-    // (c | (c|8)<<4) = 17c + 128 and (4+c | (12+c)<<4) = 17c + 196 for c < 4
-    const uint32_t xT = bT * 17u;
-    const uint32_t sel = xT + (st.xT_prev << 8) + (128u + (196u << 8));
-    st.xT_prev = xT;
+    const uint32_t sel = __ldg(sp16 + q);
     const int recv = __shfl_up_sync(FULL, (int)st.send, 1);
     const int bval = __shfl_sync(FULL, st.chunk, q);
     // up(0): low = lane l-1's bottom row at jT (its packed h-1 high half),
@@ -74,7 +72,10 @@ __device__ __forceinline__ void u16_block(U16State& st, uint32_t (&PA)[KR / 2],
     for (int k = 0; k < H; ++k) {
       const uint32_t sp = prmt2(PA[k], PB[k], sel);
       const uint32_t left = Hp[k];
-      uint32_t h = __vmaxu2(__viaddmax_u16x2(diag, sp, left), up);
+      // diag + s' as a plain 32-bit add (both halves < 2^16 - max s': no carry crosses),
+      // which ptxas may issue on the FMA pipe, then one 3-input max on the ALU pipe:
+      // 4 ALU-pipe cycles per two cells instead of 5 (PRMT 2 + VIADDMNMX 2 + VIMNMX 1)
+      uint32_t h = __vimax3_u16x2(diag + sp, left, up);
       if (MASKED) h &= mask;  // border column H'(i, 0) = 0 until each half starts
       diag = left;
       up = h;
@@ -133,7 +134,6 @@ __device__ __forceinline__ void strip_sweep_u16(const FillArgs& A, int s, int la
   U16State st;
   st.up0_prev = 0;
   st.send = 0;
-  st.xT_prev = 0;
   st.chunk = 0;
   // boundary values H'(top-1, jT) for lane 0's columns t0+1 .. t0+32 (lane q: t0+1+q),
   // fetched one block ahead; strip 0's top row is H'(0, j) = 0

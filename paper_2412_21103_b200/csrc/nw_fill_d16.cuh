@@ -176,4 +176,180 @@ __device__ __forceinline__ void strip_sweep_d16(const FillArgs& A, int s, int la
   __syncwarp();
 }
 
+// ---------------------------------------------------------------------------
+// Two independent chains per lane (score-only, KR % 4 == 0). The sweep above runs
+// one dependent chain through the lane's KR/2 packed registers per step (one
+// VIMNMX3.U16x2 + one IADD per link): on C5 (KR 28: 14 links of ~10 cycles) a
+// warp's step is bound by that chain, not by issue (ncu: 'wait' 44%, issue 48%).
+// Here the lane's rows form four groups of Q = KR/4 rows, G0..G3 top to bottom,
+// held in two register sets, each column-skewed so that within a step the two
+// sets only read values the other produced in the previous step:
+//   set A: low half = G0 rows at column jT,     high half = G2 rows at column jT-2
+//   set B: low half = G1 rows at column jT-1,   high half = G3 rows at column jT-3
+// so A's G2 half takes its top input (G1's bottom row at jT-2) and B takes G0's
+// and G2's bottom rows (at jT-1, jT-3) from the previous step, and each step runs
+// two chains of Q links that interleave. Lanes are skewed by 4 steps (lane l-1's
+// G3 bottom row reaches column jT one step before lane l's G0 needs it). Same
+// recurrence and arithmetic as d16_group, cell by cell.
+template <int KR>
+struct D16x2State {
+  uint32_t UA[KR / 4], UB[KR / 4];    // U_left of the packed rows of sets A and B
+  uint32_t PA0[KR / 4], PA2[KR / 4];  // profile words of G0 / G2 rows (set A low / high)
+  uint32_t PB1[KR / 4], PB3[KR / 4];  // profile words of G1 / G3 rows (set B low / high)
+  uint32_t vlastA, vlastB;            // V of each set's last packed row, previous step
+  uint32_t x1, x2, x3;                // 17 * code at columns jT-1, jT-2, jT-3
+  uint32_t bc_nxt;
+  int chunk_cur, chunk_nxt;
+  int usum;
+};
+
+template <int KR, bool MULTIWARP, bool MASKED>
+__device__ __forceinline__ void d16x2_group(D16x2State<KR>& st, const StripCtx& C, int t0,
+                                            const int (&rows)[4]) {
+  constexpr int Q = KR / 4;
+  const int lane = C.lane, n = C.n;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int t = t0 + q;
+    const int jT = t - 4 * lane + 1;
+    const uint32_t x0 = st.bc_nxt * 17u;
+    st.bc_nxt = __ldg(C.b + jT);  // next step's code (padding covers [-127, n + 127])
+    constexpr uint32_t CS = 128u + (196u << 8);
+    const uint32_t selA = x0 + (st.x2 << 8) + CS;     // low: code at jT, high: at jT-2
+    const uint32_t selB = st.x1 + (st.x3 << 8) + CS;  // low: at jT-1,  high: at jT-3
+    st.x3 = st.x2;
+    st.x2 = st.x1;
+    st.x1 = x0;
+    const int recv = __shfl_up_sync(FULL, (int)st.vlastB, 1);
+    const int bval = __shfl_sync(FULL, st.chunk_cur, q);
+    // A: low = lane above's G3 bottom row at jT (boundary row for lane 0), high = own
+    // G1 bottom row at jT-2 (set B's low half, previous step). B: G0 / G2 bottom rows.
+    const uint32_t upsrc = (lane == 0) ? ((uint32_t)bval << 16) : (uint32_t)recv;
+    uint32_t vA = prmt2(upsrc, st.vlastB, 0x5432u);
+    uint32_t vB = st.vlastA;
+    uint32_t mA = 0xffffffffu, mB = 0xffffffffu;
+    if (MASKED) {
+      mA = (jT >= 1 ? 0x0000ffffu : 0u) | (jT >= 3 ? 0xffff0000u : 0u);
+      mB = (jT >= 2 ? 0x0000ffffu : 0u) | (jT >= 4 ? 0xffff0000u : 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+      const uint32_t spA = prmt2(st.PA0[k], st.PA2[k], selA);
+      const uint32_t spB = prmt2(st.PB1[k], st.PB3[k], selB);
+      const uint32_t ulA = st.UA[k], ulB = st.UB[k];
+      const uint32_t zA = __vimax3_u16x2(spA, vA, ulA);
+      const uint32_t zB = __vimax3_u16x2(spB, vB, ulB);
+      uint32_t uA = zA - vA, uB = zB - vB;  // per half Z - V_up >= 0: no borrow across halves
+      if (MASKED) { uA &= mA; uB &= mB; }
+      vA = zA - ulA;
+      vB = zB - ulB;
+      st.UA[k] = uA;
+      st.UB[k] = uB;
+    }
+    st.vlastA = vA;
+    st.vlastB = vB;
+    const int jb = jT - 3;  // bottom row (G3) column
+    if (lane == 31 && (!MASKED || (jb >= 1 && jb <= n))) {
+      const int vb = (int)(vB >> 16);
+      if (MULTIWARP) {
+        unsigned long long v;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "r"(vb), "r"(C.s + 1));
+        st_relaxed_u64(static_cast<unsigned long long*>(C.bnd_out) + (t0 - 126) + q, v);
+      } else {
+        static_cast<int*>(C.bnd_out)[(t0 - 126) + q] = vb;
+      }
+    }
+    if (MASKED) {  // H(m,n) = g(m+n) + sum_i U(i,n): each group's U at column n
+      if (jT == n) {
+#pragma unroll
+        for (int k = 0; k < Q; ++k) if (k < rows[0]) st.usum += (int)(st.UA[k] & 0xffffu);
+      }
+      if (jT - 1 == n) {
+#pragma unroll
+        for (int k = 0; k < Q; ++k) if (k < rows[1]) st.usum += (int)(st.UB[k] & 0xffffu);
+      }
+      if (jT - 2 == n) {
+#pragma unroll
+        for (int k = 0; k < Q; ++k) if (k < rows[2]) st.usum += (int)(st.UA[k] >> 16);
+      }
+      if (jT - 3 == n) {
+#pragma unroll
+        for (int k = 0; k < Q; ++k) if (k < rows[3]) st.usum += (int)(st.UB[k] >> 16);
+      }
+    }
+  }
+}
+
+template <int KR, bool MULTIWARP>
+__device__ __forceinline__ void strip_sweep_d16x2(const FillArgs& A, int s, int lane) {
+  static_assert(KR % 4 == 0 && KR <= 32, "KR must be a multiple of 4");
+  constexpr int Q = KR / 4;
+  constexpr int R = 32 * KR;
+  const int n = A.n;
+  const int ia0 = s * R + lane * KR;
+  D16x2State<KR> st;
+  auto word = [&](int row) {
+    const int ac = A.a[row];
+    uint32_t w = 0;
+    for (int c = 0; c < A.K; ++c) w |= ((uint32_t)(uint8_t)A.prof[ac * A.K + c]) << (8 * c);
+    return w;
+  };
+#pragma unroll
+  for (int k = 0; k < Q; ++k) {
+    st.PA0[k] = word(ia0 + k);
+    st.PB1[k] = word(ia0 + Q + k);
+    st.PA2[k] = word(ia0 + 2 * Q + k);
+    st.PB3[k] = word(ia0 + 3 * Q + k);
+    st.UA[k] = 0;
+    st.UB[k] = 0;
+  }
+  int rows[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) rows[g] = max(0, min(Q, A.m - ia0 - g * Q));
+  st.vlastA = st.vlastB = 0;
+  st.x1 = st.x2 = st.x3 = 0;
+  st.usum = 0;
+  st.chunk_cur = st.chunk_nxt = 0;
+  st.bc_nxt = __ldg(A.b - 4 * lane);  // code at jT - 1 for step 0
+  StripCtx C;
+  C.tag_in = (unsigned)s;
+  C.b = A.b;
+  C.sprof = nullptr;
+  const size_t esz = MULTIWARP ? 8 : 4;
+  char* bnd = static_cast<char*>(A.bnd);
+  C.bnd_in = (s > 0) ? bnd + esz * (size_t)((s % A.nslots) * A.bstride) : nullptr;
+  C.bnd_out = bnd + esz * (size_t)(((s + 1) % A.nslots) * A.bstride);
+  if (MULTIWARP && s + 1 == A.withhold) C.bnd_out = A.sink;
+  C.dir_base = nullptr;
+  C.err = A.err;
+  C.poll_ns = A.poll_ns;
+  C.watchdog = A.watchdog;
+  C.hm = A.hm;
+  C.n = n;
+  C.s = s;
+  C.lane = lane;
+  if (s > 0) st.chunk_nxt = chunk_verify<MULTIWARP>(C, 0, chunk_issue<MULTIWARP>(C, 0));
+  const int ngrp = (n + 127 + 7) / 8;  // lane 31's G3 reaches column n at t = n + 126
+#pragma unroll 1
+  for (int g = 0; g < ngrp; ++g) {
+    const int t0 = g * 8;
+    st.chunk_cur = st.chunk_nxt;
+    const bool more = s > 0 && t0 + 8 < n;
+    unsigned long long raw = 0;
+    if (more) raw = chunk_issue<MULTIWARP>(C, t0 + 8);
+    const bool masked = t0 < 128 || t0 + 7 >= n - 1;
+    if (masked) d16x2_group<KR, MULTIWARP, true>(st, C, t0, rows);
+    else d16x2_group<KR, MULTIWARP, false>(st, C, t0, rows);
+    if (more) st.chunk_nxt = chunk_verify<MULTIWARP>(C, t0 + 8, raw);
+  }
+  int tot = st.usum;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
+  if (lane == 0) {
+    if (MULTIWARP) atomicAdd(A.hm, tot);
+    else *A.hm += tot;
+  }
+  __syncwarp();
+}
+
 }  // namespace nwk

@@ -71,13 +71,23 @@ __global__ void k_encode(const uint8_t* __restrict__ in, long long len,
     atomicMin(reinterpret_cast<unsigned long long*>(bad), (unsigned long long)(my_bad + pos_base));
 }
 
+// Selector table of the packed sweeps (FillArgs::sel): sel[i] = (17 c[i] + 128) |
+// (17 c[i-1] + 196) << 8 over codes c[-1 .. len) (c[-1] read from the padding).
+__global__ void k_sel16(const uint8_t* __restrict__ codes, long long len, uint16_t* __restrict__ sel) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += (long long)gridDim.x * blockDim.x)
+    sel[i] = (uint16_t)((17u * codes[i] + 128u) | ((17u * codes[i - 1] + 196u) << 8));
+}
+
 #endif  // NW_COMMON_KERNELS
 
 // One pair, one strip per warp at a time; strips handed out in order by an
 // atomic ticket so every awaited producer is already resident (no deadlock).
 // D16 (score-only, K <= 4, s - 2g >= 0): the packed difference-form sweep of
 // nw_fill_d16.cuh (KR rows per lane, two per register) instead of strip_sweep.
-template <int KR, bool DIRS, bool PROFREG, int PI, bool D16 = false>
+// D16: 0 = int32 strip_sweep, 1 = packed difference form (one chain per lane),
+// 2 = packed difference form with two chains per lane (strip_sweep_d16x2).
+template <int KR, bool DIRS, bool PROFREG, int PI, int D16 = 0>
 __global__ void __launch_bounds__(32) k_fill_pair(FillArgs A) {
   extern __shared__ __align__(16) int8_t smem[];
   const int lane = threadIdx.x & 31;
@@ -86,7 +96,8 @@ __global__ void __launch_bounds__(32) k_fill_pair(FillArgs A) {
     if (lane == 0) s = atomicAdd(A.ticket, 1);
     s = __shfl_sync(FULL, s, 0);
     if (s >= A.nstrips) break;
-    if constexpr (D16) strip_sweep_d16<KR, true>(A, s, lane);
+    if constexpr (D16 == 2) strip_sweep_d16x2<KR, true>(A, s, lane);
+    else if constexpr (D16 == 1) strip_sweep_d16<KR, true>(A, s, lane);
     else strip_sweep<KR, DIRS, PROFREG, PI, true>(A, s, lane, smem);
   }
 }
@@ -447,6 +458,7 @@ struct BatchArgs {
   int g;
   int* ticket;
   int* scores;             // per pair, pair order
+  const uint16_t* sel16;   // selector table aligned with codes (FillArgs::sel; packed sweeps)
   // per-warp scratch
   int* wbnd;               // [nwarps][2][bstride]
   long long bstride;
@@ -553,7 +565,7 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
     int hmv = 0;
     if (m > 0 && n > 0) {
       FillArgs A;
-      A.a = B.codes + ao; A.b = B.codes + bo; A.prof = B.prof; A.K = B.K;
+      A.a = B.codes + ao; A.b = B.codes + bo; A.prof = B.prof; A.K = B.K; A.sel = B.sel16 + bo;
       constexpr int RS = PACKED ? 32 * KR16 : R;  // strip height of the sweep in use
       A.m = m; A.n = n; A.nstrips = (m + RS - 1) / RS; A.nslots = 2;
       A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr; A.ckpt = nullptr; A.ck_every = 0; A.ck_stride = 0; A.top_row = nullptr; A.top_tag = 0;

@@ -18,7 +18,7 @@ template <int PI>
 void launch_batch_dirs(const BatchArgs& B, bool profreg, int packed_kr, int grid, size_t smem,
                        cudaStream_t st);
 
-template <int KR, bool DIRS, bool PROFREG, int PI, bool D16 = false>
+template <int KR, bool DIRS, bool PROFREG, int PI, int D16 = 0>
 void launch_fill_t(const FillArgs& A, int grid, size_t smem, cudaStream_t st) {
   auto k = k_fill_pair<KR, DIRS, PROFREG, PI, D16>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -316,11 +316,14 @@ def test_score_only_tall_difference_form(ctx, m, n):
         assert nwb.nw_score_only(ctx, a, b, sc) == oracle.score(a, b, sc)
 
 
+@pytest.mark.parametrize("chains", [0, 1])
 @pytest.mark.parametrize("kr", [4, 8, 12, 14, 16, 18, 20, 22, 24, 26, 28, 30, 32])
-def test_score_only_difference_form_every_kr(ctx, opts, kr):
+def test_score_only_difference_form_every_kr(ctx, opts, kr, chains):
     """The packed score-only sweep at every rows-per-lane setting the library can pick
-    (strip heights 128..1,024 rows, ragged last strips, one-strip pairs)."""
+    (strip heights 128..1,024 rows, ragged last strips, one-strip pairs), with one or
+    (rows per lane % 4 == 0) two independent chains per lane."""
     opts(ctx, "d16_force", kr)
+    opts(ctx, "d16_chains", chains)
     for k, (m, n) in enumerate([(2500, 700), (32 * kr * 3 + 17, 333), (5, 900), (1, 1)]):
         a, b = _pair(9100 + 37 * kr + k, m, n)
         for sc in (nwgen.PAPER_DNA, nwgen.Scoring(match=2, mismatch=-1, gap=-3)):
