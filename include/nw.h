@@ -328,8 +328,9 @@ enum {
   NW_OPT_DIST_VIRTUAL_RANK = 18,
   NW_OPT_DIST_PIPELINE = 19,  /* dist ctx score-only pairs: 0 = column-block pipeline across the
                                  ranks when world > 1 and m*n >= 2^34; 1 = always; 2 = never */
-  NW_OPT_D16_CHAINS = 20,      /* packed difference-form score-only fills: 0 = two independent
-                                 chains per lane when rows per lane % 4 == 0, 1 = one chain */
+  NW_OPT_D16_CHAINS = 20,      /* packed difference-form score-only pair fills: 2 = two independent
+                                 chains per lane (rows per lane % 4 == 0; measured slower on C5),
+                                 else one chain (default) */
   NW_OPT_COUNT_ = 21
 };
 nw_status nw_ctx_set_option(nw_ctx *ctx, int32_t option, int64_t value);

@@ -607,7 +607,7 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     {
       KernelTimer kt(c, 0);
       ok = dispatch_fill(dirs, pi, kr, profreg, A, grid, smem, c->stream, d16,
-                         c->opt[NW_OPT_D16_CHAINS] != 1 && !ckpt);
+                         c->opt[NW_OPT_D16_CHAINS] == 2 && !ckpt);
     }
     if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
     LAUNCHED(c);
@@ -1676,14 +1676,6 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   uint8_t* codes = c->d_codes + PAD;
   (void)already_coded;
   launch_encode(c, d_codes_raw_or_codes, total, codes, 0);
-  // selector table of the packed DNA sweeps (FillArgs::sel), aligned with the codes
-  st = grow(c, c->d_sel16, c->sel16_cap, sizeof(uint16_t) * (size_t)lc);
-  if (st) return st;
-  {
-    const int blocks = (int)std::min<long long>((lc - 1 + 255) / 256, (long long)c->sm_count * 8);
-    k_sel16<<<std::max(blocks, 1), 256, 0, c->stream>>>(c->d_codes + 1, lc - 1, c->d_sel16 + 1);
-    LAUNCHED(c);
-  }
   hl.lap("bounds, memset, encode");
   // order: implicit all-pairs -> perm of sequences by length (descending);
   // explicit pairs -> LPT order by m*n (descending), bucketed.
@@ -1708,6 +1700,13 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   for (int x = 0; x < sc->K; ++x)
     for (int y = 0; y < sc->K; ++y) smax = std::max(smax, score_of(sc, x, y) - 2 * sc->gap);
   const bool u16 = packed && (long long)maxlen * smax <= 65535;
+  if (u16) {  // selector table of the packed H' sweep (FillArgs::sel), aligned with the codes
+    st = grow(c, c->d_sel16, c->sel16_cap, sizeof(uint16_t) * (size_t)lc);
+    if (st) return st;
+    const int blocks = (int)std::min<long long>((lc - 1 + 255) / 256, (long long)c->sm_count * 8);
+    k_sel16<<<std::max(blocks, 1), 256, 0, c->stream>>>(c->d_codes + 1, lc - 1, c->d_sel16 + 1);
+    LAUNCHED(c);
+  }
   bool d16 = packed && !u16;
   if (tbk && !c->opt[NW_OPT_NO_D16]) {  // traceback: difference form with decision flags
     int smin = 1 << 30;
@@ -1905,7 +1904,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   B.ticket = c->d_ints;
   B.err = c->d_err;
   B.scores = d_scores;
-  B.sel16 = c->d_sel16 + PAD;
+  B.sel16 = c->d_sel16 ? c->d_sel16 + PAD : nullptr;  // read by the u16 sweep only
   char* base = static_cast<char*>(c->d_scratch);
   B.wbnd = reinterpret_cast<int*>(base);
   B.bstride = bstride;

@@ -316,7 +316,7 @@ def test_score_only_tall_difference_form(ctx, m, n):
         assert nwb.nw_score_only(ctx, a, b, sc) == oracle.score(a, b, sc)
 
 
-@pytest.mark.parametrize("chains", [0, 1])
+@pytest.mark.parametrize("chains", [0, 2])
 @pytest.mark.parametrize("kr", [4, 8, 12, 14, 16, 18, 20, 22, 24, 26, 28, 30, 32])
 def test_score_only_difference_form_every_kr(ctx, opts, kr, chains):
     """The packed score-only sweep at every rows-per-lane setting the library can pick

@@ -19,13 +19,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 METRICS = "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"
 
 
-def main(wl: str):
+def main(wl: str, parse_only: bool = False):
+    """Run the ncu metric pass (GPU box) unless parse_only, then summarise the CSV
+    gpurun_out/traffic_<wl>.csv into profiles/r02_traffic_<wl>.json."""
     log = os.path.join(ROOT, "gpurun_out", f"traffic_{wl}.csv")
     os.makedirs(os.path.dirname(log), exist_ok=True)
-    cmd = ["ncu", "--metrics", METRICS, "--clock-control", "none", "--csv", "--log-file", log,
-           sys.executable, "bench.py", "--workload", wl, "--steps", "1", "--warmup", "3", "--no-cpu",
-           "--no-check"]
-    subprocess.run(cmd, cwd=ROOT, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+    if not parse_only:
+        cmd = ["ncu", "--metrics", METRICS, "--clock-control", "none", "--csv", "--log-file", log,
+               sys.executable, "bench.py", "--workload", wl, "--steps", "1", "--warmup", "3",
+               "--no-cpu", "--no-check"]
+        subprocess.run(cmd, cwd=ROOT, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
     rows = list(csv.reader(io.StringIO("".join(l for l in open(log) if l.startswith('"')))))
     hdr = rows[0]
     ix = {h: i for i, h in enumerate(hdr)}
@@ -61,4 +64,4 @@ def main(wl: str):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[-1], parse_only="--parse" in sys.argv)
