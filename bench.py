@@ -552,23 +552,40 @@ def run_ours(args):
         fill_avg_ms = fill_step_ms
     peak_issue = ALU_ISSUE_LANES_PER_CLK_PER_SM * SM_COUNT * SM_MAX_MHZ * 1e6 / 1e12
     peak = ALU_PIPE_LANES_PER_CLK_PER_SM * SM_COUNT * SM_MAX_MHZ * 1e6 / 1e12
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{wl}.json")
+    # DRAM traffic per launch of the dominant kernel, from one ncu metric pass of this
+    # workload (tools/traffic.py -> profiles/r02_traffic_<wl>.json; cold cache, serialised)
+    kname = ("k_percell_fill" if wl in ("c1p", "c2p") else
+             "k_fill_pair" if wl in ("c1", "c2", "c5", "c5tb") else "k_batch")
+    traffic, tinfo = None, {}
+    tp = os.path.join(ROOT, "profiles", f"r02_traffic_{wl}.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-    walk = None  # C4's traceback walk: HBM bytes (ncu, per launch) over its live event time
-    wp = os.path.join(ROOT, "profiles", f"traffic_{wl}_walk.json")
-    if os.path.exists(wp) and tb_n:
-        wb = json.load(open(wp)).get("dram_bytes_per_launch")
-        w_ms = tb_ms / tb_n
-        walk = {"kernel": "k_batch_walk", "bound": "hbm latency (dependent loads)", "ms_per_launch": w_ms,
-                "dram_bytes_per_launch": wb, "achieved_GBps": wb / (w_ms / 1e3) / 1e9,
-                "peak_GBps": load_peaks().get("hbm_gbs"), "bytes_source": os.path.relpath(wp, ROOT)}
+        tinfo = json.load(open(tp)).get("kernels", {})
+        fills = [v for k, v in tinfo.items() if k.startswith(kname + "<")]
+        if fills:
+            traffic = sum(v["dram_read_bytes_per_launch"] + v["dram_write_bytes_per_launch"]
+                          for v in fills) / len(fills)
+    hbm = load_peaks().get("hbm_gbs")
+    walk = None  # the traceback kernels' HBM rate: ncu bytes over their live event time
+    tbk = {k: v for k, v in tinfo.items() if k.startswith(("k_tb_", "k_batch_walk"))}
+    if tbk and tb_n:
+        rd = sum(v["dram_read_bytes_per_launch"] for v in tbk.values())
+        wr = sum(v["dram_write_bytes_per_launch"] for v in tbk.values())
+        t_ms = tb_ms / max(args.steps, 1)
+        walk = {"kernels": sorted(tbk), "bound": "hbm latency (dependent loads along the paths)",
+                "ms_per_step": t_ms, "dram_read_bytes_per_step": rd, "dram_write_bytes_per_step": wr,
+                "readback_GBps": rd / (t_ms / 1e3) / 1e9, "peak_GBps": hbm,
+                "readback_frac": (rd / (t_ms / 1e3) / 1e9) / hbm if hbm else None,
+                "bytes_source": os.path.relpath(tp, ROOT)}
+    dirs_write = None  # the fill's direction writes: algorithmic bytes (2 bits per cell) over the fill time
+    if mode in ("dirs", "d16dir") and fill_n and wl not in ("c1co", "c2co"):
+        b = W.cells / 4 * (1.29 if mode == "d16dir" else 1.0)
+        dirs_write = {"algorithmic_bytes_per_step": b, "GBps": b / (fill_step_ms / 1e3) / 1e9,
+                      "peak_GBps": hbm, "note": "2 bits per cell" + (
+                          " over the 1.29x padded sweep (DESIGN.md §3.9)" if mode == "d16dir" else "")}
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (int32 lane-ops)",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "peak_issue": peak_issue, "frac_issue": (achieved / peak_issue) if achieved else None,
-                "kernel": ("k_percell_fill" if wl in ("c1p", "c2p") else
-                           "k_fill_pair" if wl in ("c1", "c2", "c5", "c5tb") else "k_batch"),
+                "kernel": kname,
                 **({"kernel_ms_is": "both k_batch launches of one step"} if wl == "msa" else {}),
                 "ops_per_cell": ops, "kernel_ms_per_launch": fill_avg_ms,
                 "kernel_launches_per_step": fill_launches_per_step,
@@ -580,7 +597,8 @@ def run_ours(args):
                                 "128 lane-ops/clk/SM warp-issue limit (2-input VIMNMX). MEASURED_PEAKS.json "
                                 "has no INT32 entry"),
                 "form": mode,
-                **({"traceback_walk": walk} if walk else {})}
+                **({"traceback_readback": walk} if walk else {}),
+                **({"direction_write": dirs_write} if dirs_write else {})}
     out = {
         "metric": "GCUPS (cell updates/s)", "value": value, "unit": "GCUPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,

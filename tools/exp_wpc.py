@@ -1,0 +1,29 @@
+"""Single-pair fill with CTAs of 1/2/4 warps (not a bench line)."""
+import json, sys
+sys.path.insert(0, '.')
+import torch
+import nwgen, oracle
+import paper_2412_21103_b200 as nwb
+ctx = nwb.Context(0, torch.cuda.current_stream().cuda_stream)
+out = {}
+d = torch.zeros(1, dtype=torch.int64, device="cuda")
+def t(fn, reps):
+    fn(); torch.cuda.synchronize(); ctx.set_timing(True); ctx.kernel_time(0)
+    for _ in range(reps): fn()
+    ms, k = ctx.kernel_time(0); ctx.set_timing(False); return round(ms / max(k, 1), 4)
+a, b = nwgen.config_c2()
+ws, wops = oracle.align(a, b, nwgen.PAPER_DNA)
+da = torch.frombuffer(bytearray(a), dtype=torch.uint8).cuda(); db = torch.frombuffer(bytearray(b), dtype=torch.uint8).cuda()
+a5, b5 = nwgen.config_c5()
+d5a = torch.frombuffer(bytearray(a5), dtype=torch.uint8).cuda(); d5b = torch.frombuffer(bytearray(b5), dtype=torch.uint8).cuda()
+for w in (1, 2, 4):
+    ctx.set_option("fill_warps_per_cta", w)
+    for kr in (2, 4, 5, 8):
+        ctx.set_option("rows_per_lane", kr)
+        out[f"c2_kr{kr}_wpc{w}_ms"] = t(lambda: nwb.nw_align_pair_dev(ctx, da, db, nwgen.PAPER_DNA, d).free(), 10)
+    ctx.set_option("rows_per_lane", 0)
+    s, tb = nwb.nw_align_pair(ctx, a, b, nwgen.PAPER_DNA); ops = nwb.nw_traceback(ctx, tb); tb.free()
+    out[f"c2_wpc{w}_parity"] = bool(s == ws and ops.tolist() == wops.tolist())
+    out[f"c5_wpc{w}_ms"] = t(lambda: nwb.nw_score_only_dev(ctx, d5a, d5b, nwgen.PAPER_DNA, d), 3)
+    out[f"c5_wpc{w}_score"] = int(d.item())
+print(json.dumps(out, indent=1))
