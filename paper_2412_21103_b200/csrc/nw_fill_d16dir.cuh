@@ -6,14 +6,17 @@
 // lane, the high half one column behind). The P:90 decision needs no extra
 // comparisons: each candidate is maximal exactly when its difference to Z is 0,
 //     D maximal <=> Z - (s-2g) == 0,   U maximal <=> U == 0,   L maximal <=> V == 0,
-// so the bits for the tie order pi = (X, Y, Z) are [q_X == 0], [q_Y == 0], tested
-// for both halves at once by the 32-bit add q + 0x7fff7fff (bit 15 of a half is set
-// iff that half is nonzero; every q < 2^15, so no carry crosses a half), gathered by
-// one sign-replicating PRMT and inserted at bit q with one LOP3. Per packed register
-// and 8 steps the flags go to one 32-bit word (halves sharing a byte each):
-//   byte 0: X flags of the low cell, byte 1: X of the high cell,
-//   byte 2: Y flags of the low cell, byte 3: Y of the high cell,  step q at bit q.
+// so the bits for the tie order pi = (X, Y, Z) are nbX = [q_X != 0], nbY = [q_Y != 0]
+// (code X if !nbX, else Y if !nbY, else Z). Both halves at once: min(q, 1) per half
+// (VIMNMX.U16x2, one ALU-pipe cycle) gives nb in bit 0 of each half, and two IMADs on
+// the FMA pipe pack them: m = 2 min(q_Y, 1) + min(q_X, 1), acc = 4 acc + m. Over the
+// 8 steps of a group acc fills each half exactly (16 bits), so nothing carries from
+// the low half into the high half. Per packed register and 8 steps one 32-bit word:
+//   low half = the low cell (row k), high half = the high cell (row k+h); step q's
+//   nbX at bit 2(7-q) of its half and nbY at bit 2(7-q)+1.
 // Word index ((s*G + g)*H + k)*32 + lane, G = 8-step groups per strip.
+// (Round 1 used q + 0x7fff7fff, a sign-replicating PRMT and a LOP3 per register and
+// step, all on the ALU pipe, which that kernel saturated while the FMA pipe idled.)
 #pragma once
 #include "nw_fill_d16.cuh"
 
@@ -87,15 +90,10 @@ __device__ __forceinline__ void d16dir_group(D16DirState<KR>& st, const FillArgs
       // q_X, q_Y in {D: dd, U: un, L: vn}; flag = [q == 0] per half (top bit of each half)
       const uint32_t qX = T::X == 1 ? dd : (T::X == 2 ? un : vn);
       const uint32_t qY = T::Y == 1 ? dd : (T::Y == 2 ? un : vn);
-      // bit 15 of a half of q + 0x7fff is set iff that half is nonzero (every q < 2^15,
-      // so no carry leaves a half): a plain 32-bit add, which ptxas can issue on the
-      // FMA pipe, instead of a VIADD.16x2 on the ALU pipe
-      const uint32_t nX = qX + 0x7fff7fffu;
-      const uint32_t nY = qY + 0x7fff7fffu;
-      // bytes X.lo, X.hi, Y.lo, Y.hi, each the sign-replicated top bit (0xff: not maximal)
-      const uint32_t tk = prmt2(nX, nY, 0xFDB9u);
-      // step q's flags at bit q of each byte; the word restarts every 8-step group
-      st.acc[k] = (q == 0 ? 0u : st.acc[k]) | (~tk & (0x01010101u << q));
+      // nb per half = min(q, 1); m = 2 nbY + nbX (bits 0-1 and 16-17); acc = 4 acc + m,
+      // the word restarting every 8-step group
+      const uint32_t m = __vminu2(qY, 0x00010001u) * 2u + __vminu2(qX, 0x00010001u);
+      st.acc[k] = (q == 0 ? 0u : st.acc[k] * 4u) + m;
       if (MASKED) un &= mask;  // U(i, 0) = 0 until each half reaches column 1
       st.Up[k] = un;
       vup = vn;

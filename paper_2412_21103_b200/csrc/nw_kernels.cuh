@@ -664,8 +664,9 @@ __device__ __forceinline__ void walk_lanes(const BatchArgs& B, long long task, b
         cur = idx;
       }
       const int qq = t & 7;
-      const uint32_t fx = (w >> (8 * hi + qq)) & 1u, fy = (w >> (16 + 8 * hi + qq)) & 1u;
-      const int code = fx ? X : (fy ? Y : Z);
+      // nw_fill_d16dir.cuh layout: half hi, step qq: nbX at bit 2(7-qq), nbY at 2(7-qq)+1
+      const uint32_t fx = (w >> (16 * hi + 14 - 2 * qq)) & 1u, fy = (w >> (16 * hi + 15 - 2 * qq)) & 1u;
+      const int code = !fx ? X : (!fy ? Y : Z);  // nb bits: 1 = not maximal
       o[--pos] = (uint8_t)(code == 1 ? 1 : (code == 2 ? cV : cH));
       i -= (code != 3);
       j -= (code != 2);
