@@ -331,7 +331,9 @@ enum {
   NW_OPT_D16_CHAINS = 20,      /* packed difference-form score-only pair fills: 2 = two independent
                                  chains per lane (rows per lane % 4 == 0; measured slower on C5),
                                  else one chain (default) */
-  NW_OPT_COUNT_ = 21
+  NW_OPT_BATCH_U16_KR = 21,    /* score-only packed H' batch sweep: rows per lane 8, 16 or 32
+                                 (0: by the median sequence length) */
+  NW_OPT_COUNT_ = 22
 };
 nw_status nw_ctx_set_option(nw_ctx *ctx, int32_t option, int64_t value);
 /* Current value, or -1 for a NULL ctx / unknown option. */

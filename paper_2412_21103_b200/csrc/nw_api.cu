@@ -452,9 +452,11 @@ int d16_kr(const nw_ctx* c, long long m) {
 }
 
 bool dispatch_batch(bool dirs, int pi, bool profreg, bool u16, bool d16, int packed_kr,
-                    const BatchArgs& B, int grid, size_t smem, cudaStream_t st) {
+                    const BatchArgs& B, int grid, size_t smem, cudaStream_t st, int u16_kr = 16) {
   if (!dirs) {
-    if (u16) launch_batch_t<KR_BATCH, false, true, 123, 1>(B, grid, smem, st);
+    if (u16 && u16_kr == 32) launch_batch_t<KR_BATCH, false, true, 123, 1, 32>(B, grid, smem, st);
+    else if (u16 && u16_kr == 8) launch_batch_t<KR_BATCH, false, true, 123, 1, 8>(B, grid, smem, st);
+    else if (u16) launch_batch_t<KR_BATCH, false, true, 123, 1>(B, grid, smem, st);
     else if (d16) launch_batch_t<KR_BATCH, false, true, 123, 2>(B, grid, smem, st);
     else if (profreg) launch_batch_t<KR_BATCH, false, true, 123>(B, grid, smem, st);
     else launch_batch_t<KR_BATCH, false, false, 123>(B, grid, smem, st);
@@ -1669,7 +1671,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   if (st) return st;
   // codes buffer: PAD | codes | tail: the sweeps read up to one strip of rows
   // (512 for the packed sweep) and ~94 columns past a sequence's end
-  const long long lc = PAD + total + 512 + 2 * PAD;
+  const long long lc = PAD + total + R_MAX + 2 * PAD;
   st = grow(c, c->d_codes, c->codes_cap, (size_t)lc);
   if (st) return st;
   CUDA_TRY(c, cudaMemsetAsync(c->d_codes, 0, (size_t)lc, c->stream));
@@ -1982,7 +1984,23 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   bool ok;
   {
     KernelTimer kt(c, 0);
-    ok = dispatch_batch(tbk, pi, profreg, u16, d16, packed_kr, B, grid, smem, c->stream);
+    // rows per lane of the packed H' sweep: more rows amortise the per-step overhead,
+    // fewer waste less of a short pair's last strip; by the median sequence length
+    // (C3, median ~1,250: 32 rows = 9.51 TCUPS vs 16: 9.20, 8: 7.73; profiles/r02_exp_u16kr.json)
+    int u16_kr = 16;
+    if (u16) {
+      std::vector<long long> ls;
+      ls.reserve(std::min<long long>(nseq, 4096));
+      for (int k = 0; k < nseq && k < 4096; ++k) ls.push_back(h_offs[k + 1] - h_offs[k]);
+      if (!ls.empty()) {
+        std::nth_element(ls.begin(), ls.begin() + ls.size() / 2, ls.end());
+        const long long med = ls[ls.size() / 2];
+        u16_kr = med >= 1024 ? 32 : (med >= 384 ? 16 : 8);
+      }
+      if (c->opt[NW_OPT_BATCH_U16_KR] == 8 || c->opt[NW_OPT_BATCH_U16_KR] == 16 || c->opt[NW_OPT_BATCH_U16_KR] == 32)
+        u16_kr = (int)c->opt[NW_OPT_BATCH_U16_KR];
+    }
+    ok = dispatch_batch(tbk, pi, profreg, u16, d16, packed_kr, B, grid, smem, c->stream, u16_kr);
   }
   if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
   LAUNCHED(c);

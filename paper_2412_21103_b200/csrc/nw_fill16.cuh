@@ -100,7 +100,7 @@ __device__ __forceinline__ void u16_block(U16State& st, uint32_t (&PA)[KR / 2],
 // strip_sweep<..., MULTIWARP = false> (the batch kernel's per-warp strips).
 template <int KR>
 __device__ __forceinline__ void strip_sweep_u16(const FillArgs& A, int s, int lane) {
-  static_assert(KR % 2 == 0 && KR <= 16, "KR must be even");
+  static_assert(KR % 2 == 0 && KR <= 32, "KR must be even");
   constexpr int H = KR / 2;
   constexpr int R = 32 * KR;
   const int n = A.n;

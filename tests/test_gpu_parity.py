@@ -519,3 +519,17 @@ def test_batch_traceback_device_plan(ctx, opts, host_plan):
             p, q = pairs[k]
             ws, wops = oracle.align(ss.seq(p), ss.seq(q), sc)
             assert paths[k].tolist() == wops.tolist(), (k, tie)
+
+
+@pytest.mark.parametrize("kr", [0, 8, 16, 32])
+def test_batch_score_only_u16_rows_per_lane(ctx, opts, kr):
+    """The packed H' batch sweep at 8/16/32 rows per lane (0: chosen by the median
+    length): pair lengths straddle the 256/512/1,024-row strip edges, empty sequences."""
+    opts(ctx, "batch_u16_kr", kr)
+    ss = nwgen.random_set(80 + kr, 26, 0, 2100)
+    pairs = nwgen.all_pairs(ss.nseq)
+    want = oracle.batch_score(ss.residues, ss.offs, pairs, nwgen.PAPER_DNA)
+    assert nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, nwgen.PAPER_DNA).tolist() == want.tolist()
+    rev = pairs[::3, ::-1].copy()
+    assert nwb.nw_align_batch(ctx, ss.residues, ss.offs, rev, nwgen.PAPER_DNA).tolist() == \
+        oracle.batch_score(ss.residues, ss.offs, rev, nwgen.PAPER_DNA).tolist()
