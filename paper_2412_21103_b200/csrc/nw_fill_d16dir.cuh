@@ -14,7 +14,10 @@
 // the low half into the high half. Per packed register and 8 steps one 32-bit word:
 //   low half = the low cell (row k), high half = the high cell (row k+h); step q's
 //   nbX at bit 2(7-q) of its half and nbY at bit 2(7-q)+1.
-// Word index ((s*G + g)*H + k)*32 + lane, G = 8-step groups per strip.
+// Word index ((s*G + g)*32 + lane)*H + k, G = 8-step groups per strip: a lane's H words
+// of a group are contiguous, stored as 16-byte vectors, so the traceback walk, which
+// moves up through a lane's rows and left through a group's steps, finds them in one
+// load (round 1: ((s*G + g)*H + k)*32 + lane, one 4-byte word per load).
 // (Round 1 used q + 0x7fff7fff, a sign-replicating PRMT and a LOP3 per register and
 // step, all on the ALU pipe, which that kernel saturated while the FMA pipe idled.)
 #pragma once
@@ -115,8 +118,10 @@ __device__ __forceinline__ void d16dir_group(D16DirState<KR>& st, const FillArgs
     }
   }
   uint32_t* d = dir_base + (long long)(t0 >> 3) * (H * 32);
+  static_assert(H % 4 == 0, "flag words are stored as 16-byte vectors");
 #pragma unroll
-  for (int k = 0; k < H; ++k) d[k * 32] = st.acc[k];
+  for (int k = 0; k < H; k += 4)
+    *reinterpret_cast<uint4*>(d + k) = make_uint4(st.acc[k], st.acc[k + 1], st.acc[k + 2], st.acc[k + 3]);
 }
 
 // One strip of one pair inside the batch kernel (single warp, sequential strips).
@@ -162,7 +167,7 @@ __device__ __forceinline__ void strip_sweep_d16dir(const FillArgs& A, int s, int
   st.bc_nxt = __ldg(A.b - 2 * lane);
   const int* bnd_in = (s > 0) ? static_cast<const int*>(A.bnd) + (size_t)(s % A.nslots) * A.bstride : nullptr;
   int* bnd_out = static_cast<int*>(A.bnd) + (size_t)((s + 1) % A.nslots) * A.bstride;
-  uint32_t* dir_base = reinterpret_cast<uint32_t*>(A.dirs) + (long long)s * A.wpl * (H * 32) + lane;
+  uint32_t* dir_base = reinterpret_cast<uint32_t*>(A.dirs) + (long long)s * A.wpl * (H * 32) + lane * H;
   const int ngrp = (n + 63 + 7) / 8;
   int chunk = 0;
 #pragma unroll 1

@@ -651,17 +651,27 @@ __device__ __forceinline__ void walk_lanes(const BatchArgs& B, long long task, b
     pos = m + n;
     int i = m, j = n;
     long long cur = -1;
-    uint32_t w = 0;
+    uint4 blk[H / 4];  // the lane's H flag words of one 8-step group (nw_fill_d16dir.cuh)
     while (i > 0 && j > 0) {
       const int ia = i - 1;
       const int s = ia / RS, rr = ia % RS, l = rr / KR16, r = rr % KR16;
       const int hi = r >= H;
       const int kk = hi ? r - H : r;
       const int t = hi ? j + 2 * l : j - 1 + 2 * l;
-      const long long idx = (((long long)s * G + (t >> 3)) * H + kk) * 32 + l;
-      if (idx != cur) {  // a run of horizontal moves stays in one word
-        w = COHERENT ? __ldcg(d + idx) : __ldg(d + idx);
-        cur = idx;
+      const long long bidx = (((long long)s * G + (t >> 3)) * 32 + l) * H;
+      if (bidx != cur) {  // up-moves inside the lane's rows and left-moves inside the group
+                          // reuse the block: one 16-byte load per block change
+        const uint4* bp = reinterpret_cast<const uint4*>(d + bidx);
+#pragma unroll
+        for (int v = 0; v < H / 4; ++v) blk[v] = COHERENT ? __ldcg(bp + v) : __ldg(bp + v);
+        cur = bidx;
+      }
+      uint32_t w = 0;
+#pragma unroll
+      for (int v = 0; v < H / 4; ++v) {
+        const uint4 b4 = blk[v];
+        const int k4 = kk - 4 * v;
+        w = k4 == 0 ? b4.x : k4 == 1 ? b4.y : k4 == 2 ? b4.z : k4 == 3 ? b4.w : w;
       }
       const int qq = t & 7;
       // nw_fill_d16dir.cuh layout: half hi, step qq: nbX at bit 2(7-qq), nbY at 2(7-qq)+1
