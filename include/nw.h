@@ -333,7 +333,9 @@ enum {
                                  else one chain (default) */
   NW_OPT_BATCH_U16_KR = 21,    /* score-only packed H' batch sweep: rows per lane 8, 16 or 32
                                  (0: by the median sequence length) */
-  NW_OPT_COUNT_ = 22
+  NW_OPT_BATCH_BND_GLOBAL = 22, /* 1: the packed H' batch sweep keeps its boundary rows in global
+                                  scratch instead of shared memory */
+  NW_OPT_COUNT_ = 23
 };
 nw_status nw_ctx_set_option(nw_ctx *ctx, int32_t option, int64_t value);
 /* Current value, or -1 for a NULL ctx / unknown option. */

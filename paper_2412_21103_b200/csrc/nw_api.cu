@@ -1872,7 +1872,13 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
     if (st) return st;
   }
   const size_t smem_prof = profreg ? 0 : (((size_t)warps_per_cta * sc->K * RS + 15) & ~size_t(15));
-  const size_t smem = smem_prof;
+  // the packed H' sweep keeps its boundary row in shared memory when 6 CTAs still fit
+  // an SM (C3: 4 warps x 2,066 ints = 33 KB per CTA); its DRAM traffic is then the
+  // inputs and the scores (the global per-warp rows were 533 MB of DRAM writes per C3
+  // launch, evicted from L2)
+  const size_t smem_bnd = ((size_t)warps_per_cta * (size_t)(maxlen + 1 + 64) * 4 + 15) & ~size_t(15);
+  const bool bnd_smem = u16 && smem_prof + smem_bnd <= 37 * 1024 && !c->opt[NW_OPT_BATCH_BND_GLOBAL];
+  const size_t smem = smem_prof + (bnd_smem ? smem_bnd : 0);
   // 6 x 4 warps per SM (24 warps, 72 registers each): C4 2.11 -> 2.26 TCUPS, C3 6.73 -> 6.84
   // over 4 per SM; 8 no better (tools/exp_ctas.sh, profiles/r01_exp_ctas.txt)
   int ctas_per_sm = 6;
@@ -1907,6 +1913,8 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   B.err = c->d_err;
   B.scores = d_scores;
   B.sel16 = c->d_sel16 ? c->d_sel16 + PAD : nullptr;  // read by the u16 sweep only
+  B.bnd_smem = bnd_smem ? 1 : 0;
+  B.bnd_smem_off = (int)smem_prof;
   char* base = static_cast<char*>(c->d_scratch);
   B.wbnd = reinterpret_cast<int*>(base);
   B.bstride = bstride;

@@ -486,6 +486,8 @@ struct BatchArgs {
   // (rank-space order, gathered and scattered to pair order by k_rs_scatter).
   long long tbase = 0;
   int compact = 0;
+  int bnd_smem = 0;           // packed H' sweep: the boundary row in shared memory (one slot
+  int bnd_smem_off = 0;       //   of bstride ints per warp at this byte offset)
 };
 
 // flat rank-space index k -> (p', q'), p' < q', lexicographic over N items
@@ -536,7 +538,12 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
   constexpr int RSP = PACKED ? 32 * KR16 : R;  // strip height (shared-profile rows)
   int8_t* sprof = smem + (PROFREG ? 0 : wib * (B.K * RSP));
-  int* bnd = B.wbnd + gw * 2 * B.bstride;
+  // the strips of a pair run one after another in this warp; the packed H' sweep reads
+  // the row above (32 columns ahead) before overwriting it (62 columns behind), so one
+  // row in shared memory suffices (bnd_smem; global scratch otherwise)
+  int* bnd = (PACKED == 1 && B.bnd_smem)
+                 ? reinterpret_cast<int*>(smem + B.bnd_smem_off) + wib * B.bstride
+                 : B.wbnd + gw * 2 * B.bstride;
   uint16_t* wd = DIRS ? B.wdirs + gw * B.dstride : nullptr;
   for (;;) {
     long long task = 0;
@@ -567,7 +574,7 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       FillArgs A;
       A.a = B.codes + ao; A.b = B.codes + bo; A.prof = B.prof; A.K = B.K; A.sel = B.sel16 + bo;
       constexpr int RS = PACKED ? 32 * KR16 : R;  // strip height of the sweep in use
-      A.m = m; A.n = n; A.nstrips = (m + RS - 1) / RS; A.nslots = 2;
+      A.m = m; A.n = n; A.nstrips = (m + RS - 1) / RS; A.nslots = (PACKED == 1 && B.bnd_smem) ? 1 : 2;
       A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr; A.ckpt = nullptr; A.ck_every = 0; A.ck_stride = 0; A.top_row = nullptr; A.top_tag = 0;
       A.dirs = PACKED == 3 ? reinterpret_cast<uint16_t*>(B.tdirs + B.tdir_off[task]) : wd;
       A.wpl = PACKED ? (n + 63 + 7) / 8 : (n + 31 + 7) / 8;  // 8-step groups per strip

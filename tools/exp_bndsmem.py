@@ -1,0 +1,23 @@
+"""C3 batch fill: boundary rows in shared memory vs global scratch (not a bench line)."""
+import json, sys
+sys.path.insert(0, '.')
+import torch, numpy as np
+import nwgen, oracle
+import paper_2412_21103_b200 as nwb
+ctx = nwb.Context(0, torch.cuda.current_stream().cuda_stream)
+ss = nwgen.config_c3()
+ds = torch.from_numpy(ss.residues).cuda(); do = torch.from_numpy(ss.offs).cuda()
+P = ss.nseq * (ss.nseq - 1) // 2
+out = {}
+rng = np.random.Generator(np.random.PCG64(1)); idx = np.sort(rng.choice(P, 64, replace=False))
+want = oracle.batch_score(ss.residues, ss.offs, nwgen.all_pairs(ss.nseq)[idx], nwgen.PAPER_DNA)
+for g in (1, 0, 1, 0):
+    ctx.set_option("batch_bnd_global", g)
+    sc = torch.zeros(P, dtype=torch.int32, device="cuda")
+    f = lambda: nwb.nw_align_batch_dev(ctx, ds, do, ss.offs, None, None, P, nwgen.PAPER_DNA, 0, sc)
+    f(); torch.cuda.synchronize(); ctx.set_timing(True); ctx.kernel_time(0)
+    for _ in range(3): f()
+    ms, k = ctx.kernel_time(0); ctx.set_timing(False)
+    out.setdefault(f"global{g}", []).append({"ms": round(ms / k, 2), "TCUPS": round(3216418768982 / (ms / k) / 1e9, 3),
+                      "sample_ok": bool((sc.cpu().numpy()[idx] == want).all())})
+print(json.dumps(out, indent=1))
