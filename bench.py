@@ -670,6 +670,10 @@ def main():
         run_reference(args)
     elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # no torchrun environment: one process per GPU, spawned here (rank 0 prints)
+        import torch
+        if torch.cuda.device_count() < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {torch.cuda.device_count()} CUDA "
+                             "device(s) visible (one process per GPU)")
         from paper_2412_21103_b200 import dist as nwdist
         nwdist.launch(args.gpus, run_ours, (args,))
     else:
