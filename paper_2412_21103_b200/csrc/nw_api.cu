@@ -953,6 +953,17 @@ nw_status nw_ctx_set_dist(nw_ctx* c, int32_t rank, int32_t world, const uint8_t*
   c->comm = comm;
   c->rank = rank;
   c->world = world;
+  // a new group: the column-block buffers, their peer mapping and the tag counter start
+  // afresh (identically on every rank), so stale entries of earlier calls can never match
+  if (c->cb_next) cudaIpcCloseMemHandle(c->cb_next);
+  c->cb_next = nullptr;
+  if (c->d_cb_recv) cudaFree(c->d_cb_recv);
+  c->d_cb_recv = nullptr;
+  c->cb_recv_cap = 0;
+  if (c->d_cb_ring) cudaFree(c->d_cb_ring);
+  c->d_cb_ring = nullptr;
+  c->cb_ring_cap = 0;
+  c->cb_tag_next = 1;
   return NW_OK;
 }
 
