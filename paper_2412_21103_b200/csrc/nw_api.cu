@@ -963,6 +963,9 @@ nw_status nw_ctx_set_dist(nw_ctx* c, int32_t rank, int32_t world, const uint8_t*
   if (c->d_cb_ring) cudaFree(c->d_cb_ring);
   c->d_cb_ring = nullptr;
   c->cb_ring_cap = 0;
+  if (c->d_cb_vrecv) cudaFree(c->d_cb_vrecv);
+  c->d_cb_vrecv = nullptr;
+  c->cb_vrecv_cap = 0;
   c->cb_tag_next = 1;
   return NW_OK;
 }
