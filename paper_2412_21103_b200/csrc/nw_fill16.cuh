@@ -141,6 +141,10 @@ __device__ __forceinline__ void strip_sweep_u16(const FillArgs& A, int s, int la
   if (s > 0) chunk_nxt = (lane + 1 <= n) ? bnd_in[lane + 1] : 0;
   const int nsteps = n + 63;  // last lane's high half reaches column n at t = n + 62
   for (int t0 = 0; t0 < nsteps; t0 += 32) {
+    // orders this block's boundary loads (columns >= t0+33) before lane 31's later stores
+    // to the same row (62 columns behind, in a later block): with the row in shared
+    // memory (one slot) that is a write-after-read within the warp (racecheck)
+    __syncwarp();
     st.chunk = chunk_nxt;
     if (s > 0) {
       const int jj = t0 + 33 + lane;
