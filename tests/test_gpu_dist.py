@@ -136,3 +136,34 @@ def test_c3_partition_ranges_fullsize(ctx, opts):
         bufs, _ = _run(ctx, torch, ss, None, sc, nwb.NW_SCORE_ONLY, bufs)
     ctx.set_option("dist_virtual_rank", 0)
     assert torch.equal(bufs[0], single[0])
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_partition_invariance_host_entry(ctx, opts, G):
+    """The host entry point (nw_align_batch) on the same replayed G-rank partition,
+    explicit pairs with traceback, into caller-owned output buffers."""
+    sc = nwgen.PAPER_DNA
+    ss, pairs = _case("explicit", seed=10 + G)
+    oo = nwb.nw_batch_ops_offsets(ss.offs, pairs)
+    out = (np.full(len(pairs), -7, np.int32), np.zeros(int(oo[-1]) + 1, np.uint8),
+           np.zeros(len(pairs) + 1, np.int64), np.zeros(len(pairs), np.int32))
+    opts(ctx, "dist_virtual_world", G)
+    for r in range(G):
+        ctx.set_option("dist_virtual_rank", r)
+        scores, ops, ops_off, ops_len = nwb.nw_align_batch(ctx, ss.residues, ss.offs, pairs, sc,
+                                                           nwb.NW_TRACEBACK, out=out)
+    ctx.set_option("dist_virtual_rank", 0)
+    want = oracle.batch_score(ss.residues, ss.offs, pairs, sc)
+    assert scores.tolist() == want.tolist()
+    paths = nwb.batch_paths(ops, ops_off, ops_len)
+    for k in range(0, len(pairs), 13):
+        assert paths[k].tolist() == oracle.align(ss.seq(pairs[k][0]), ss.seq(pairs[k][1]), sc)[1].tolist()
+
+
+def test_set_dist_validates(ctx):
+    uid = nwb.nw_dist_unique_id()
+    for rank, world in [(-1, 1), (1, 1), (0, 0)]:
+        with pytest.raises(nwb.NWError) as e:
+            ctx.set_dist(rank, world, uid)
+        assert e.value.status == nwb.NW_E_INVAL
+    assert ctx.dist_info() == (0, 1)
