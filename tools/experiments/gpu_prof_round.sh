@@ -1,5 +1,5 @@
 # Full ncu captures of the dominant kernels (split from gpu_round.sh: gpurun brings
-# back at most 64 MiB per call). Usage: bash tools/gpu_prof_round.sh [c2|batch]
+# back at most 64 MiB per call). Usage: bash tools/experiments/gpu_prof_round.sh [c2|batch]
 set -x
 mkdir -p gpurun_out
 if [ "$1" != batch ]; then
