@@ -51,11 +51,12 @@ SM_COUNT = 148
 SM_MAX_MHZ = 1965.0
 # SURVEY.md §8(d) algorithmic op floors per cell, by the arithmetic form of the fill:
 # int32 with directions 6, int32 score-only 3, two 16-bit cells per register (H' half
-# rows, C3) 1.5, the packed difference form (C5: PRMT + VIMNMX3.U16x2 + 2 IADD per two
-# cells) 2, packed with decision flags (C4) 2 (SURVEY's "u16x2 + direction")
-OPS_PER_CELL = {"dirs": 6, "score": 3, "u16": 1.5, "d16": 2, "d16dir": 2}
+# rows, C3; and the same with a moving per-strip base, C5: PRMT + IADD + VIMNMX3.U16x2 per
+# two cells) 1.5, the packed difference form (the C5 checkpoint pass: PRMT + VIMNMX3.U16x2
+# + 2 IADD per two cells) 2, packed with decision flags (C4) 2 (SURVEY's "u16x2 + direction")
+OPS_PER_CELL = {"dirs": 6, "score": 3, "u16": 1.5, "h16": 1.5, "d16": 2, "d16dir": 2}
 FORM = {"c1": "dirs", "c2": "dirs", "c1p": "dirs", "c2p": "dirs", "c1co": "dirs", "c2co": "dirs",
-        "c3": "u16", "c4": "d16dir", "c5": "d16", "c5tb": "d16", "msa": "u16"}
+        "c3": "u16", "c4": "d16dir", "c5": "h16", "c5tb": "d16", "msa": "u16"}
 WORKLOADS = {
     "c1": "C1: single DNA pair 1,000 x 1,000, +1/-1/-1, score + full traceback",
     "c2": "C2: single DNA pair 20,000 x 20,000, +1/-1/-1, score + 2-bit packed traceback",
@@ -535,6 +536,8 @@ def run_ours(args):
     fill_avg_ms = fill_ms / max(fill_n, 1)
     fill_launches_per_step = fill_n / max(args.steps, 1)
     mode = FORM[wl]
+    if wl == "c5" and sharded:  # the column-block pipeline across ranks runs the difference form
+        mode = "d16"
     ops = OPS_PER_CELL[mode]
     # the step's cells over the fill time of the whole step (C4 fills in two launches:
     # the pairs kept in their orientation, then the transposed ones)

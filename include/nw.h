@@ -335,7 +335,12 @@ enum {
                                  (0: by the median sequence length) */
   NW_OPT_BATCH_BND_GLOBAL = 22, /* 1: the packed H' batch sweep keeps its boundary rows in global
                                   scratch instead of shared memory */
-  NW_OPT_COUNT_ = 23
+  NW_OPT_PAIR_FORM = 23,       /* tall score-only pairs: 0 = packed H' with a moving base
+                                  (nw_fill_h16, default), 1 = packed difference form (nw_fill_d16) */
+  NW_OPT_H16_REBASE = 24,      /* packed H' pair sweep: rebase period in 8-step groups (power of two,
+                                  0: the largest <= 64 the value range allows); test hook */
+  NW_OPT_H16_KR = 25,          /* rows per lane of the packed H' pair sweep (even, 12..32; 0: rule) */
+  NW_OPT_COUNT_ = 26
 };
 nw_status nw_ctx_set_option(nw_ctx *ctx, int32_t option, int64_t value);
 /* Current value, or -1 for a NULL ctx / unknown option. */

@@ -385,6 +385,43 @@ bool dispatch_fill(bool dirs, int pi, int kr, bool profreg, const FillArgs& A, i
   return false;
 }
 
+// Packed H' pair sweep with a moving base (nw_fill_h16.cuh).
+template <int F>
+bool dispatch_fill_h16_t(int kr, const FillArgs& A, int grid, cudaStream_t st) {
+  switch (kr) {
+    case 8: launch_fill_t<8, false, true, 123, F>(A, grid, 0, st); return true;
+    case 12: launch_fill_t<12, false, true, 123, F>(A, grid, 0, st); return true;
+    case 16: launch_fill_t<16, false, true, 123, F>(A, grid, 0, st); return true;
+    case 18: launch_fill_t<18, false, true, 123, F>(A, grid, 0, st); return true;
+    case 20: launch_fill_t<20, false, true, 123, F>(A, grid, 0, st); return true;
+    case 22: launch_fill_t<22, false, true, 123, F>(A, grid, 0, st); return true;
+    case 24: launch_fill_t<24, false, true, 123, F>(A, grid, 0, st); return true;
+    case 26: launch_fill_t<26, false, true, 123, F>(A, grid, 0, st); return true;
+    case 28: launch_fill_t<28, false, true, 123, F>(A, grid, 0, st); return true;
+    case 30: launch_fill_t<30, false, true, 123, F>(A, grid, 0, st); return true;
+    case 32: launch_fill_t<32, false, true, 123, F>(A, grid, 0, st); return true;
+  }
+  return false;
+}
+bool dispatch_fill_h16(int kr, const FillArgs& A, int grid, cudaStream_t st) {
+  return dispatch_fill_h16_t<3>(kr, A, grid, st);
+}
+
+#ifdef NW_TRACE
+// experiment builds only: per-strip timestamps of the h16 sweep (every 1024 groups)
+unsigned long long* g_trace = nullptr;
+int g_trace_strips = 0;
+unsigned long long* nw_trace_buffer(int nstrips) {
+  if (nstrips > g_trace_strips) {
+    if (g_trace) cudaFree(g_trace);
+    cudaMalloc(&g_trace, sizeof(unsigned long long) * 256 * nstrips);
+    g_trace_strips = nstrips;
+  }
+  cudaMemset(g_trace, 0, sizeof(unsigned long long) * 256 * g_trace_strips);
+  return g_trace;
+}
+#endif
+
 // Packed difference form (nw_fill_d16.cuh) applies to score-only DNA-size
 // alphabets with s - 2g >= 0 for every symbol pair.
 bool d16_ok(const nw_ctx* c, const nw_scoring* sc) {
@@ -451,6 +488,32 @@ int d16_kr(const nw_ctx* c, long long m) {
   return (k >= 12 && k <= 32 && k % 2 == 0) ? (int)k : kd;
 }
 
+// Rebase period (8-step groups) of the packed H' pair sweep at KR rows per lane, or 0
+// when the form does not apply: every relative value must stay below 2^16, i.e.
+// S (32 KR + 8 reb + 160) <= 65535 with S = max(s - 2g) (nw_fill_h16.cuh).
+int h16_rebase_groups(const nw_ctx* c, const nw_scoring* sc, int kr) {
+  if (!d16_ok(c, sc)) return 0;
+  int smax = 0;
+  for (int x = 0; x < sc->K; ++x)
+    for (int y = 0; y < sc->K; ++y) smax = std::max(smax, score_of(sc, x, y) - 2 * sc->gap);
+  int reb = (int)std::max(0LL, std::min(c->opt[NW_OPT_H16_REBASE], 64LL));
+  if (reb == 0) reb = 64;
+  while (reb & (reb - 1)) reb &= reb - 1;  // power of two
+  while (reb >= 1 && (long long)smax * (32LL * kr + 8LL * reb + 160) > 65535) reb >>= 1;
+  return reb;
+}
+
+// Rows per lane of the packed H' pair sweep: NW_OPT_H16_KR, else the strip-count rule
+// of d16_kr (same lock-step argument).
+int h16_kr(const nw_ctx* c, long long m) {
+  const long long k = c->opt[NW_OPT_H16_KR];
+  if (k >= 8 && k <= 32 && k % 2 == 0 && (k >= 16 || k == 8 || k == 12)) return (int)k;
+  int kd = 32;
+  for (int q = 16; q <= 32; q += 2)
+    if ((m + 32LL * q - 1) / (32LL * q) <= 8LL * c->sm_count) { kd = q; break; }
+  return kd;
+}
+
 bool dispatch_batch(bool dirs, int pi, bool profreg, bool u16, bool d16, int packed_kr,
                     const BatchArgs& B, int grid, size_t smem, cudaStream_t st, int u16_kr = 16) {
   if (!dirs) {
@@ -499,7 +562,8 @@ nw_status init_small(nw_ctx* c, int nints, ZeroRanges zr = ZeroRanges{{nullptr, 
 nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb, long long n,
                     const nw_scoring* sc, long long* d_score, nw_tb* tb, int kr,
                     unsigned long long* ckpt = nullptr, int ck_every = 0, long long ck_stride = 0,
-                    const unsigned long long* top_row = nullptr, unsigned top_tag = 0);
+                    const unsigned long long* top_row = nullptr, unsigned top_tag = 0,
+                    int h16_reb = 0);
 
 bool cblock_dist_applies(const nw_ctx* c, long long m, long long n, const nw_scoring* sc);
 nw_status cblock_dist(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b, long long n,
@@ -572,7 +636,7 @@ namespace {
 nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb, long long n,
                     const nw_scoring* sc, long long* d_score, nw_tb* tb, int kr,
                     unsigned long long* ckpt, int ck_every, long long ck_stride,
-                    const unsigned long long* top_row, unsigned top_tag) {
+                    const unsigned long long* top_row, unsigned top_tag, int h16_reb) {
   const int R = 32 * kr;
   const int nstrips = (int)((m + R - 1) / R);
   const bool dirs = tb != nullptr;
@@ -600,7 +664,21 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     }
     const bool profreg = sc->K <= 4;
     const size_t smem = profreg ? 0 : (size_t)sc->K * R;
+    const bool h16 = !dirs && !ckpt && h16_reb > 0;
     const bool d16 = !dirs && (kr >= 12 || (!ckpt && c->opt[NW_OPT_D16_FORCE] && d16_ok(c, sc)));
+    if (h16) {  // selector table of the packed H' sweep over cb[-PAD, n + PAD) (FillArgs::sel)
+      const long long ls = n + 2 * PAD;
+      st = grow(c, c->d_sel16, c->sel16_cap, sizeof(uint16_t) * (size_t)ls);
+      if (st) return st;
+      const int blocks = (int)std::min<long long>((ls - 1 + 255) / 256, (long long)c->sm_count * 8);
+      k_sel16<<<std::max(blocks, 1), 256, 0, c->stream>>>(cb - PAD + 1, ls - 1, c->d_sel16 + 1);
+      LAUNCHED(c);
+      A.sel = c->d_sel16 + PAD;
+      A.reb_groups = h16_reb;
+#ifdef NW_TRACE
+      A.trace = nw_trace_buffer(nstrips);
+#endif
+    }
     // persistent grid: one warp per CTA, at most the resident capacity
     int per_sm = 16;
     int grid = std::min<long long>(nstrips, (long long)c->sm_count * per_sm);
@@ -608,8 +686,10 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     bool ok;
     {
       KernelTimer kt(c, 0);
-      ok = dispatch_fill(dirs, pi, kr, profreg, A, grid, smem, c->stream, d16,
-                         c->opt[NW_OPT_D16_CHAINS] == 2 && !ckpt);
+      if (h16) ok = dispatch_fill_h16(kr, A, grid, c->stream);
+      else
+        ok = dispatch_fill(dirs, pi, kr, profreg, A, grid, smem, c->stream, d16,
+                           c->opt[NW_OPT_D16_CHAINS] == 2 && !ckpt);
     }
     if (!ok) return fail(c, NW_E_INVAL, "bad tie order");
     LAUNCHED(c);
@@ -750,6 +830,15 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
     const int f = (int)std::max(4LL, std::min(c->opt[NW_OPT_D16_FORCE], 32LL));
     kr = (f >= 12 && f <= 32 && f % 2 == 0) ? f : (f >= 32 ? 32 : (f >= 16 ? 16 : (f >= 8 ? 8 : 4)));
   }
+  // packed H' with a moving base: the default for tall score-only
+  // pairs; NW_OPT_H16_KR forces it at any size (tests)
+  int h16_reb = 0;
+  const bool h16_tall = m >= 32LL * 16 * 150 && c->opt[NW_OPT_PAIR_FORM] != 1 && !c->opt[NW_OPT_D16_FORCE];
+  if (!want_dirs && d16_ok(c, sc) && (h16_tall || c->opt[NW_OPT_H16_KR])) {
+    const int kh = h16_kr(c, m);
+    h16_reb = h16_rebase_groups(c, sc, kh);
+    if (h16_reb > 0) kr = kh;
+  }
   st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
   if (st) return st;
   // two ring slots (+ a sink slot for the NW_OPT_TEST_WITHHOLD hook)
@@ -771,7 +860,7 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
     if (st) return st;
   }
   long long* d_score = host ? c->d_score : score_out;
-  st = pair_core(c, ca, m, cb, n, sc, d_score, tb, kr);
+  st = pair_core(c, ca, m, cb, n, sc, d_score, tb, kr, nullptr, 0, 0, nullptr, 0, h16_reb);
   if (st) {
     if (tb) nw_tb_free(tb);
     return st;
@@ -795,6 +884,14 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
 // ======================= exported C ABI =======================
 
 extern "C" {
+
+#ifdef NW_TRACE
+int nw_debug_trace(unsigned long long* out, int max_strips) {
+  const int k = std::min(max_strips, g_trace_strips);
+  if (g_trace && k > 0) cudaMemcpy(out, g_trace, sizeof(unsigned long long) * 256 * k, cudaMemcpyDeviceToHost);
+  return k;
+}
+#endif
 
 const char* nw_strerror(nw_status st) {
   switch (st) {

@@ -59,6 +59,8 @@ struct FillArgs {
   const uint16_t* sel = nullptr;      // packed sweeps (batch): selector table aligned with b, sel[i] =
                                       //   (17 b[i] + 128) | (17 b[i-1] + 196) << 8 (prmt2 of PA/PB)
   long long watchdog = 1LL << 28;     // re-polls of a late boundary chunk before *err is raised
+  unsigned long long* trace = nullptr;  // experiment builds only (NW_TRACE): per-strip timestamps
+  int reb_groups = 64;                // h16 single-pair sweep: rebase period (8-step groups, power of 2)
   int withhold = 0;                   // test only (NW_OPT_TEST_WITHHOLD): strip withhold-1 writes its
   void* sink = nullptr;               //   bottom row to `sink` instead, so its consumer never sees it
 };

@@ -1,0 +1,199 @@
+// nw_fill_h16.cuh -- score-only single-pair sweep in the shifted form H' with two
+// cells per register and a moving per-strip base.
+//
+// Same recurrence as nw_fill.cuh (Eq. 1, reading R1, in the shifted form
+// H' = H - g(i+j) >= 0 of DESIGN.md §3.1) and the same packed half-row layout as
+// nw_fill16.cuh: lane l owns KR = 2h rows, packed register k holds row k (low half)
+// and row k+h (high half, one column behind), lanes skewed by two steps, and per two
+// cells the update is one PRMT (both profile bytes), one 32-bit add (diag + s', no
+// carry crosses the halves) and one VIMNMX3.U16x2 -- one dependent link per packed
+// row instead of the two of the difference form (nw_fill_d16.cuh: VIMNMX3 then IADD).
+//
+// H' itself grows without bound (up to min(m,n) * max(s')), so a strip keeps its
+// values relative to a warp-uniform base B (int32): every register holds H' - B.
+// Every `reb` 8-step groups the warp takes the minimum live value (a warp min of the
+// lanes' minima) and moves B up by it. H' is non-decreasing down a column and along a
+// row, and every live value of the strip lies between H'(top-1, jT0 - 64) and
+// H'(bottom, jT0) (jT0 = lane 0's column), so with S = max(s') the relative values
+// stay below S * (R + 65 + 8 * reb) + S, which the host keeps <= 65535 (h16_ok). The
+// strips still exchange ABSOLUTE H' through the tagged 64-bit entries of nw_fill.cuh:
+// lane 31 adds B when it publishes, lane 0's chunk subtracts B when it is taken.
+// Border values (column 0, H'(i,0) = 0) are only present while B = 0: they are the
+// live minimum until every half of the warp has left column 0.
+#pragma once
+#include "nw_fill.cuh"
+#include "nw_fill16.cuh"
+
+namespace nwk {
+
+template <int KR>
+struct H16State {
+  uint32_t PA[KR / 2], PB[KR / 2];  // profile words of rows k and k+h (s' bytes per code)
+  uint32_t Hp[KR / 2];              // H' - B of packed row k at the previous step
+  uint32_t up0_prev;                // up(0) of the previous step (diag of packed 0)
+  int chunk_cur, chunk_nxt;         // boundary H' (absolute) of 8 columns, lane q < 8: column t0+1+q
+  int base;                         // B (warp-uniform)
+  uint32_t sel_nxt[8];              // selector table entries of the next group (prefetched)
+};
+
+// 8 steps (t0 % 8 == 0). MASKED groups hold a half outside [1, n] or the cell (m, n).
+template <int KR, bool MASKED>
+__device__ __forceinline__ void h16_group(H16State<KR>& st, const StripCtx& C, const uint16_t* sel,
+                                          int t0) {
+  constexpr int H = KR / 2;
+  const int lane = C.lane, n = C.n;
+  // selectors of this group (prefetched one group ahead: a lone warp otherwise waits
+  // for the first of them every group, ncu) and the loads of the next group's;
+  // entry jT - 1 holds the codes of columns jT (low half) and jT - 1 (high half)
+  uint32_t scur[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) scur[q] = st.sel_nxt[q];
+  const uint16_t* sp16 = sel + (t0 + 8 - 2 * lane);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) st.sel_nxt[q] = __ldg(sp16 + q);
+  unsigned long long* op = static_cast<unsigned long long*>(C.bnd_out) + (t0 - 62);
+  // lane 0 takes the boundary values relative to B (columns beyond n: 0, never read
+  // by a cell inside the grid, and small enough to keep every half in range)
+  const int jc = t0 + 1 + lane;
+  const int crel = (lane < 8 && jc <= n) ? st.chunk_cur - st.base : 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int t = t0 + q;
+    const uint32_t s = scur[q];
+    const int recv = __shfl_up_sync(FULL, (int)st.Hp[H - 1], 1);
+    const int bval = __shfl_sync(FULL, crel, q);
+    // up(0): low = lane l-1's bottom row at jT (its packed h-1 high half, one step old;
+    // for lane 0 the boundary row), high = own packed h-1 low half of the previous step
+    const uint32_t upsrc = (lane == 0) ? ((uint32_t)bval << 16) : (uint32_t)recv;
+    uint32_t up = prmt2(upsrc, st.Hp[H - 1], 0x5432u);
+    uint32_t diag = st.up0_prev;
+    st.up0_prev = up;
+    const int jT = t - 2 * lane + 1;
+    uint32_t mask = 0xffffffffu;
+    if (MASKED) mask = (jT >= 1 ? 0x0000ffffu : 0u) | (jT >= 2 ? 0xffff0000u : 0u);
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      const uint32_t sp = prmt2(st.PA[k], st.PB[k], s);
+      const uint32_t left = st.Hp[k];
+      uint32_t h = __vimax3_u16x2(diag + sp, left, up);
+      if (MASKED) h &= mask;  // border column H'(i, 0) = 0 until each half starts (B = 0 then)
+      diag = left;
+      up = h;
+      st.Hp[k] = h;
+    }
+    const int jB = jT - 1;
+    if (lane == 31 && (!MASKED || (jB >= 1 && jB <= n))) {
+      const int hb = (int)(st.Hp[H - 1] >> 16) + st.base;  // bottom row H' at jB, absolute
+      unsigned long long v;
+      asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "r"(hb), "r"(C.tag_out));
+      st_relaxed_u64(op + q, v);
+    }
+    if (MASKED && C.hm_lane == lane && C.hm_t == t) {  // H'(m, n), absolute
+      const int hk = C.hm_r >= H ? C.hm_r - H : C.hm_r;
+      uint32_t w = 0;
+#pragma unroll
+      for (int k = 0; k < H; ++k) w = (k == hk) ? st.Hp[k] : w;  // selects: Hp stays in registers
+      *C.hm = (int)(C.hm_r >= H ? (w >> 16) : (w & 0xffffu)) + st.base;
+    }
+  }
+}
+
+// Moves B up by the warp's minimum live relative value (all halves of Hp and up0_prev).
+template <int KR>
+__device__ __forceinline__ void h16_rebase(H16State<KR>& st) {
+  constexpr int H = KR / 2;
+  uint32_t mn = st.up0_prev;
+#pragma unroll
+  for (int k = 0; k < H; ++k) mn = __vminu2(mn, st.Hp[k]);
+  int d = (int)min(mn & 0xffffu, mn >> 16);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d = min(d, __shfl_xor_sync(FULL, d, o));
+  const uint32_t dd = (uint32_t)d * 0x00010001u;  // every half >= d: no borrow crosses
+#pragma unroll
+  for (int k = 0; k < H; ++k) st.Hp[k] -= dd;
+  st.up0_prev -= dd;
+  st.base += d;
+}
+
+// One strip, score-only, MULTIWARP (tagged 64-bit entries). A.sel: the selector
+// table of nw_fill16.cuh aligned with b; A.reb_groups: rebase period in 8-step groups
+// (a power of two).
+template <int KR>
+__device__ __forceinline__ void strip_sweep_h16(const FillArgs& A, int s, int lane) {
+  static_assert(KR % 2 == 0 && KR <= 32, "KR must be even");
+  constexpr int H = KR / 2;
+  constexpr int R = 32 * KR;
+  const int n = A.n;
+  const int ia0 = s * R + lane * KR;
+  H16State<KR> st;
+#pragma unroll
+  for (int k = 0; k < H; ++k) {
+    const int a0 = A.a[ia0 + k], a1 = A.a[ia0 + k + H];
+    uint32_t w0 = 0, w1 = 0;
+    for (int c = 0; c < A.K; ++c) {
+      w0 |= ((uint32_t)(uint8_t)A.prof[a0 * A.K + c]) << (8 * c);
+      w1 |= ((uint32_t)(uint8_t)A.prof[a1 * A.K + c]) << (8 * c);
+    }
+    st.PA[k] = w0;
+    st.PB[k] = w1;
+    st.Hp[k] = 0;
+  }
+  st.up0_prev = 0;
+  st.base = 0;
+  st.chunk_cur = st.chunk_nxt = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) st.sel_nxt[q] = __ldg(A.sel + (q - 2 * lane));  // group 0
+  StripCtx C;
+  C.tag_in = (unsigned)s;
+  C.tag_out = (unsigned)s + 1;
+  C.b = A.b;
+  C.sprof = nullptr;
+  char* bnd = static_cast<char*>(A.bnd);
+  C.bnd_in = (s > 0) ? bnd + 8 * (size_t)((s % A.nslots) * A.bstride) : nullptr;
+  C.bnd_out = bnd + 8 * (size_t)(((s + 1) % A.nslots) * A.bstride);
+  if (s + 1 == A.withhold) C.bnd_out = A.sink;
+  C.dir_base = nullptr;
+  C.err = A.err;
+  C.poll_ns = A.poll_ns;
+  C.watchdog = A.watchdog;
+  C.hm = A.hm;
+  C.n = n;
+  C.s = s;
+  C.lane = lane;
+  // where H'(m, n) lives: row rr of this strip -> lane, packed row, half; column n
+  C.hm_lane = -1;
+  C.hm_r = 0;
+  C.hm_t = 0;
+  if ((A.m - 1) / R == s) {
+    const int rr = (A.m - 1) % R;
+    C.hm_lane = rr / KR;
+    C.hm_r = rr % KR;  // packed row hm_r % h, high half iff hm_r >= h
+    C.hm_t = n - 1 + 2 * C.hm_lane + (C.hm_r >= H ? 1 : 0);
+  }
+  if (s > 0) st.chunk_nxt = chunk_verify<true>(C, 0, chunk_issue<true>(C, 0));
+  const int ngrp = (n + 63 + 7) / 8;  // last lane's high half reaches column n at t = n + 62
+  const int rmask = A.reb_groups - 1;  // power of two
+#pragma unroll 1
+  for (int g = 0; g < ngrp; ++g) {
+    const int t0 = g * 8;
+    if ((g & rmask) == 0 && g > 0) h16_rebase<KR>(st);
+#ifdef NW_TRACE
+    if (A.trace && lane == 0 && (g & 1023) == 0 && (g >> 10) < 256) {
+      unsigned long long ts;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+      A.trace[(size_t)s * 256 + (g >> 10)] = ts;
+    }
+#endif
+    st.chunk_cur = st.chunk_nxt;
+    const bool more = s > 0 && t0 + 8 < n;
+    unsigned long long raw = 0;
+    if (more) raw = chunk_issue<true>(C, t0 + 8);
+    const bool masked = t0 < 64 || t0 + 7 >= n - 1;
+    if (masked) h16_group<KR, true>(st, C, A.sel, t0);
+    else h16_group<KR, false>(st, C, A.sel, t0);
+    if (more) st.chunk_nxt = chunk_verify<true>(C, t0 + 8, raw);
+  }
+  __syncwarp();
+}
+
+}  // namespace nwk

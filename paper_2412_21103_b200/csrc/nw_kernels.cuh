@@ -15,6 +15,7 @@
 #include "nw_cblock.cuh"
 #include "nw_fill_d16.cuh"
 #include "nw_fill_d16dir.cuh"
+#include "nw_fill_h16.cuh"
 
 namespace nwk {
 
@@ -86,7 +87,8 @@ __global__ void k_sel16(const uint8_t* __restrict__ codes, long long len, uint16
 // D16 (score-only, K <= 4, s - 2g >= 0): the packed difference-form sweep of
 // nw_fill_d16.cuh (KR rows per lane, two per register) instead of strip_sweep.
 // D16: 0 = int32 strip_sweep, 1 = packed difference form (one chain per lane),
-// 2 = packed difference form with two chains per lane (strip_sweep_d16x2).
+// 2 = packed difference form with two chains per lane (strip_sweep_d16x2),
+// 3 = packed H' with a moving per-strip base (strip_sweep_h16, nw_fill_h16.cuh).
 template <int KR, bool DIRS, bool PROFREG, int PI, int D16 = 0>
 __global__ void __launch_bounds__(32) k_fill_pair(FillArgs A) {
   extern __shared__ __align__(16) int8_t smem[];
@@ -96,7 +98,8 @@ __global__ void __launch_bounds__(32) k_fill_pair(FillArgs A) {
     if (lane == 0) s = atomicAdd(A.ticket, 1);
     s = __shfl_sync(FULL, s, 0);
     if (s >= A.nstrips) break;
-    if constexpr (D16 == 2) strip_sweep_d16x2<KR, true>(A, s, lane);
+    if constexpr (D16 == 3) strip_sweep_h16<KR>(A, s, lane);
+    else if constexpr (D16 == 2) strip_sweep_d16x2<KR, true>(A, s, lane);
     else if constexpr (D16 == 1) strip_sweep_d16<KR, true>(A, s, lane);
     else strip_sweep<KR, DIRS, PROFREG, PI, true>(A, s, lane, smem);
   }

@@ -1,0 +1,99 @@
+// Microbenchmark of the packed H' step (nw_fill_h16.cuh) without memory traffic:
+// cycles per step of one warp's sweep of KR rows per lane (KR/2 packed registers:
+// PRMT + IADD + VIMNMX3.U16x2 each, the shuffle of the lane above's bottom row),
+// with W warps per SM sub-partition and C independent strips interleaved in one
+// warp's instruction stream (C = 2: two chains, as two far-apart strips per warp).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/h16_step tools/h16_step.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t prmt2(uint32_t x, uint32_t y, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(y), "r"(sel));
+  return d;
+}
+
+template <int KR, int C>
+__global__ void k_step(uint32_t* out, long long* cyc, int steps) {
+  constexpr int H = KR / 2;
+  const int lane = threadIdx.x & 31;
+  uint32_t PA[C][H], PB[C][H], Hp[C][H], up0p[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      PA[c][k] = 0x01030103u * (lane + k + c);
+      PB[c][k] = 0x03010301u * (lane + k + 2 * c);
+      Hp[c][k] = 0;
+    }
+    up0p[c] = 0;
+  }
+  uint32_t selx = 0x2c80u + lane;
+  __syncthreads();
+  const long long t0 = clock64();
+#pragma unroll 1
+  for (int t = 0; t < steps; t += 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t s = selx + (q << 4);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int recv = __shfl_up_sync(0xffffffffu, (int)Hp[c][H - 1], 1);
+        const uint32_t upsrc = lane == 0 ? (uint32_t)(t + q) << 16 : (uint32_t)recv;
+        uint32_t up = prmt2(upsrc, Hp[c][H - 1], 0x5432u);
+        uint32_t diag = up0p[c];
+        up0p[c] = up;
+#pragma unroll
+        for (int k = 0; k < H; ++k) {
+          const uint32_t sp = prmt2(PA[c][k], PB[c][k], s);
+          const uint32_t left = Hp[c][k];
+          const uint32_t h = __vimax3_u16x2(diag + sp, left, up);
+          diag = left;
+          up = h;
+          Hp[c][k] = h;
+        }
+      }
+    }
+    selx ^= 0x1111u;
+  }
+  const long long t1 = clock64();
+  uint32_t acc = 0;
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+#pragma unroll
+    for (int k = 0; k < H; ++k) acc += Hp[c][k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int KR, int C>
+void run(uint32_t* out, long long* cyc, int W) {
+  const int steps = 1 << 15;
+  k_step<KR, C><<<1, 128 * W>>>(out, cyc, steps);
+  k_step<KR, C><<<1, 128 * W>>>(out, cyc, steps);
+  cudaDeviceSynchronize();
+  long long c = 0;
+  cudaMemcpy(&c, cyc, sizeof c, cudaMemcpyDeviceToHost);
+  const double cps = (double)c / steps;
+  // cells per cycle per SM sub-partition: W warps x C strips x 32 lanes x KR rows per step
+  printf("  \"kr%d_c%d_w%d\": {\"cycles_per_step\": %.1f, \"cells_per_cycle_smsp\": %.2f},\n", KR, C, W,
+         cps, W * C * 32.0 * KR / cps);
+}
+
+int main() {
+  uint32_t* out;
+  long long* cyc;
+  cudaMalloc(&out, 4 * 4096);
+  cudaMalloc(&cyc, 8 * 16);
+  printf("{\n");
+  for (int W : {1, 2, 3, 4}) {
+    run<28, 1>(out, cyc, W);
+    run<14, 2>(out, cyc, W);
+    run<28, 2>(out, cyc, W);
+    run<16, 1>(out, cyc, W);
+    run<32, 1>(out, cyc, W);
+  }
+  printf("  \"end\": 0\n}\n");
+  return 0;
+}
