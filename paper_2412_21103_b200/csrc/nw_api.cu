@@ -517,7 +517,8 @@ int h16_kr(const nw_ctx* c, long long m) {
 bool dispatch_batch(bool dirs, int pi, bool profreg, bool u16, bool d16, int packed_kr,
                     const BatchArgs& B, int grid, size_t smem, cudaStream_t st, int u16_kr = 16) {
   if (!dirs) {
-    if (u16 && u16_kr == 32) launch_batch_t<KR_BATCH, false, true, 123, 1, 32>(B, grid, smem, st);
+    if (u16 && u16_kr == 1) launch_batch_t<KR_BATCH, false, true, 123, 4, 32>(B, grid, smem, st);
+    else if (u16 && u16_kr == 32) launch_batch_t<KR_BATCH, false, true, 123, 1, 32>(B, grid, smem, st);
     else if (u16 && u16_kr == 8) launch_batch_t<KR_BATCH, false, true, 123, 1, 8>(B, grid, smem, st);
     else if (u16) launch_batch_t<KR_BATCH, false, true, 123, 1>(B, grid, smem, st);
     else if (d16) launch_batch_t<KR_BATCH, false, true, 123, 2>(B, grid, smem, st);
@@ -2114,10 +2115,11 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
       if (!ls.empty()) {
         std::nth_element(ls.begin(), ls.begin() + ls.size() / 2, ls.end());
         const long long med = ls[ls.size() / 2];
-        u16_kr = med >= 1024 ? 32 : (med >= 384 ? 16 : 8);
+        u16_kr = med >= 1024 ? 1 : (med >= 384 ? 16 : 8);  // 1: each pair at 32 or 16 rows per lane
       }
-      if (c->opt[NW_OPT_BATCH_U16_KR] == 8 || c->opt[NW_OPT_BATCH_U16_KR] == 16 || c->opt[NW_OPT_BATCH_U16_KR] == 32)
-        u16_kr = (int)c->opt[NW_OPT_BATCH_U16_KR];
+      const long long o = c->opt[NW_OPT_BATCH_U16_KR];
+      if (o == 1 || o == 8 || o == 16 || o == 32) u16_kr = (int)o;
+      if (c->opt[NW_OPT_BATCH_MIX_W] > 0) B.mix_w16 = (int)std::min(c->opt[NW_OPT_BATCH_MIX_W], 100000LL);
     }
     ok = dispatch_batch(tbk, pi, profreg, u16, d16, packed_kr, B, grid, smem, c->stream, u16_kr);
   }

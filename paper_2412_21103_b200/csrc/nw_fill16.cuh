@@ -34,13 +34,17 @@ struct U16State {
   int chunk;          // boundary values, lane q holds column t0+1+q
 };
 
-// One 32-step block (t0 % 32 == 0). MASKED blocks contain a half outside
-// [1, n] for some lane, or the H'(m, n) cell.
-template <int KR, bool MASKED>
+// One 32-step block (t0 % 32 == 0). BORDER blocks (t0 < 64) hold halves left of
+// column 1 (and, for n < 64, right of column n). A half at column <= 0 must stay 0
+// (H'(i, 0) = 0): its inputs there (left, up, diag) are 0 by induction, so it is
+// enough that its s' is 0, which the selector override gives (nibble 8 / 12 = sign
+// replication of byte 0 of PA / PB, s' >= 0 -> 0x00) -- 2 instructions per step
+// instead of a mask on every packed register. Past column n nothing needs masking:
+// the cells there are never read, and the boundary row has >= 64 entries of slack.
+template <int KR, bool BORDER>
 __device__ __forceinline__ void u16_block(U16State& st, uint32_t (&PA)[KR / 2],
                                           uint32_t (&PB)[KR / 2], uint32_t (&Hp)[KR / 2],
-                                          const FillArgs& A, int lane, int t0, int* bnd_out,
-                                          int hm_lane, int hm_k, int hm_hi, int hm_t) {
+                                          const FillArgs& A, int lane, int t0, int* bnd_out) {
   constexpr int H = KR / 2;
   const int n = A.n;
   // s' selector of step t: nibbles (bT, bT|8, 4+bB, 12+bB) -> byte bT of PA zero-extended
@@ -53,7 +57,7 @@ __device__ __forceinline__ void u16_block(U16State& st, uint32_t (&PA)[KR / 2],
 #pragma unroll 8
   for (int q = 0; q < 32; ++q) {
     const int t = t0 + q;
-    const uint32_t sel = __ldg(sp16 + q);
+    uint32_t sel = __ldg(sp16 + q);
     const int recv = __shfl_up_sync(FULL, (int)st.send, 1);
     const int bval = __shfl_sync(FULL, st.chunk, q);
     // up(0): low = lane l-1's bottom row at jT (its packed h-1 high half),
@@ -62,11 +66,9 @@ __device__ __forceinline__ void u16_block(U16State& st, uint32_t (&PA)[KR / 2],
     uint32_t up = prmt2(upsrc, Hp[H - 1], 0x5432u);
     uint32_t diag = st.up0_prev;
     st.up0_prev = up;
-    uint32_t mask = 0xffffffffu;
-    int jT = 0;
-    if (MASKED) {  // low half active iff jT >= 1, high half iff jB = jT - 1 >= 1
-      jT = t - 2 * lane + 1;
-      mask = (jT >= 1 ? 0x0000ffffu : 0u) | (jT >= 2 ? 0xffff0000u : 0u);
+    const int jT = t - 2 * lane + 1;
+    if (BORDER) {  // low half left of column 1 iff jT < 1, high half iff jB = jT - 1 < 1
+      if (jT < 2) sel = (jT < 1) ? 0xcc88u : ((sel & 0xffu) | 0xcc00u);
     }
 #pragma unroll
     for (int k = 0; k < H; ++k) {
@@ -75,29 +77,23 @@ __device__ __forceinline__ void u16_block(U16State& st, uint32_t (&PA)[KR / 2],
       // diag + s' as a plain 32-bit add (both halves < 2^16 - max s': no carry crosses),
       // which ptxas may issue on the FMA pipe, then one 3-input max on the ALU pipe:
       // 4 ALU-pipe cycles per two cells instead of 5 (PRMT 2 + VIADDMNMX 2 + VIMNMX 1)
-      uint32_t h = __vimax3_u16x2(diag + sp, left, up);
-      if (MASKED) h &= mask;  // border column H'(i, 0) = 0 until each half starts
+      const uint32_t h = __vimax3_u16x2(diag + sp, left, up);
       diag = left;
       up = h;
       Hp[k] = h;
     }
     st.send = Hp[H - 1];
-    if (MASKED) {
-      const int jB = jT - 1;
-      if (lane == 31 && jB >= 1 && jB <= n) op[q] = (int)(st.send >> 16);
-      if (lane == hm_lane && t == hm_t) {
-#pragma unroll
-        for (int k = 0; k < H; ++k)
-          if (k == hm_k) *A.hm = (int)(hm_hi ? (Hp[k] >> 16) : (Hp[k] & 0xffffu));
-      }
-    } else {
-      if (lane == 31) op[q] = (int)(st.send >> 16);
-    }
+    const int jB = jT - 1;
+    if (lane == 31 && (!BORDER || (jB >= 1 && jB <= n + 31))) op[q] = (int)(st.send >> 16);
   }
 }
 
 // One strip, score-only, packed. Same FillArgs / boundary conventions as
-// strip_sweep<..., MULTIWARP = false> (the batch kernel's per-warp strips).
+// strip_sweep<..., MULTIWARP = false> (the batch kernel's per-warp strips). Rows past
+// m get an all-zero profile (s' = 0): such a row repeats the row above exactly
+// (H'(i+1, j) = max(H'(i, j-1), H'(i, j), H'(i+1, j-1)) = H'(i, j), H' being
+// non-decreasing along a row), so the last strip's bottom row is H'(m, .) and H'(m, n)
+// is read from the boundary row after the sweep (no per-step capture).
 template <int KR>
 __device__ __forceinline__ void strip_sweep_u16(const FillArgs& A, int s, int lane) {
   static_assert(KR % 2 == 0 && KR <= 32, "KR must be even");
@@ -115,22 +111,12 @@ __device__ __forceinline__ void strip_sweep_u16(const FillArgs& A, int s, int la
       w0 |= ((uint32_t)(uint8_t)A.prof[a0 * A.K + c]) << (8 * c);
       w1 |= ((uint32_t)(uint8_t)A.prof[a1 * A.K + c]) << (8 * c);
     }
-    PA[k] = w0;
-    PB[k] = w1;
+    PA[k] = (ia0 + k < A.m) ? w0 : 0u;
+    PB[k] = (ia0 + k + H < A.m) ? w1 : 0u;
     Hp[k] = 0;
   }
   const int* bnd_in = (s > 0) ? static_cast<const int*>(A.bnd) + (size_t)(s % A.nslots) * A.bstride : nullptr;
   int* bnd_out = static_cast<int*>(A.bnd) + (size_t)((s + 1) % A.nslots) * A.bstride;
-  // where H'(m, n) lives: row rr of this strip -> lane, packed k, half; column n
-  int hm_lane = -1, hm_k = 0, hm_hi = 0, hm_t = 0;
-  if ((A.m - 1) / R == s) {
-    const int rr = (A.m - 1) % R;
-    hm_lane = rr / KR;
-    const int r = rr % KR;
-    hm_hi = r >= H;
-    hm_k = hm_hi ? r - H : r;
-    hm_t = n - 1 + 2 * hm_lane + hm_hi;  // jT = n (low) or jB = n (high)
-  }
   U16State st;
   st.up0_prev = 0;
   st.send = 0;
@@ -150,12 +136,11 @@ __device__ __forceinline__ void strip_sweep_u16(const FillArgs& A, int s, int la
       const int jj = t0 + 33 + lane;
       chunk_nxt = (jj <= n) ? bnd_in[jj] : 0;
     }
-    const bool masked = t0 < 64 || t0 + 31 >= n - 1;
-    if (masked)
-      u16_block<KR, true>(st, PA, PB, Hp, A, lane, t0, bnd_out, hm_lane, hm_k, hm_hi, hm_t);
-    else
-      u16_block<KR, false>(st, PA, PB, Hp, A, lane, t0, bnd_out, hm_lane, hm_k, hm_hi, hm_t);
+    if (t0 < 64) u16_block<KR, true>(st, PA, PB, Hp, A, lane, t0, bnd_out);
+    else u16_block<KR, false>(st, PA, PB, Hp, A, lane, t0, bnd_out);
   }
+  __syncwarp();
+  if (s == A.nstrips - 1 && lane == 0) *A.hm = bnd_out[n];  // H'(m, n): the bottom row at n
   __syncwarp();
 }
 

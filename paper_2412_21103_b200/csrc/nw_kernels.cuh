@@ -475,6 +475,7 @@ struct BatchArgs {
   int X, Y, Z;
   int* err;
   int transpose_ok;        // score-only, s symmetric: a pair may be filled transposed
+  int mix_w16 = 1100;      // PACKED 4: relative cost (x1000) of a 512-row strip cell vs a 1,024-row one
   // Two-phase traceback (the packed sweep, PACKED == 3): the fill
   // keeps every pair's decision words at tdirs + tdir_off[task] (32-bit words) and
   // k_batch_walk walks them after the fill, one thread per pair.
@@ -528,7 +529,8 @@ __device__ __forceinline__ void task_pair(const BatchArgs& B, long long task, in
 // PACKED (s - 2g >= 0), KR16 rows per lane, two per register:
 // 1 = the H' half-row sweep of nw_fill16.cuh (score-only, K <= 4, every H' < 2^16),
 // 2 = the difference-form sweep of nw_fill_d16.cuh (score-only, K <= 4, any length),
-// 3 = the difference-form sweep with decision flags of nw_fill_d16dir.cuh (DIRS).
+// 3 = the difference-form sweep with decision flags of nw_fill_d16dir.cuh (DIRS),
+// 4 = as 1, each pair at 32 or 16 rows per lane (whichever sweeps less weighted area).
 template <int KR16, bool COHERENT>
 __device__ __forceinline__ void walk_lanes(const BatchArgs& B, long long task, bool act, int lane);
 
@@ -544,7 +546,7 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
   // the strips of a pair run one after another in this warp; the packed H' sweep reads
   // the row above (32 columns ahead) before overwriting it (62 columns behind), so one
   // row in shared memory suffices (bnd_smem; global scratch otherwise)
-  int* bnd = (PACKED == 1 && B.bnd_smem)
+  int* bnd = ((PACKED == 1 || PACKED == 4) && B.bnd_smem)
                  ? reinterpret_cast<int*>(smem + B.bnd_smem_off) + wib * B.bstride
                  : B.wbnd + gw * 2 * B.bstride;
   uint16_t* wd = DIRS ? B.wdirs + gw * B.dstride : nullptr;
@@ -562,7 +564,29 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       const long long to = ao; ao = bo; bo = to;
       const int tm = m; m = n; n = tm;
     }
-    if (!DIRS && B.transpose_ok) {
+    bool half = false;  // PACKED 4: this pair runs 512-row strips (strip_sweep_u16<16>)
+    if (PACKED == 4) {
+      // the orientation and strip height (1,024 or 512 rows) with the least weighted swept
+      // area: strips x height x (columns + lane skew), 512-row cells weighted mix_w16/1000
+      // (their per-cell overhead is higher); transposing needs the symmetric s
+      auto cost = [&](int rows, int cols, int rs, long long w) {
+        return (long long)((rows + rs - 1) / rs) * rs * (cols + 64) * w;
+      };
+      long long best = cost(m, n, 1024, 1000);
+      int pick = 0;
+      const long long c1 = cost(m, n, 512, B.mix_w16);
+      if (c1 < best) { best = c1; pick = 1; }
+      if (B.transpose_ok) {
+        const long long c2 = cost(n, m, 1024, 1000), c3 = cost(n, m, 512, B.mix_w16);
+        if (c2 < best) { best = c2; pick = 2; }
+        if (c3 < best) { best = c3; pick = 3; }
+      }
+      half = pick & 1;
+      if (pick >= 2) {
+        const long long to = ao; ao = bo; bo = to;
+        const int tm = m; m = n; n = tm;
+      }
+    } else if (!DIRS && B.transpose_ok) {
       // score-only with a symmetric s: Score(a, b) = Score(b, a) (the transpose
       // invariant of the oracle pins), so put on the rows whichever sequence wastes
       // fewer lanes of the last strip: strips x (columns + lane skew)
@@ -576,14 +600,21 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
     if (m > 0 && n > 0) {
       FillArgs A;
       A.a = B.codes + ao; A.b = B.codes + bo; A.prof = B.prof; A.K = B.K; A.sel = B.sel16 + bo;
-      constexpr int RS = PACKED ? 32 * KR16 : R;  // strip height of the sweep in use
-      A.m = m; A.n = n; A.nstrips = (m + RS - 1) / RS; A.nslots = (PACKED == 1 && B.bnd_smem) ? 1 : 2;
+      constexpr int RS = PACKED == 4 ? 1024 : PACKED ? 32 * KR16 : R;  // strip height of the sweep in use
+      A.m = m; A.n = n; A.nstrips = (m + RS - 1) / RS; A.nslots = ((PACKED == 1 || PACKED == 4) && B.bnd_smem) ? 1 : 2;
       A.bnd = bnd; A.bstride = B.bstride; A.ticket = nullptr; A.ckpt = nullptr; A.ck_every = 0; A.ck_stride = 0; A.top_row = nullptr; A.top_tag = 0;
       A.dirs = PACKED == 3 ? reinterpret_cast<uint16_t*>(B.tdirs + B.tdir_off[task]) : wd;
       A.wpl = PACKED ? (n + 63 + 7) / 8 : (n + 31 + 7) / 8;  // 8-step groups per strip
       A.hm = B.whm + gw; A.err = B.err;
       if constexpr (PACKED == 1) {
         for (int s = 0; s < A.nstrips; ++s) strip_sweep_u16<KR16>(A, s, lane);
+      } else if constexpr (PACKED == 4) {
+        if (half) {
+          A.nstrips = (m + 511) / 512;
+          for (int s = 0; s < A.nstrips; ++s) strip_sweep_u16<16>(A, s, lane);
+        } else {
+          for (int s = 0; s < A.nstrips; ++s) strip_sweep_u16<32>(A, s, lane);
+        }
       } else if constexpr (PACKED == 2) {
         if (lane == 0) *A.hm = 0;  // the difference-form sweep accumulates sum U(i, n)
         __syncwarp();

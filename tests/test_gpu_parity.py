@@ -521,10 +521,11 @@ def test_batch_traceback_device_plan(ctx, opts, host_plan):
             assert paths[k].tolist() == wops.tolist(), (k, tie)
 
 
-@pytest.mark.parametrize("kr", [0, 8, 16, 32])
+@pytest.mark.parametrize("kr", [0, 1, 8, 16, 32])
 def test_batch_score_only_u16_rows_per_lane(ctx, opts, kr):
-    """The packed H' batch sweep at 8/16/32 rows per lane (0: chosen by the median
-    length): pair lengths straddle the 256/512/1,024-row strip edges, empty sequences."""
+    """The packed H' batch sweep at 8/16/32 rows per lane (1: 32 or 16 per pair; 0: chosen
+    by the median length): pair lengths straddle the 256/512/1,024-row strip edges,
+    empty sequences."""
     opts(ctx, "batch_u16_kr", kr)
     ss = nwgen.random_set(80 + kr, 26, 0, 2100)
     pairs = nwgen.all_pairs(ss.nseq)
@@ -533,3 +534,18 @@ def test_batch_score_only_u16_rows_per_lane(ctx, opts, kr):
     rev = pairs[::3, ::-1].copy()
     assert nwb.nw_align_batch(ctx, ss.residues, ss.offs, rev, nwgen.PAPER_DNA).tolist() == \
         oracle.batch_score(ss.residues, ss.offs, rev, nwgen.PAPER_DNA).tolist()
+
+
+@pytest.mark.parametrize("w", [1, 1100, 100000])
+def test_batch_u16_mixed_strip_heights(ctx, opts, w):
+    """Mixed 1,024/512-row strips (batch_u16_kr 1) with the weight pushing every pair to
+    512 rows (w = 1), the default, or to 1,024 rows (w = 100000); a symmetric scoring (the
+    orientation may flip) and an asymmetric substitution matrix (it may not)."""
+    opts(ctx, "batch_u16_kr", 1)
+    opts(ctx, "batch_mix_w", w)
+    ss = nwgen.random_set(9900 + w % 97, 24, 0, 2300)
+    pairs = nwgen.all_pairs(ss.nseq)
+    asym = np.array([[3, 0, 1, 0], [1, 2, 0, 0], [0, 1, 4, 2], [2, 0, 0, 3]], dtype=np.int32)
+    for sc in (nwgen.PAPER_DNA, nwgen.Scoring(gap=-1, subst=asym)):
+        want = oracle.batch_score(ss.residues, ss.offs, pairs, sc)
+        assert nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, sc).tolist() == want.tolist(), w

@@ -1,4 +1,5 @@
-"""C3 batch fill with 8/16/32 rows per lane in the packed H' sweep (not a bench line)."""
+"""C3 batch fill with 8/16/32 rows per lane in the packed H' sweep, or mixed 32/16 per
+pair at several weights (not a bench line). usage: exp_u16kr.py [kr:w,...] [out.json]"""
 import json, sys
 sys.path.insert(0, '.')
 import torch, numpy as np
@@ -12,13 +13,17 @@ out = {}
 rng = np.random.Generator(np.random.PCG64(1)); idx = np.sort(rng.choice(P, 64, replace=False))
 allp = nwgen.all_pairs(ss.nseq)
 want = oracle.batch_score(ss.residues, ss.offs, allp[idx], nwgen.PAPER_DNA)
-for kr in (16, 32, 8):
+cfgs = sys.argv[1].split(",") if len(sys.argv) > 1 else ["16:0", "32:0", "8:0"]
+for cfg in cfgs:
+    kr, w = (int(x) for x in cfg.split(":"))
     ctx.set_option("batch_u16_kr", kr)
+    ctx.set_option("batch_mix_w", w)
     sc = torch.zeros(P, dtype=torch.int32, device="cuda")
     f = lambda: nwb.nw_align_batch_dev(ctx, ds, do, ss.offs, None, None, P, nwgen.PAPER_DNA, 0, sc)
     f(); torch.cuda.synchronize(); ctx.set_timing(True); ctx.kernel_time(0)
     for _ in range(3): f()
     ms, k = ctx.kernel_time(0); ctx.set_timing(False)
-    out[f"kr{kr}"] = {"ms": round(ms / k, 2), "TCUPS": round(3216418768982 / (ms / k) / 1e9, 3),
+    out[f"kr{kr}_w{w}"] = {"ms": round(ms / k, 2), "TCUPS": round(3216418768982 / (ms / k) / 1e9, 3),
                       "sample_ok": bool((sc.cpu().numpy()[idx] == want).all())}
 print(json.dumps(out, indent=1))
+if len(sys.argv) > 2: json.dump(out, open(sys.argv[2], "w"), indent=1)
