@@ -1251,6 +1251,8 @@ namespace {
 // Geometry of one column-block call: arithmetic form, strip height, blocks, messages.
 struct CbGeom {
   bool d16;             // packed difference form (s - 2g >= 0), else int32 H'
+  bool h16;             // packed H' with a moving base: preferred over d16
+  int reb;              // h16: rebase period (8-step groups)
   int KR, R, S, W, nblocks;
   long long mstride;    // entries per left-column message: R (d16) or R + 1 (int32)
   long long rstride;    // entries per receive slot: S * mstride
@@ -1267,13 +1269,16 @@ CbGeom cb_geom(const nw_ctx* c, long long m, long long n, const nw_scoring* sc, 
   CbGeom g;
   g.d16 = d16_ok(c, sc);
   g.KR = g.d16 ? d16_kr(c, std::max(m, 1LL)) : CB_KR32;
+  g.reb = (g.d16 && c->opt[NW_OPT_PAIR_FORM] != 1) ? h16_rebase_groups(c, sc, g.KR) : 0;
+  g.h16 = g.reb > 0;
+  if (g.h16) g.d16 = false;
   g.R = 32 * g.KR;
   g.S = (int)std::max<long long>((m + g.R - 1) / g.R, 1);
   if (block_cols > 0) g.W = block_cols;
   else if (G == 1) g.W = (int)std::max<long long>(n, 1);
   else g.W = (int)std::max<long long>(1024, (n + 32LL * G - 1) / (32LL * G));  // ~32 rounds
   g.nblocks = (int)std::max<long long>((n + g.W - 1) / g.W, 1);
-  g.mstride = g.d16 ? g.R : g.R + 1;
+  g.mstride = g.d16 ? g.R : g.R + 1;  // h16 and int32: corner + R rows
   g.rstride = (long long)g.S * g.mstride;
   g.recv_bytes = sizeof(unsigned long long) * 2 * (size_t)g.rstride;
   return g;
@@ -1338,6 +1343,17 @@ nw_status cblock_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* 
     A.watchdog = c->opt[NW_OPT_WATCHDOG_POLLS] > 0 ? c->opt[NW_OPT_WATCHDOG_POLLS] : (1LL << 28);
     A.rank0 = rank0;
     A.nranks_here = nhere;
+    A.sel = nullptr;
+    A.reb_groups = g.reb;
+    if (g.h16) {  // selector table over cb[-PAD, n + PAD) (nw_fill16.cuh)
+      const long long ls = n + 2 * PAD;
+      st = grow(c, c->d_sel16, c->sel16_cap, sizeof(uint16_t) * (size_t)ls);
+      if (st) return st;
+      const int blocks = (int)std::min<long long>((ls - 1 + 255) / 256, (long long)c->sm_count * 8);
+      k_sel16<<<std::max(blocks, 1), 256, 0, c->stream>>>(cb - PAD + 1, ls - 1, c->d_sel16 + 1);
+      LAUNCHED(c);
+      A.sel = c->d_sel16 + PAD;
+    }
     // every rank's warps must be resident together (they wait on each other);
     // NW_OPT_CBLOCK_WARPS_PER_SM caps this launch's share of the GPU
     int per_sm = 8;
@@ -1347,7 +1363,19 @@ nw_status cblock_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* 
     const int grid_r = std::max(nhere, grid - grid % nhere);
     {
       KernelTimer kt(c, 0);
-      if (g.d16) {
+      if (g.h16) {
+        switch (g.KR) {
+#define NW_CB_CASE(K)                                                                 \
+  case K:                                                                             \
+    if (sys) k_fill_cblock_h16<K, true><<<grid_r, 32, 0, c->stream>>>(A);            \
+    else k_fill_cblock_h16<K, false><<<grid_r, 32, 0, c->stream>>>(A);               \
+    break;
+          NW_CB_CASE(16) NW_CB_CASE(18) NW_CB_CASE(20) NW_CB_CASE(22) NW_CB_CASE(24)
+          NW_CB_CASE(26) NW_CB_CASE(28) NW_CB_CASE(30) NW_CB_CASE(32)
+#undef NW_CB_CASE
+          default: return fail(c, NW_E_INVAL, "column-block rows per lane %d", g.KR);
+        }
+      } else if (g.d16) {
         switch (g.KR) {
 #define NW_CB_CASE(K)                                                                 \
   case K:                                                                             \

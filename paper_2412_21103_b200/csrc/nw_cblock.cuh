@@ -34,6 +34,7 @@
 #include "nw_fill.cuh"
 #include "nw_fill16.cuh"
 #include "nw_fill_d16.cuh"
+#include "nw_fill_h16.cuh"
 
 namespace nwk {
 
@@ -59,6 +60,8 @@ struct CBlockArgs {
   int* hm;                   // d16: sum of U(i, n) (the last block's owner); int32: H'(m, n)
   int* err;
   long long watchdog;        // re-polls before *err is raised
+  const uint16_t* sel;       // h16: selector table aligned with b (nw_fill16.cuh)
+  int reb_groups;            // h16: rebase period in 8-step groups (power of two)
   int rank0;                 // first rank handled by this launch (real ranks: own rank)
   int nranks_here;           // ranks handled by this launch (virtual: G, real: 1)
 };
@@ -274,6 +277,178 @@ __global__ void __launch_bounds__(32) k_fill_cblock_d16(CBlockArgs A) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
       if (lane == 0) atomicAdd(A.hm, tot);
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------- packed H' form
+template <int KR, typename St>
+__device__ __forceinline__ void h16_rebase_cb(St& st) {
+  constexpr int H = KR / 2;
+  uint32_t mn = st.up0_prev;
+#pragma unroll
+  for (int k = 0; k < H; ++k) mn = __vminu2(mn, st.Hp[k]);
+  int d = (int)min(mn & 0xffffu, mn >> 16);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d = min(d, __shfl_xor_sync(FULL, d, o));
+  const uint32_t dd = (uint32_t)d * 0x00010001u;
+#pragma unroll
+  for (int k = 0; k < H; ++k) st.Hp[k] -= dd;
+  st.up0_prev -= dd;
+  st.base += d;
+}
+
+// The packed H' sweep with a moving per-strip base of nw_fill_h16.cuh over a block:
+// the task's values are kept relative to a warp-uniform base B, which starts at the
+// corner H'(top-1, c0) (every cell of the task is >= it) and moves up every `reb`
+// groups; the ring rows and the left messages carry ABSOLUTE H' (corner + R rows, as
+// the int32 form). Halves left of local column 1 hold the left boundary column; rows
+// past m have an all-zero profile, so they repeat row m and the last strip's bottom
+// row at column n is H'(m, n) (nw_fill16.cuh).
+template <int KR>
+struct CbH16State {
+  uint32_t PA[KR / 2], PB[KR / 2];
+  uint32_t Hp[KR / 2];
+  uint32_t up0_prev;
+  int chunk_cur, chunk_nxt;
+  int base;
+  uint32_t sel_nxt[8];
+};
+
+template <int KR, bool SYS, bool MASKED>
+__device__ __forceinline__ void cb_h16_group(CbH16State<KR>& st, const StripCtx& C, const uint16_t* sel,
+                                             int t0, const uint32_t (&Bv)[KR / 2], int c0, bool hm_strip,
+                                             unsigned long long* rout, unsigned rtag, int* hm) {
+  constexpr int H = KR / 2;
+  const int lane = C.lane, w = C.n;
+  uint32_t scur[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) scur[q] = st.sel_nxt[q];
+  const uint16_t* sp16 = sel + (t0 + 8 - 2 * lane);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) st.sel_nxt[q] = __ldg(sp16 + q);
+  unsigned long long* op = static_cast<unsigned long long*>(C.bnd_out) + (t0 - 62);
+  const int jc = t0 + 1 + lane;
+  const int crel = (lane < 8 && jc <= w) ? st.chunk_cur - st.base : 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int t = t0 + q;
+    const uint32_t s = scur[q];
+    const int recv = __shfl_up_sync(FULL, (int)st.Hp[H - 1], 1);
+    const int bval = __shfl_sync(FULL, crel, q);
+    const uint32_t upsrc = (lane == 0) ? ((uint32_t)bval << 16) : (uint32_t)recv;
+    uint32_t up = prmt2(upsrc, st.Hp[H - 1], 0x5432u);
+    uint32_t diag = st.up0_prev;
+    st.up0_prev = up;
+    const int jT = t - 2 * lane + 1;  // local column of the low halves
+    uint32_t mask = 0xffffffffu;
+    if (MASKED) mask = (jT >= 1 ? 0x0000ffffu : 0u) | (jT >= 2 ? 0xffff0000u : 0u);
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      const uint32_t sp = prmt2(st.PA[k], st.PB[k], s);
+      const uint32_t left = st.Hp[k];
+      uint32_t h = __vimax3_u16x2(diag + sp, left, up);
+      if (MASKED) h = (h & mask) | (Bv[k] & ~mask);  // H'(i, c0): the left boundary column
+      diag = left;
+      up = h;
+      st.Hp[k] = h;
+    }
+    const int jB = jT - 1;
+    if (lane == 31 && (!MASKED || (jB >= 1 && jB <= w))) {
+      const int hb = (int)(st.Hp[H - 1] >> 16) + st.base;  // bottom row at local column jB, absolute
+      unsigned long long v;
+      asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "r"(hb), "r"(C.tag_out));
+      st_relaxed_u64(op + q, v);
+      if (MASKED && hm_strip && jB == w) *hm = hb;  // last strip, last block: H'(m, n)
+    }
+    if (MASKED && rout) {  // the right column (local column w) -> the next block's rank
+      if (jT == w) {
+#pragma unroll
+        for (int k = 0; k < H; ++k) cb_st<SYS>(rout + 1 + lane * KR + k, (st.Hp[k] & 0xffffu) + st.base, rtag);
+        if (lane == 0) cb_st<SYS>(rout, (unsigned)(bval + st.base), rtag);  // corner H'(top-1, c1)
+      }
+      if (jB == w) {
+#pragma unroll
+        for (int k = 0; k < H; ++k) cb_st<SYS>(rout + 1 + lane * KR + H + k, (st.Hp[k] >> 16) + st.base, rtag);
+      }
+    }
+  }
+}
+
+template <int KR, bool SYS>
+__global__ void __launch_bounds__(32) k_fill_cblock_h16(CBlockArgs A) {
+  constexpr int H = KR / 2, R = 32 * KR;
+  const int lane = threadIdx.x;
+  const int lr = blockIdx.x % A.nranks_here;
+  const int rank = A.rank0 + lr;
+  unsigned long long* ring = A.bnd + (size_t)lr * 2 * A.bstride;
+  const unsigned long long* recv_me = A.recv_tab[rank];
+  CBTask T;
+  while (cb_next_task(A, lr, rank, lane, recv_me, T)) {
+    const int s = T.s;
+    const int ia0 = s * R + lane * KR;
+    // left boundary column (absolute): corner + R rows; lane l reads entries l*KR .. l*KR+KR
+    // (entry 0 of lane 0 is the corner H'(top-1, c0)); the grid border is 0
+    unsigned v[KR + 1];
+    if (T.lin) {
+      cb_recv<SYS, KR + 1>(A, T.lin + lane * KR, T.seq, v, lane);
+    } else {
+#pragma unroll
+      for (int r = 0; r <= KR; ++r) v[r] = 0;
+    }
+    CbH16State<KR> st;
+    st.base = __shfl_sync(FULL, (int)v[0], 0);  // the corner: every cell of the task is >= it
+    uint32_t Bv[H];
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      Bv[k] = (v[1 + k] - (unsigned)st.base) | ((v[1 + H + k] - (unsigned)st.base) << 16);
+      const int a0 = A.a[ia0 + k], a1 = A.a[ia0 + k + H];
+      uint32_t w0 = 0, w1 = 0;
+      for (int c = 0; c < A.K; ++c) {
+        w0 |= ((uint32_t)(uint8_t)A.prof[a0 * A.K + c]) << (8 * c);
+        w1 |= ((uint32_t)(uint8_t)A.prof[a1 * A.K + c]) << (8 * c);
+      }
+      st.PA[k] = (ia0 + k < A.m) ? w0 : 0u;  // rows past m repeat row m (zero profile)
+      st.PB[k] = (ia0 + k + H < A.m) ? w1 : 0u;
+      st.Hp[k] = Bv[k];
+    }
+    st.up0_prev = 0;  // lane 0's first diag: the corner, relative 0
+    st.chunk_cur = st.chunk_nxt = 0;
+    const uint16_t* sel = A.sel + T.c0;  // selector table entries of the block's columns
+#pragma unroll
+    for (int q = 0; q < 8; ++q) st.sel_nxt[q] = __ldg(sel + (q - 2 * lane));
+    StripCtx C;
+    C.b = A.b + T.c0;
+    C.sprof = nullptr;
+    C.bnd_in = (s > 0) ? ring + (size_t)(s & 1) * A.bstride + T.c0 : nullptr;
+    C.bnd_out = ring + (size_t)((s + 1) & 1) * A.bstride + T.c0;
+    C.tag_in = T.seq - 1u;
+    C.tag_out = T.seq;
+    C.dir_base = nullptr;
+    C.err = A.err;
+    C.poll_ns = 0;
+    C.watchdog = A.watchdog;
+    C.hm = A.hm;
+    C.n = T.w;
+    C.s = s;
+    C.lane = lane;
+    const bool hm_strip = s == A.S - 1 && T.c1 == A.n;
+    if (s > 0) st.chunk_nxt = chunk_verify<true>(C, 0, chunk_issue<true>(C, 0));
+    const int ngrp = (T.w + 63 + 7) / 8;
+    const int rmask = A.reb_groups - 1;
+#pragma unroll 1
+    for (int g = 0; g < ngrp; ++g) {
+      const int t0 = g * 8;
+      if ((g & rmask) == 0 && g >= 8) h16_rebase_cb<KR>(st);
+      st.chunk_cur = st.chunk_nxt;
+      const bool more = s > 0 && t0 + 8 < T.w;
+      unsigned long long raw = 0;
+      if (more) raw = chunk_issue<true>(C, t0 + 8);
+      const bool masked = t0 < 64 || t0 + 7 >= T.w - 1;
+      if (masked) cb_h16_group<KR, SYS, true>(st, C, sel, t0, Bv, T.c0, hm_strip, T.rout, T.rtag, A.hm);
+      else cb_h16_group<KR, SYS, false>(st, C, sel, t0, Bv, T.c0, hm_strip, T.rout, T.rtag, A.hm);
+      if (more) st.chunk_nxt = chunk_verify<true>(C, t0 + 8, raw);
     }
     __syncwarp();
   }

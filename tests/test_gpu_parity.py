@@ -281,7 +281,9 @@ def test_score_only_prefix_and_closed_forms_c5(ctx):
 
 # ---------------------------------------------------------------- column blocks (a10)
 
-CB_SCORINGS = {"d16": nwgen.PAPER_DNA,                                  # difference form
+CB_SCORINGS = {"h16": nwgen.PAPER_DNA,                                  # packed H', moving base
+               "h16b": nwgen.Scoring(match=2, mismatch=-1, gap=-3),
+               "d16": nwgen.PAPER_DNA,                                  # difference form
                "d16b": nwgen.Scoring(match=2, mismatch=-1, gap=-3),
                "int32": nwgen.Scoring(match=2, mismatch=-4, gap=-1)}     # s - 2g < 0: int32 H'
 
@@ -289,13 +291,25 @@ CB_SCORINGS = {"d16": nwgen.PAPER_DNA,                                  # differ
 @pytest.mark.parametrize("form", sorted(CB_SCORINGS))
 @pytest.mark.parametrize("m,n", [(1, 1), (300, 500), (1000, 5000), (3000, 700), (513, 2049), (2000, 7)])
 @pytest.mark.parametrize("ranks,w", [(1, 0), (2, 64), (3, 1000), (8, 0), (5, 257), (4, 1)])
-def test_cblock_virtual_ranks(ctx, form, m, n, ranks, w):
+def test_cblock_virtual_ranks(ctx, opts, form, m, n, ranks, w):
     """Column-block wavefront across virtual ranks == oracle score (SURVEY §8(e) C5 path),
-    both arithmetic forms, blocks down to one column, many calls on one context (the
-    per-call tags of nw_cblock.cuh: buffers are never re-zeroed between calls)."""
+    all three arithmetic forms (pair_form 1 selects the difference form over the packed
+    H' one), blocks down to one column, many calls on one context (the per-call tags of
+    nw_cblock.cuh: buffers are never re-zeroed between calls)."""
+    opts(ctx, "pair_form", 1 if form.startswith("d16") else 0)
     a, b = _pair(7000 + m + n, m, n)
     sc = CB_SCORINGS[form]
     assert nwb.nw_score_only_cblock(ctx, a, b, sc, ranks, w) == oracle.score(a, b, sc)
+
+
+@pytest.mark.parametrize("reb", [1, 2])
+def test_cblock_h16_frequent_rebase_tall(ctx, opts, reb):
+    """The packed H' column-block form with the base moving every 1-2 groups on a pair
+    tall enough for many strips, over 3 virtual ranks (left messages, corners, ring)."""
+    opts(ctx, "h16_rebase", reb)
+    a, b = _pair(7100 + reb, 40_000, 3_000)
+    for sc in (nwgen.PAPER_DNA, nwgen.Scoring(match=31, mismatch=-30, gap=-15)):
+        assert nwb.nw_score_only_cblock(ctx, a, b, sc, 3, 700) == oracle.score(a, b, sc)
 
 
 def test_cblock_c5_prefix_and_closed_forms(ctx):

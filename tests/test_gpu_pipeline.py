@@ -19,8 +19,9 @@ from paper_2412_21103_b200 import dist as nwdist
 
 pytestmark = pytest.mark.gpu
 
-CASES = [(3000, 9000, 0, "d16"), (2500, 4000, 700, "int32")]
-SC = {"d16": nwgen.PAPER_DNA, "int32": nwgen.Scoring(match=2, mismatch=-4, gap=-1)}
+CASES = [(3000, 9000, 0, "h16"), (2800, 6000, 500, "d16"), (2500, 4000, 700, "int32")]
+SC = {"h16": nwgen.PAPER_DNA, "d16": nwgen.PAPER_DNA, "int32": nwgen.Scoring(match=2, mismatch=-4, gap=-1)}
+PAIR_FORM = {"h16": 0, "d16": 1, "int32": 0}  # NW_OPT_PAIR_FORM: 1 = the difference form
 
 
 def _rank_worker(m, n, w, form, out_dir):
@@ -31,6 +32,7 @@ def _rank_worker(m, n, w, form, out_dir):
     torch.cuda.set_device(0)
     ctx = nwb.Context(0, torch.cuda.current_stream().cuda_stream)
     ctx.set_option("cblock_warps_per_sm", 2)  # both ranks' warps resident on the one GPU
+    ctx.set_option("pair_form", PAIR_FORM[form])
     h = nwb.nw_cblock_ipc_export(ctx, m)
     hs = [None] * world
     dist.all_gather_object(hs, h)
@@ -64,10 +66,11 @@ def test_two_process_ipc_pipeline(tmp_path, m, n, w, form):
         assert got == [want, want]
 
 
-@pytest.mark.parametrize("form", ["d16", "int32"])
+@pytest.mark.parametrize("form", ["h16", "d16", "int32"])
 def test_dist_ctx_pipeline_world1(form):
     import torch
     c = nwb.Context(0)
+    c.set_option("pair_form", PAIR_FORM[form])
     c.set_dist(0, 1, nwb.nw_dist_unique_id())
     c.set_option("dist_pipeline", 1)
     for m, n in [(5000, 3000), (700, 12000), (1, 9)]:

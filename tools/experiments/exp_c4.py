@@ -20,7 +20,8 @@ d_oo = torch.from_numpy(oo).cuda()
 d_ops = torch.zeros(int(oo[-1]) + 1, dtype=torch.uint8, device="cuda")
 d_len = torch.zeros(len(pairs), dtype=torch.int32, device="cuda")
 d_sc = torch.zeros(len(pairs), dtype=torch.int32, device="cuda")
-for mode in ("two_phase", "two_phase"):
+for mode in os.environ.get("EXP_KR16", "0,0").split(","):
+    ctx.set_option("batch_kr16", int(mode))
     run = lambda: nwb.nw_align_batch_dev(ctx, d_seqs, d_offs, ss.offs, d_pairs, pairs, len(pairs), sc,
                                          nwb.NW_TRACEBACK, d_sc, d_oo, d_ops, d_len)
     run(); run(); torch.cuda.synchronize()

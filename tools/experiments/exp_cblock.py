@@ -1,4 +1,4 @@
-"""Column-block pipeline vs the plain difference-form fill on C5 (not a bench line).
+"""Column-block pipeline vs the plain single-pair fill on C5 (not a bench line).
 Kernel event times (class 0) of: nw_score_only_dev (plain), the dist-ctx pipeline at
 world 1 (NW_OPT_DIST_PIPELINE=1), and nw_score_only_cblock over G virtual ranks."""
 import json, sys, time
@@ -27,7 +27,7 @@ def timed(ctx, fn, reps=3):
 c = nwb.Context(0, st)
 d = torch.zeros(1, dtype=torch.int64, device="cuda")
 ms = timed(c, lambda: nwb.nw_score_only_dev(c, da, db, sc, d))
-out["plain_d16_ms"] = ms; out["plain_d16_TCUPS"] = cells / ms / 1e9
+out["plain_ms"] = ms; out["plain_TCUPS"] = cells / ms / 1e9
 c2 = nwb.Context(0, st)
 c2.set_dist(0, 1, nwb.nw_dist_unique_id())
 c2.set_option("dist_pipeline", 1)
@@ -40,3 +40,4 @@ for G in [1, 2, 4, 8]:
         out[f"virtual_G{G}_w{w}_ms"] = ms
         out[f"virtual_G{G}_w{w}_TCUPS"] = cells / ms / 1e9
 print(json.dumps(out, indent=1))
+if len(sys.argv) > 1: json.dump(out, open(sys.argv[1], "w"), indent=1)

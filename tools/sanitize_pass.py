@@ -50,10 +50,21 @@ ok("score int32", nwb.nw_score_only(ctx, a, b, NEG) == oracle.score(a, b, NEG))
 ctx.set_option("d16_force", 16)
 ok("score d16", nwb.nw_score_only(ctx, a, b, DNA) == oracle.score(a, b, DNA))
 ctx.set_option("d16_force", 0)
+# packed H' with a moving base (nw_fill_h16), rebasing every group
+ctx.set_option("h16_kr", 16)
+ctx.set_option("h16_rebase", 1)
+ah, bh = nwgen.random_pair(6, 2100, 700)
+ok("score h16", nwb.nw_score_only(ctx, ah, bh, DNA) == oracle.score(ah, bh, DNA))
+ctx.set_option("h16_kr", 0)
+ctx.set_option("h16_rebase", 0)
 # batches: u16 score-only (implicit), d16 (long), int32; traceback two-phase + int32
 ss = nwgen.random_set(3, 10, 0, 400)
 ok("batch u16", nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, DNA).tolist()
    == oracle.batch_score(ss.residues, ss.offs, nwgen.all_pairs(ss.nseq), DNA).tolist())
+ctx.set_option("batch_u16_kr", 1)  # mixed 1,024/512-row strips
+ok("batch u16 mixed", nwb.nw_align_batch(ctx, ss.residues, ss.offs, None, DNA).tolist()
+   == oracle.batch_score(ss.residues, ss.offs, nwgen.all_pairs(ss.nseq), DNA).tolist())
+ctx.set_option("batch_u16_kr", 0)
 sl = nwgen.random_set(4, 4, 3000, 5000)
 ok("batch d16", nwb.nw_align_batch(ctx, sl.residues, sl.offs, None, DNA).tolist()
    == oracle.batch_score(sl.residues, sl.offs, nwgen.all_pairs(sl.nseq), DNA).tolist())
