@@ -1276,7 +1276,7 @@ CbGeom cb_geom(const nw_ctx* c, long long m, long long n, const nw_scoring* sc, 
   g.S = (int)std::max<long long>((m + g.R - 1) / g.R, 1);
   if (block_cols > 0) g.W = block_cols;
   else if (G == 1) g.W = (int)std::max<long long>(n, 1);
-  else g.W = (int)std::max<long long>(1024, (n + 32LL * G - 1) / (32LL * G));  // ~32 rounds
+  else g.W = (int)std::max<long long>(1024, ((n + 32LL * G - 1) / (32LL * G) + 1) & ~1LL);  // ~32 rounds, even
   g.nblocks = (int)std::max<long long>((n + g.W - 1) / g.W, 1);
   g.mstride = g.d16 ? g.R : g.R + 1;  // h16 and int32: corner + R rows
   g.rstride = (long long)g.S * g.mstride;
@@ -2026,7 +2026,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   // scratch (~maxlen^2/4 bytes) per launched warp
   const long long nwarps = std::min<long long>((long long)c->sm_count * ctas_per_sm * warps_per_cta,
                                                (ntasks + warps_per_cta - 1) / warps_per_cta * warps_per_cta);
-  const long long bstride = maxlen + 1 + 64;
+  const long long bstride = (maxlen + 1 + 64 + 1) & ~1LL;  // even: 8-byte vector stores of the bottom row (nw_fill.cuh)
   // direction scratch per warp, in halfwords: int32 sweep = halfword per (group,
   // row, lane); packed sweep = 32-bit word per (group, packed row, lane)
   const long long wpl = (maxlen + (packed_sweep ? 63 : 31) + 7) / 8;  // 8-step groups per strip

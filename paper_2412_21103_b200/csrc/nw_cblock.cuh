@@ -329,6 +329,7 @@ __device__ __forceinline__ void cb_h16_group(CbH16State<KR>& st, const StripCtx&
 #pragma unroll
   for (int q = 0; q < 8; ++q) st.sel_nxt[q] = __ldg(sp16 + q);
   unsigned long long* op = static_cast<unsigned long long*>(C.bnd_out) + (t0 - 62);
+  uint32_t bot[8];
   const int jc = t0 + 1 + lane;
   const int crel = (lane < 8 && jc <= w) ? st.chunk_cur - st.base : 0;
 #pragma unroll
@@ -355,13 +356,8 @@ __device__ __forceinline__ void cb_h16_group(CbH16State<KR>& st, const StripCtx&
       st.Hp[k] = h;
     }
     const int jB = jT - 1;
-    if (lane == 31 && (!MASKED || (jB >= 1 && jB <= w))) {
-      const int hb = (int)(st.Hp[H - 1] >> 16) + st.base;  // bottom row at local column jB, absolute
-      unsigned long long v;
-      asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "r"(hb), "r"(C.tag_out));
-      st_relaxed_u64(op + q, v);
-      if (MASKED && hm_strip && jB == w) *hm = hb;  // last strip, last block: H'(m, n)
-    }
+    bot[q] = st.Hp[H - 1] >> 16;  // lane 31's bottom row at local column jB, stored per group
+    if (MASKED && hm_strip && lane == 31 && jB == w) *hm = (int)bot[q] + st.base;  // H'(m, n)
     if (MASKED && rout) {  // the right column (local column w) -> the next block's rank
       if (jT == w) {
 #pragma unroll
@@ -371,6 +367,24 @@ __device__ __forceinline__ void cb_h16_group(CbH16State<KR>& st, const StripCtx&
       if (jB == w) {
 #pragma unroll
         for (int k = 0; k < H; ++k) cb_st<SYS>(rout + 1 + lane * KR + H + k, (st.Hp[k] >> 16) + st.base, rtag);
+      }
+    }
+  }
+  // the group's 8 ring entries (local columns t0-62 .. t0-55) in one go, as nw_fill_h16.cuh:
+  // 64-bit vector elements (each single-copy atomic) when 16-byte aligned (c0 even)
+  if (lane == 31) {
+    const unsigned long long tg = (unsigned long long)C.tag_out << 32;
+    const bool vec = (c0 & 1) == 0;
+#pragma unroll
+    for (int q = 0; q < 8; q += 2) {
+      const int j0 = t0 - 62 + q;
+      const unsigned long long e0 = tg | (bot[q] + (unsigned)st.base);
+      const unsigned long long e1 = tg | (bot[q + 1] + (unsigned)st.base);
+      if (vec && (!MASKED || (j0 >= 1 && j0 + 1 <= w))) {
+        asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(op + q), "l"(e0), "l"(e1) : "memory");
+      } else {
+        if (j0 >= 1 && j0 <= w) st_relaxed_u64(op + q, e0);
+        if (j0 + 1 >= 1 && j0 + 1 <= w) st_relaxed_u64(op + q + 1, e1);
       }
     }
   }

@@ -247,6 +247,9 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
     st.send = st.Hl[KR - 1];
     if (lane == 31 && (!MASKED || (j >= 1 && j <= n))) {
       // lane 31's column is j = t - 30: stores step through the group's base pointers
+      // (stored per step: buffering the group's 8 values for one vector store, as the
+      // packed H' sweep does, made C2 slower, 1.59 -> 1.68 ms: the later publication
+      // lengthens every strip hand-off)
       if (MULTIWARP) {
         unsigned long long v;
         asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "r"(st.send), "r"(C.s + 1));  // (tag << 32) | H'
@@ -256,9 +259,10 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
       }
     }
     if (MASKED && lane == C.hm_lane && t == C.hm_t) {
+      int w = 0;
 #pragma unroll
-      for (int r = 0; r < KR; ++r)
-        if (r == C.hm_r) *C.hm = st.Hl[r];
+      for (int r = 0; r < KR; ++r) w = (r == C.hm_r) ? st.Hl[r] : w;  // selects: Hl stays in registers
+      *C.hm = w;
     }
   }
   if (DIRS) {  // group g = t0/8: halfword (g, r, lane), step k at bits (15-2k, 14-2k) = (nbX, nbY)

@@ -52,6 +52,7 @@ __device__ __forceinline__ void h16_group(H16State<KR>& st, const StripCtx& C, c
 #pragma unroll
   for (int q = 0; q < 8; ++q) st.sel_nxt[q] = __ldg(sp16 + q);
   unsigned long long* op = static_cast<unsigned long long*>(C.bnd_out) + (t0 - 62);
+  uint32_t bot[8];
   // lane 0 takes the boundary values relative to B (columns beyond n: 0, never read
   // by a cell inside the grid, and small enough to keep every half in range)
   const int jc = t0 + 1 + lane;
@@ -81,19 +82,36 @@ __device__ __forceinline__ void h16_group(H16State<KR>& st, const StripCtx& C, c
       up = h;
       st.Hp[k] = h;
     }
-    const int jB = jT - 1;
-    if (lane == 31 && (!MASKED || (jB >= 1 && jB <= n))) {
-      const int hb = (int)(st.Hp[H - 1] >> 16) + st.base;  // bottom row H' at jB, absolute
-      unsigned long long v;
-      asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "r"(hb), "r"(C.tag_out));
-      st_relaxed_u64(op + q, v);
-    }
+    // lane 31's bottom row at jB = jT - 1 (relative), kept for the group's one vector store
+    // (a global store every step sat in the MIO queue ahead of the next step's shuffle:
+    // +40-60 cycles per step, tools/h16_step.cu)
+    bot[q] = st.Hp[H - 1] >> 16;
     if (MASKED && C.hm_lane == lane && C.hm_t == t) {  // H'(m, n), absolute
       const int hk = C.hm_r >= H ? C.hm_r - H : C.hm_r;
       uint32_t w = 0;
 #pragma unroll
       for (int k = 0; k < H; ++k) w = (k == hk) ? st.Hp[k] : w;  // selects: Hp stays in registers
       *C.hm = (int)(C.hm_r >= H ? (w >> 16) : (w & 0xffffu)) + st.base;
+    }
+  }
+  // the group's 8 bottom-row entries (columns t0-62 .. t0-55), tagged and absolute, as
+  // four 16-byte stores of two 64-bit elements: each element is a single-copy-atomic
+  // 8-byte access, so every entry still carries its own validity (nw_fill.cuh). Entries
+  // are 16-byte aligned (t0 - 62 + q even, even row stride). Columns outside [1, n] are
+  // skipped.
+  if (lane == 31) {
+    const unsigned long long tg = (unsigned long long)C.tag_out << 32;
+#pragma unroll
+    for (int q = 0; q < 8; q += 2) {
+      const int j0 = t0 - 62 + q;  // column of entry q (lane 31's jB at step t0 + q)
+      const unsigned long long e0 = tg | (bot[q] + (unsigned)st.base);
+      const unsigned long long e1 = tg | (bot[q + 1] + (unsigned)st.base);
+      if (!MASKED || (j0 >= 1 && j0 + 1 <= n)) {
+        asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(op + q), "l"(e0), "l"(e1) : "memory");
+      } else {
+        if (j0 >= 1 && j0 <= n) st_relaxed_u64(op + q, e0);
+        if (j0 + 1 >= 1 && j0 + 1 <= n) st_relaxed_u64(op + q + 1, e1);
+      }
     }
   }
 }
