@@ -332,8 +332,8 @@ enum {
                                  chains per lane (rows per lane % 4 == 0; measured slower on C5),
                                  else one chain (default) */
   NW_OPT_BATCH_U16_KR = 21,    /* score-only packed H' batch sweep: rows per lane 8, 16 or 32, or 1 =
-                                 32 or 16 per pair, whichever sweeps less weighted area (0: by the
-                                 median sequence length: 1 from 1,024, else 16 or 8) */
+                                 32, 24 or 16 per pair, whichever sweeps less weighted area (0: by
+                                 the median sequence length: 1 from 1,024, else 16 or 8) */
   NW_OPT_BATCH_BND_GLOBAL = 22, /* 1: the packed H' batch sweep keeps its boundary rows in global
                                   scratch instead of shared memory */
   NW_OPT_PAIR_FORM = 23,       /* tall score-only pairs: 0 = packed H' with a moving base
@@ -343,7 +343,8 @@ enum {
   NW_OPT_H16_KR = 25,          /* rows per lane of the packed H' pair sweep (even, 12..32; 0: rule) */
   NW_OPT_BATCH_MIX_W = 26,     /* packed H' batch sweep, mixed strip heights: relative cost (x1000) of
                                   a 512-row strip's cell vs a 1,024-row one (0: 1100) */
-  NW_OPT_COUNT_ = 27
+  NW_OPT_BATCH_MIX_W24 = 27,   /* the same for a 768-row strip's cell (0: 1040) */
+  NW_OPT_COUNT_ = 28
 };
 nw_status nw_ctx_set_option(nw_ctx *ctx, int32_t option, int64_t value);
 /* Current value, or -1 for a NULL ctx / unknown option. */

@@ -2148,6 +2148,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
       const long long o = c->opt[NW_OPT_BATCH_U16_KR];
       if (o == 1 || o == 8 || o == 16 || o == 32) u16_kr = (int)o;
       if (c->opt[NW_OPT_BATCH_MIX_W] > 0) B.mix_w16 = (int)std::min(c->opt[NW_OPT_BATCH_MIX_W], 100000LL);
+      if (c->opt[NW_OPT_BATCH_MIX_W24] > 0) B.mix_w24 = (int)std::min(c->opt[NW_OPT_BATCH_MIX_W24], 100000LL);
     }
     ok = dispatch_batch(tbk, pi, profreg, u16, d16, packed_kr, B, grid, smem, c->stream, u16_kr);
   }

@@ -476,6 +476,7 @@ struct BatchArgs {
   int* err;
   int transpose_ok;        // score-only, s symmetric: a pair may be filled transposed
   int mix_w16 = 1100;      // PACKED 4: relative cost (x1000) of a 512-row strip cell vs a 1,024-row one
+  int mix_w24 = 1040;      // PACKED 4: the same for a 768-row strip cell
   // Two-phase traceback (the packed sweep, PACKED == 3): the fill
   // keeps every pair's decision words at tdirs + tdir_off[task] (32-bit words) and
   // k_batch_walk walks them after the fill, one thread per pair.
@@ -530,7 +531,7 @@ __device__ __forceinline__ void task_pair(const BatchArgs& B, long long task, in
 // 1 = the H' half-row sweep of nw_fill16.cuh (score-only, K <= 4, every H' < 2^16),
 // 2 = the difference-form sweep of nw_fill_d16.cuh (score-only, K <= 4, any length),
 // 3 = the difference-form sweep with decision flags of nw_fill_d16dir.cuh (DIRS),
-// 4 = as 1, each pair at 32 or 16 rows per lane (whichever sweeps less weighted area).
+// 4 = as 1, each pair at 32, 24 or 16 rows per lane (whichever sweeps less weighted area).
 template <int KR16, bool COHERENT>
 __device__ __forceinline__ void walk_lanes(const BatchArgs& B, long long task, bool act, int lane);
 
@@ -565,9 +566,11 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       const int tm = m; m = n; n = tm;
     }
     bool half = false;  // PACKED 4: this pair runs 512-row strips (strip_sweep_u16<16>)
+    bool three = false;  // PACKED 4: 768-row strips (strip_sweep_u16<24>)
     if (PACKED == 4) {
-      // the orientation and strip height (1,024 or 512 rows) with the least weighted swept
-      // area: strips x height x (columns + lane skew), 512-row cells weighted mix_w16/1000
+      // the orientation and strip height (1,024, 768 or 512 rows) with the least weighted
+      // swept area: strips x height x (columns + lane skew), 768/512-row cells weighted
+      // mix_w24/1000, mix_w16/1000
       // (their per-cell overhead is higher); transposing needs the symmetric s
       auto cost = [&](int rows, int cols, int rs, long long w) {
         return (long long)((rows + rs - 1) / rs) * rs * (cols + 64) * w;
@@ -576,13 +579,22 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
       int pick = 0;
       const long long c1 = cost(m, n, 512, B.mix_w16);
       if (c1 < best) { best = c1; pick = 1; }
+      const long long c1b = cost(m, n, 768, B.mix_w24);
+      if (c1b < best) { best = c1b; pick = 4; }
       if (B.transpose_ok) {
         const long long c2 = cost(n, m, 1024, 1000), c3 = cost(n, m, 512, B.mix_w16);
         if (c2 < best) { best = c2; pick = 2; }
         if (c3 < best) { best = c3; pick = 3; }
+        const long long c3b = cost(n, m, 768, B.mix_w24);
+        if (c3b < best) { best = c3b; pick = 6; }
       }
       half = pick & 1;
-      if (pick >= 2) {
+      three = pick >= 4;
+      if (pick == 6) {
+        const long long to = ao; ao = bo; bo = to;
+        const int tm = m; m = n; n = tm;
+      }
+      if (pick == 2 || pick == 3) {
         const long long to = ao; ao = bo; bo = to;
         const int tm = m; m = n; n = tm;
       }
@@ -612,6 +624,9 @@ __global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
         if (half) {
           A.nstrips = (m + 511) / 512;
           for (int s = 0; s < A.nstrips; ++s) strip_sweep_u16<16>(A, s, lane);
+        } else if (three) {
+          A.nstrips = (m + 767) / 768;
+          for (int s = 0; s < A.nstrips; ++s) strip_sweep_u16<24>(A, s, lane);
         } else {
           for (int s = 0; s < A.nstrips; ++s) strip_sweep_u16<32>(A, s, lane);
         }

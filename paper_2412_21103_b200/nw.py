@@ -29,7 +29,7 @@ OPTIONS = {"rows_per_lane": 0, "d16_force": 1, "d16_kr": 2, "no_d16": 3, "tall_k
            "host_profile": 14, "watchdog_polls": 15, "test_withhold": 16,
            "dist_virtual_world": 17, "dist_virtual_rank": 18,
            "dist_pipeline": 19, "d16_chains": 20, "batch_u16_kr": 21, "batch_bnd_global": 22,
-           "pair_form": 23, "h16_rebase": 24, "h16_kr": 25, "batch_mix_w": 26}
+           "pair_form": 23, "h16_rebase": 24, "h16_kr": 25, "batch_mix_w": 26, "batch_mix_w24": 27}
 
 
 class NWError(RuntimeError):

@@ -550,14 +550,15 @@ def test_batch_score_only_u16_rows_per_lane(ctx, opts, kr):
         oracle.batch_score(ss.residues, ss.offs, rev, nwgen.PAPER_DNA).tolist()
 
 
-@pytest.mark.parametrize("w", [1, 1100, 100000])
-def test_batch_u16_mixed_strip_heights(ctx, opts, w):
-    """Mixed 1,024/512-row strips (batch_u16_kr 1) with the weight pushing every pair to
-    512 rows (w = 1), the default, or to 1,024 rows (w = 100000); a symmetric scoring (the
-    orientation may flip) and an asymmetric substitution matrix (it may not)."""
+@pytest.mark.parametrize("w,w24", [(1, 0), (0, 1), (0, 0), (100000, 100000)])
+def test_batch_u16_mixed_strip_heights(ctx, opts, w, w24):
+    """Mixed 1,024/768/512-row strips (batch_u16_kr 1) with the weights pushing every pair
+    to 512 rows (w = 1) or 768 rows (w24 = 1), the defaults, or to 1,024 rows; a symmetric
+    scoring (the orientation may flip) and an asymmetric substitution matrix (it may not)."""
     opts(ctx, "batch_u16_kr", 1)
     opts(ctx, "batch_mix_w", w)
-    ss = nwgen.random_set(9900 + w % 97, 24, 0, 2300)
+    opts(ctx, "batch_mix_w24", w24)
+    ss = nwgen.random_set(9900 + w % 97 + w24 % 89, 24, 0, 2300)
     pairs = nwgen.all_pairs(ss.nseq)
     asym = np.array([[3, 0, 1, 0], [1, 2, 0, 0], [0, 1, 4, 2], [2, 0, 0, 3]], dtype=np.int32)
     for sc in (nwgen.PAPER_DNA, nwgen.Scoring(gap=-1, subst=asym)):
