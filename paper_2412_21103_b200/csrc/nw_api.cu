@@ -665,21 +665,25 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     }
     const bool profreg = sc->K <= 4;
     const size_t smem = profreg ? 0 : (size_t)sc->K * R;
-    const bool h16 = !dirs && !ckpt && h16_reb > 0;
+    const bool h16 = !ckpt && !top_row && h16_reb > 0;  // with dirs: KR 4 or 8 (the caller checks)
     const bool d16 = !dirs && (kr >= 12 || (!ckpt && c->opt[NW_OPT_D16_FORCE] && d16_ok(c, sc)));
-    if (h16) {  // selector table of the packed H' sweep over cb[-PAD, n + PAD) (FillArgs::sel)
-      const long long ls = n + 2 * PAD;
-      st = grow(c, c->d_sel16, c->sel16_cap, sizeof(uint16_t) * (size_t)ls);
+    if (h16) {  // 4 shifted copies of the selector table over cb[-PAD, n + PAD) (FillArgs::sel4)
+      const long long ls = (n + 2 * PAD + 7) & ~7LL;
+      st = grow(c, c->d_sel16, c->sel16_cap, sizeof(uint16_t) * 4 * (size_t)ls);
       if (st) return st;
-      const int blocks = (int)std::min<long long>((ls - 1 + 255) / 256, (long long)c->sm_count * 8);
-      k_sel16<<<std::max(blocks, 1), 256, 0, c->stream>>>(cb - PAD + 1, ls - 1, c->d_sel16 + 1);
+      const int blocks = (int)std::min<long long>((4 * ls + 255) / 256, (long long)c->sm_count * 8);
+      k_sel16x4<<<std::max(blocks, 1), 256, 0, c->stream>>>(cb, n, c->d_sel16, ls);
       LAUNCHED(c);
-      A.sel = c->d_sel16 + PAD;
+      A.sel4 = c->d_sel16 + PAD;
+      A.sel4_stride = ls;
       A.reb_groups = h16_reb;
 #ifdef NW_TRACE
       A.trace = nw_trace_buffer(nstrips);
 #endif
     }
+#ifdef NW_TRACE
+    if (!h16) A.trace = nw_trace_buffer(nstrips);
+#endif
     // persistent grid: one warp per CTA, at most the resident capacity
     int per_sm = 16;
     int grid = std::min<long long>(nstrips, (long long)c->sm_count * per_sm);
@@ -687,7 +691,18 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     bool ok;
     {
       KernelTimer kt(c, 0);
-      if (h16) ok = dispatch_fill_h16(kr, A, grid, c->stream);
+      if (h16 && dirs) {
+        ok = true;
+        switch (pi) {
+          case 123: launch_fill_dirs_h16<123>(A, kr, grid, c->stream); break;
+          case 132: launch_fill_dirs_h16<132>(A, kr, grid, c->stream); break;
+          case 213: launch_fill_dirs_h16<213>(A, kr, grid, c->stream); break;
+          case 231: launch_fill_dirs_h16<231>(A, kr, grid, c->stream); break;
+          case 312: launch_fill_dirs_h16<312>(A, kr, grid, c->stream); break;
+          case 321: launch_fill_dirs_h16<321>(A, kr, grid, c->stream); break;
+          default: ok = false;
+        }
+      } else if (h16) ok = dispatch_fill_h16(kr, A, grid, c->stream);
       else
         ok = dispatch_fill(dirs, pi, kr, profreg, A, grid, smem, c->stream, d16,
                            c->opt[NW_OPT_D16_CHAINS] == 2 && !ckpt);
@@ -840,6 +855,11 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
     h16_reb = h16_rebase_groups(c, sc, kh);
     if (h16_reb > 0) kr = kh;
   }
+  // with directions, NW_OPT_PAIR_FORM = 2: the packed H' fill writing the int32 sweep's
+  // decision layout at the same rows per lane (4 or 8), so the strip traceback is
+  // unchanged (C2: 1.88 vs 1.59 ms for the int32 fill, not the default)
+  if (want_dirs && d16_ok(c, sc) && (kr == 4 || kr == 8) && c->opt[NW_OPT_PAIR_FORM] == 2)
+    h16_reb = h16_rebase_groups(c, sc, kr);
   st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
   if (st) return st;
   // two ring slots (+ a sink slot for the NW_OPT_TEST_WITHHOLD hook)

@@ -314,6 +314,7 @@ struct CbH16State {
   int chunk_cur, chunk_nxt;
   int base;
   uint32_t sel_nxt[8];
+  uint32_t bot7;  // lane 31: absolute bottom-row H' of the previous group's last step
 };
 
 template <int KR, bool SYS, bool MASKED>
@@ -328,7 +329,6 @@ __device__ __forceinline__ void cb_h16_group(CbH16State<KR>& st, const StripCtx&
   const uint16_t* sp16 = sel + (t0 + 8 - 2 * lane);
 #pragma unroll
   for (int q = 0; q < 8; ++q) st.sel_nxt[q] = __ldg(sp16 + q);
-  unsigned long long* op = static_cast<unsigned long long*>(C.bnd_out) + (t0 - 62);
   uint32_t bot[8];
   const int jc = t0 + 1 + lane;
   const int crel = (lane < 8 && jc <= w) ? st.chunk_cur - st.base : 0;
@@ -356,7 +356,26 @@ __device__ __forceinline__ void cb_h16_group(CbH16State<KR>& st, const StripCtx&
       st.Hp[k] = h;
     }
     const int jB = jT - 1;
-    bot[q] = st.Hp[H - 1] >> 16;  // lane 31's bottom row at local column jB, stored per group
+    bot[q] = st.Hp[H - 1] >> 16;  // lane 31's bottom row at local column jB
+    if (q == 6 && lane == 31) {
+      // local columns t0-63 .. t0-56 = the consumer's chunk [8c+1, 8c+8], published together
+      // (as nw_fill_h16.cuh; ring entries one slot up, 16-byte aligned pairs when c0 is even)
+      const unsigned long long tg = (unsigned long long)C.tag_out << 32;
+      const unsigned bb = (unsigned)st.base;
+      const unsigned long long e[8] = {tg | st.bot7, tg | (bot[0] + bb), tg | (bot[1] + bb), tg | (bot[2] + bb),
+                                       tg | (bot[3] + bb), tg | (bot[4] + bb), tg | (bot[5] + bb), tg | (bot[6] + bb)};
+      unsigned long long* p = static_cast<unsigned long long*>(C.bnd_out) + (t0 - 63);
+      const int j0 = t0 - 63;
+      if ((c0 & 1) == 0 && (!MASKED || (j0 >= 1 && j0 + 7 <= w))) {
+#pragma unroll
+        for (int u = 0; u < 8; u += 2)
+          asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p + u), "l"(e[u]), "l"(e[u + 1]) : "memory");
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (j0 + u >= 1 && j0 + u <= w) st_relaxed_u64(p + u, e[u]);
+      }
+    }
     if (MASKED && hm_strip && lane == 31 && jB == w) *hm = (int)bot[q] + st.base;  // H'(m, n)
     if (MASKED && rout) {  // the right column (local column w) -> the next block's rank
       if (jT == w) {
@@ -370,24 +389,7 @@ __device__ __forceinline__ void cb_h16_group(CbH16State<KR>& st, const StripCtx&
       }
     }
   }
-  // the group's 8 ring entries (local columns t0-62 .. t0-55) in one go, as nw_fill_h16.cuh:
-  // 64-bit vector elements (each single-copy atomic) when 16-byte aligned (c0 even)
-  if (lane == 31) {
-    const unsigned long long tg = (unsigned long long)C.tag_out << 32;
-    const bool vec = (c0 & 1) == 0;
-#pragma unroll
-    for (int q = 0; q < 8; q += 2) {
-      const int j0 = t0 - 62 + q;
-      const unsigned long long e0 = tg | (bot[q] + (unsigned)st.base);
-      const unsigned long long e1 = tg | (bot[q + 1] + (unsigned)st.base);
-      if (vec && (!MASKED || (j0 >= 1 && j0 + 1 <= w))) {
-        asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(op + q), "l"(e0), "l"(e1) : "memory");
-      } else {
-        if (j0 >= 1 && j0 <= w) st_relaxed_u64(op + q, e0);
-        if (j0 + 1 >= 1 && j0 + 1 <= w) st_relaxed_u64(op + q + 1, e1);
-      }
-    }
-  }
+  st.bot7 = bot[7] + (unsigned)st.base;  // local column t0-55: published with the next chunk
 }
 
 template <int KR, bool SYS>
@@ -435,8 +437,8 @@ __global__ void __launch_bounds__(32) k_fill_cblock_h16(CBlockArgs A) {
     StripCtx C;
     C.b = A.b + T.c0;
     C.sprof = nullptr;
-    C.bnd_in = (s > 0) ? ring + (size_t)(s & 1) * A.bstride + T.c0 : nullptr;
-    C.bnd_out = ring + (size_t)((s + 1) & 1) * A.bstride + T.c0;
+    C.bnd_in = (s > 0) ? ring + (size_t)(s & 1) * A.bstride + T.c0 + 1 : nullptr;  // column j at index j+1
+    C.bnd_out = ring + (size_t)((s + 1) & 1) * A.bstride + T.c0 + 1;
     C.tag_in = T.seq - 1u;
     C.tag_out = T.seq;
     C.dir_base = nullptr;
@@ -447,6 +449,7 @@ __global__ void __launch_bounds__(32) k_fill_cblock_h16(CBlockArgs A) {
     C.n = T.w;
     C.s = s;
     C.lane = lane;
+    st.bot7 = 0;
     const bool hm_strip = s == A.S - 1 && T.c1 == A.n;
     if (s > 0) st.chunk_nxt = chunk_verify<true>(C, 0, chunk_issue<true>(C, 0));
     const int ngrp = (T.w + 63 + 7) / 8;
@@ -463,6 +466,11 @@ __global__ void __launch_bounds__(32) k_fill_cblock_h16(CBlockArgs A) {
       if (masked) cb_h16_group<KR, SYS, true>(st, C, sel, t0, Bv, T.c0, hm_strip, T.rout, T.rtag, A.hm);
       else cb_h16_group<KR, SYS, false>(st, C, sel, t0, Bv, T.c0, hm_strip, T.rout, T.rtag, A.hm);
       if (more) st.chunk_nxt = chunk_verify<true>(C, t0 + 8, raw);
+    }
+    if (lane == 31) {  // the last step's ring entry (local column 8 ngrp - 63), if inside the block
+      const int jl = 8 * ngrp - 63;
+      if (jl >= 1 && jl <= T.w)
+        st_relaxed_u64(static_cast<unsigned long long*>(C.bnd_out) + jl, ((unsigned long long)T.seq << 32) | st.bot7);
     }
     __syncwarp();
   }

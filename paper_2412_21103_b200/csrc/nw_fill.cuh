@@ -60,6 +60,8 @@ struct FillArgs {
                                       //   (17 b[i] + 128) | (17 b[i-1] + 196) << 8 (prmt2 of PA/PB)
   long long watchdog = 1LL << 28;     // re-polls of a late boundary chunk before *err is raised
   unsigned long long* trace = nullptr;  // experiment builds only (NW_TRACE): per-strip timestamps
+  const uint16_t* sel4 = nullptr;     // h16 sweep: 4 copies of the selector table, copy k (stride
+  long long sel4_stride = 0;          //   sel4_stride entries) holding sel[i - 2k] at entry i
   int reb_groups = 64;                // h16 single-pair sweep: rebase period (8-step groups, power of 2)
   int withhold = 0;                   // test only (NW_OPT_TEST_WITHHOLD): strip withhold-1 writes its
   void* sink = nullptr;               //   bottom row to `sink` instead, so its consumer never sees it
@@ -130,6 +132,7 @@ struct StripCtx {
   unsigned tag_out;                 // tag this sweep writes (column-block sweeps; others use s+1)
   void* bnd_out;                    // boundary row written (this strip's bottom)
   uint16_t* dir_base;               // this lane's decision-bit halfwords
+  long long wpl;                    // h16 with directions: 8-step (int32) groups per strip
   int* err;
   int* hm;
   unsigned poll_ns;
@@ -192,6 +195,9 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
   constexpr int R = 32 * KR;
   using T = Tie<PI>;
   const int lane = C.lane, n = C.n;
+#ifdef NW_I32_GROUPSTORE
+  int bot[8];
+#endif
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int t = t0 + q;
@@ -245,7 +251,12 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
     }
     st.diag = MASKED ? ((j >= 1) ? up : 0) : up;
     st.send = st.Hl[KR - 1];
+#ifdef NW_I32_GROUPSTORE
+    bot[q] = st.send;
+    if (false) {
+#else
     if (lane == 31 && (!MASKED || (j >= 1 && j <= n))) {
+#endif
       // lane 31's column is j = t - 30: stores step through the group's base pointers
       // (stored per step: buffering the group's 8 values for one vector store, as the
       // packed H' sweep does, made C2 slower, 1.59 -> 1.68 ms: the later publication
@@ -265,6 +276,30 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
       *C.hm = w;
     }
   }
+#ifdef NW_I32_GROUPSTORE
+  if (lane == 31) {
+#pragma unroll
+    for (int q = 0; q < 8; q += 2) {
+      const int j0 = t0 - 30 + q;
+      const bool both = !MASKED || (j0 >= 1 && j0 + 1 <= n);
+      if (MULTIWARP) {
+        unsigned long long* p = static_cast<unsigned long long*>(C.bnd_out) + j0;
+        const unsigned long long tg = (unsigned long long)(unsigned)(C.s + 1) << 32;
+        const unsigned long long e0 = tg | (unsigned)bot[q], e1 = tg | (unsigned)bot[q + 1];
+        if (both) {
+          asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(e0), "l"(e1) : "memory");
+        } else {
+          if (j0 >= 1 && j0 <= n) st_relaxed_u64(p, e0);
+          if (j0 + 1 >= 1 && j0 + 1 <= n) st_relaxed_u64(p + 1, e1);
+        }
+      } else {
+        int* p = static_cast<int*>(C.bnd_out) + j0;
+        if (j0 >= 1 && j0 <= n) p[0] = bot[q];
+        if (j0 + 1 >= 1 && j0 + 1 <= n) p[1] = bot[q + 1];
+      }
+    }
+  }
+#endif
   if (DIRS) {  // group g = t0/8: halfword (g, r, lane), step k at bits (15-2k, 14-2k) = (nbX, nbY)
     uint16_t* d = C.dir_base + (long long)(t0 >> 3) * (KR * 32);
 #pragma unroll
@@ -344,6 +379,13 @@ __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, 
 #pragma unroll 1
   for (int g = 0; g < ngrp; ++g) {
     const int t0 = g * 8;
+#ifdef NW_TRACE
+    if (MULTIWARP && A.trace && lane == 0 && (g & 255) == 0 && (g >> 8) < 256) {
+      unsigned long long ts;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+      A.trace[(size_t)s * 256 + (g >> 8)] = ts;
+    }
+#endif
     st.chunk_cur = st.chunk_nxt;
     const bool more = has_top && t0 + 8 < n;
     unsigned long long raw = 0;

@@ -33,25 +33,29 @@ struct H16State {
   uint32_t up0_prev;                // up(0) of the previous step (diag of packed 0)
   int chunk_cur, chunk_nxt;         // boundary H' (absolute) of 8 columns, lane q < 8: column t0+1+q
   int base;                         // B (warp-uniform)
-  uint32_t sel_nxt[8];              // selector table entries of the next group (prefetched)
+  uint4 sel_nxt;                    // selector entries of the next group: 8 x u16 in one 16-byte load
+  uint32_t acc[KR / 2], accp[KR / 2];  // DIRS: decision flags of this / the previous 8-step group
+  uint32_t bot7;                    // lane 31: absolute bottom-row H' of the previous group's last step
 };
 
 // 8 steps (t0 % 8 == 0). MASKED groups hold a half outside [1, n] or the cell (m, n).
-template <int KR, bool MASKED>
+template <int KR, bool MASKED, bool DIRS = false, int PI = 123>
 __device__ __forceinline__ void h16_group(H16State<KR>& st, const StripCtx& C, const uint16_t* sel,
                                           int t0) {
+  using T = Tie<PI>;
   constexpr int H = KR / 2;
   const int lane = C.lane, n = C.n;
   // selectors of this group (prefetched one group ahead: a lone warp otherwise waits
   // for the first of them every group, ncu) and the loads of the next group's;
   // entry jT - 1 holds the codes of columns jT (low half) and jT - 1 (high half)
-  uint32_t scur[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) scur[q] = st.sel_nxt[q];
-  const uint16_t* sp16 = sel + (t0 + 8 - 2 * lane);
-#pragma unroll
-  for (int q = 0; q < 8; ++q) st.sel_nxt[q] = __ldg(sp16 + q);
-  unsigned long long* op = static_cast<unsigned long long*>(C.bnd_out) + (t0 - 62);
+  // One 16-byte load per lane and group from the lane's shifted copy of the table
+  // (FillArgs::sel4: copy k = lane % 4 is shifted by 2k entries, so the lane's 8 entries
+  // start 16-byte aligned); odd entries are the high halves, moved down by an IMAD.HI
+  // (FMA pipe; PRMT reads only the low 16 bits of its selector).
+  const uint4 wcur = st.sel_nxt;
+  st.sel_nxt = __ldg(reinterpret_cast<const uint4*>(sel + (t0 + 8 - 2 * lane)));
+  const uint32_t scur[8] = {wcur.x, __umulhi(wcur.x, 65536u), wcur.y, __umulhi(wcur.y, 65536u),
+                            wcur.z, __umulhi(wcur.z, 65536u), wcur.w, __umulhi(wcur.w, 65536u)};
   uint32_t bot[8];
   // lane 0 takes the boundary values relative to B (columns beyond n: 0, never read
   // by a cell inside the grid, and small enough to keep every half in range)
@@ -76,7 +80,18 @@ __device__ __forceinline__ void h16_group(H16State<KR>& st, const StripCtx& C, c
     for (int k = 0; k < H; ++k) {
       const uint32_t sp = prmt2(st.PA[k], st.PB[k], s);
       const uint32_t left = st.Hp[k];
-      uint32_t h = __vimax3_u16x2(diag + sp, left, up);
+      const uint32_t cd = diag + sp;
+      uint32_t h = __vimax3_u16x2(cd, left, up);
+      if (DIRS) {
+        // P:90 decision for the tie order pi = (X, Y, Z): nbX = [c_X < H'], nbY = [c_Y < H'],
+        // per half min(H' - c, 1) (H' >= c: no borrow between halves); two IMADs put step q
+        // of the group at bits (2(7-q)+1, 2(7-q)) = (nbX, nbY) of each half, the int32
+        // sweep's order (nw_fill.cuh)
+        const uint32_t cX = T::X == 1 ? cd : (T::X == 2 ? up : left);
+        const uint32_t cY = T::Y == 1 ? cd : (T::Y == 2 ? up : left);
+        const uint32_t m = __vminu2(h - cX, 0x00010001u) * 2u + __vminu2(h - cY, 0x00010001u);
+        st.acc[k] = (q == 0 ? 0u : st.acc[k] * 4u) + m;
+      }
       if (MASKED) h &= mask;  // border column H'(i, 0) = 0 until each half starts (B = 0 then)
       diag = left;
       up = h;
@@ -86,6 +101,26 @@ __device__ __forceinline__ void h16_group(H16State<KR>& st, const StripCtx& C, c
     // (a global store every step sat in the MIO queue ahead of the next step's shuffle:
     // +40-60 cycles per step, tools/h16_step.cu)
     bot[q] = st.Hp[H - 1] >> 16;
+    if (q == 6 && lane == 31) {
+      // columns t0-63 .. t0-56 = the consumer's chunk [8c+1, 8c+8] (c = t0/8 - 8), complete
+      // now: publish them together, so the next strip's chunk is valid at once (entries
+      // sit one slot up: column j at ring index j+1, 16-byte aligned for j = 8c+1)
+      const unsigned long long tg = (unsigned long long)C.tag_out << 32;
+      const unsigned b = (unsigned)st.base;
+      const unsigned long long e[8] = {tg | st.bot7, tg | (bot[0] + b), tg | (bot[1] + b), tg | (bot[2] + b),
+                                       tg | (bot[3] + b), tg | (bot[4] + b), tg | (bot[5] + b), tg | (bot[6] + b)};
+      unsigned long long* p = static_cast<unsigned long long*>(C.bnd_out) + (t0 - 63);
+      const int j0 = t0 - 63;
+      if (!MASKED || (j0 >= 1 && j0 + 7 <= n)) {
+#pragma unroll
+        for (int u = 0; u < 8; u += 2)
+          asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p + u), "l"(e[u]), "l"(e[u + 1]) : "memory");
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (j0 + u >= 1 && j0 + u <= n) st_relaxed_u64(p + u, e[u]);
+      }
+    }
     if (MASKED && C.hm_lane == lane && C.hm_t == t) {  // H'(m, n), absolute
       const int hk = C.hm_r >= H ? C.hm_r - H : C.hm_r;
       uint32_t w = 0;
@@ -94,26 +129,28 @@ __device__ __forceinline__ void h16_group(H16State<KR>& st, const StripCtx& C, c
       *C.hm = (int)(C.hm_r >= H ? (w >> 16) : (w & 0xffffu)) + st.base;
     }
   }
-  // the group's 8 bottom-row entries (columns t0-62 .. t0-55), tagged and absolute, as
-  // four 16-byte stores of two 64-bit elements: each element is a single-copy-atomic
-  // 8-byte access, so every entry still carries its own validity (nw_fill.cuh). Entries
-  // are 16-byte aligned (t0 - 62 + q even, even row stride). Columns outside [1, n] are
-  // skipped.
-  if (lane == 31) {
-    const unsigned long long tg = (unsigned long long)C.tag_out << 32;
+  if (DIRS) {
+    // Store the flags in the int32 sweep's layout (nw_fill.cuh: halfword ((s*G + g)*KR +
+    // r)*32 + l, int32 step t = j - 1 + l, so the traceback kernels read either fill):
+    // here the low half of lane l is at int32 step t0 + q - l, the high half at
+    // t0 + q - l - 1. With l' = l (low) or l + 1 (high) = 8a + d, int32 group
+    // g = t0/8 - a - 1 is complete after this group: its 8 steps are the previous
+    // group's steps d..7 and this group's steps 0..d-1, i.e. bits 16-2d.. of
+    // (prev << 16 | cur). Groups outside [0, G) are not stored.
+    const int G = (int)C.wpl;
+    const int glo = (t0 >> 3) - (lane >> 3) - 1, dlo = lane & 7;
+    const int ghi = (t0 >> 3) - ((lane + 1) >> 3) - 1, dhi = (lane + 1) & 7;
+    uint16_t* d = C.dir_base;
 #pragma unroll
-    for (int q = 0; q < 8; q += 2) {
-      const int j0 = t0 - 62 + q;  // column of entry q (lane 31's jB at step t0 + q)
-      const unsigned long long e0 = tg | (bot[q] + (unsigned)st.base);
-      const unsigned long long e1 = tg | (bot[q + 1] + (unsigned)st.base);
-      if (!MASKED || (j0 >= 1 && j0 + 1 <= n)) {
-        asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(op + q), "l"(e0), "l"(e1) : "memory");
-      } else {
-        if (j0 >= 1 && j0 <= n) st_relaxed_u64(op + q, e0);
-        if (j0 + 1 >= 1 && j0 + 1 <= n) st_relaxed_u64(op + q + 1, e1);
-      }
+    for (int k = 0; k < H; ++k) {
+      const uint32_t xlo = prmt2(st.acc[k], st.accp[k], 0x5410u);  // prev low << 16 | cur low
+      const uint32_t xhi = prmt2(st.acc[k], st.accp[k], 0x7632u);  // prev high << 16 | cur high
+      if (glo >= 0 && glo < G) d[((long long)glo * KR + k) * 32] = (uint16_t)(xlo >> (16 - 2 * dlo));
+      if (ghi >= 0 && ghi < G) d[((long long)ghi * KR + k + H) * 32] = (uint16_t)(xhi >> (16 - 2 * dhi));
+      st.accp[k] = st.acc[k];
     }
   }
+  st.bot7 = bot[7] + (unsigned)st.base;  // column t0-55: published with the next group's chunk
 }
 
 // Moves B up by the warp's minimum live relative value (all halves of Hp and up0_prev).
@@ -133,10 +170,12 @@ __device__ __forceinline__ void h16_rebase(H16State<KR>& st) {
   st.base += d;
 }
 
-// One strip, score-only, MULTIWARP (tagged 64-bit entries). A.sel: the selector
-// table of nw_fill16.cuh aligned with b; A.reb_groups: rebase period in 8-step groups
+// One strip, score-only, MULTIWARP (tagged 64-bit entries). A.sel4: four shifted copies
+// of the selector table of nw_fill16.cuh aligned with b; A.reb_groups: rebase period in 8-step groups
 // (a power of two).
-template <int KR>
+// DIRS: also the P:90 decision bits for the tie order PI, stored in the int32 sweep's
+// layout (A.dirs, A.wpl groups per strip), so the strip traceback reads them unchanged.
+template <int KR, bool DIRS = false, int PI = 123>
 __device__ __forceinline__ void strip_sweep_h16(const FillArgs& A, int s, int lane) {
   static_assert(KR % 2 == 0 && KR <= 32, "KR must be even");
   constexpr int H = KR / 2;
@@ -155,22 +194,29 @@ __device__ __forceinline__ void strip_sweep_h16(const FillArgs& A, int s, int la
     st.PA[k] = w0;
     st.PB[k] = w1;
     st.Hp[k] = 0;
+    st.acc[k] = 0;
+    st.accp[k] = 0;
   }
   st.up0_prev = 0;
   st.base = 0;
   st.chunk_cur = st.chunk_nxt = 0;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) st.sel_nxt[q] = __ldg(A.sel + (q - 2 * lane));  // group 0
+  // the lane's copy of the selector table (entry i of copy k holds sel[i - 2k])
+  const uint16_t* sel = A.sel4 + (lane & 3) * A.sel4_stride + 2 * (lane & 3);
+  st.sel_nxt = __ldg(reinterpret_cast<const uint4*>(sel - 2 * lane));  // group 0
   StripCtx C;
   C.tag_in = (unsigned)s;
   C.tag_out = (unsigned)s + 1;
   C.b = A.b;
   C.sprof = nullptr;
   char* bnd = static_cast<char*>(A.bnd);
-  C.bnd_in = (s > 0) ? bnd + 8 * (size_t)((s % A.nslots) * A.bstride) : nullptr;
-  C.bnd_out = bnd + 8 * (size_t)(((s + 1) % A.nslots) * A.bstride);
-  if (s + 1 == A.withhold) C.bnd_out = A.sink;
-  C.dir_base = nullptr;
+  // entries one slot up (column j at index j + 1): the chunk-aligned publication of
+  // h16_group stores 16-byte-aligned pairs
+  C.bnd_in = (s > 0) ? bnd + 8 * (size_t)((s % A.nslots) * A.bstride + 1) : nullptr;
+  C.bnd_out = bnd + 8 * (size_t)(((s + 1) % A.nslots) * A.bstride + 1);
+  if (s + 1 == A.withhold) C.bnd_out = static_cast<char*>(A.sink) + 8;
+  st.bot7 = 0;
+  C.dir_base = DIRS ? A.dirs + (long long)s * A.wpl * (KR * 32) + lane : nullptr;
+  C.wpl = A.wpl;
   C.err = A.err;
   C.poll_ns = A.poll_ns;
   C.watchdog = A.watchdog;
@@ -196,10 +242,10 @@ __device__ __forceinline__ void strip_sweep_h16(const FillArgs& A, int s, int la
     const int t0 = g * 8;
     if ((g & rmask) == 0 && g > 0) h16_rebase<KR>(st);
 #ifdef NW_TRACE
-    if (A.trace && lane == 0 && (g & 1023) == 0 && (g >> 10) < 256) {
+    if (A.trace && lane == 0 && (g & 255) == 0 && (g >> 8) < 256) {
       unsigned long long ts;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
-      A.trace[(size_t)s * 256 + (g >> 10)] = ts;
+      A.trace[(size_t)s * 256 + (g >> 8)] = ts;
     }
 #endif
     st.chunk_cur = st.chunk_nxt;
@@ -207,9 +253,25 @@ __device__ __forceinline__ void strip_sweep_h16(const FillArgs& A, int s, int la
     unsigned long long raw = 0;
     if (more) raw = chunk_issue<true>(C, t0 + 8);
     const bool masked = t0 < 64 || t0 + 7 >= n - 1;
-    if (masked) h16_group<KR, true>(st, C, A.sel, t0);
-    else h16_group<KR, false>(st, C, A.sel, t0);
+    if (masked) h16_group<KR, true, DIRS, PI>(st, C, sel, t0);
+    else h16_group<KR, false, DIRS, PI>(st, C, sel, t0);
     if (more) st.chunk_nxt = chunk_verify<true>(C, t0 + 8, raw);
+  }
+  if (lane == 31) {  // the last step's bottom-row entry (column 8 ngrp - 63), if inside the grid
+    const int jl = 8 * ngrp - 63;
+    if (jl >= 1 && jl <= n)
+      st_relaxed_u64(static_cast<unsigned long long*>(C.bnd_out) + jl,
+                     ((unsigned long long)C.tag_out << 32) | st.bot7);
+  }
+  if (DIRS) {  // the last int32 group of lane 31's high half (l + 1 = 32: d = 0, a = 4)
+    const int G = (int)A.wpl;
+    const int ghi = ngrp - ((lane + 1) >> 3) - 1;
+    const int glo = ngrp - (lane >> 3) - 1;
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      if (ghi < G && ((lane + 1) & 7) == 0) C.dir_base[((long long)ghi * KR + k + H) * 32] = (uint16_t)(st.accp[k] >> 16);
+      if (glo < G && (lane & 7) == 0) C.dir_base[((long long)glo * KR + k) * 32] = (uint16_t)(st.accp[k] & 0xffffu);
+    }
   }
   __syncwarp();
 }

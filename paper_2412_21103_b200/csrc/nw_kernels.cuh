@@ -74,6 +74,19 @@ __global__ void k_encode(const uint8_t* __restrict__ in, long long len,
 
 // Selector table of the packed sweeps (FillArgs::sel): sel[i] = (17 c[i] + 128) |
 // (17 c[i-1] + 196) << 8 over codes c[-1 .. len) (c[-1] read from the padding).
+// Four shifted copies of the selector table for 16-byte-aligned per-lane loads
+// (nw_fill_h16.cuh): out[k*stride + PAD + i] = sel[i - 2k] for i in [-PAD, stride - PAD),
+// sel[j] = (17 b[j] + 128) | (17 b[j-1] + 196) << 8, b = codes (readable on [-PAD, n + PAD));
+// entries whose codes fall outside that range are 0 (never used inside the grid).
+__global__ void k_sel16x4(const uint8_t* __restrict__ b, long long n, uint16_t* __restrict__ out,
+                          long long stride) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < 4 * stride;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long k = e / stride, j = (e % stride) - PAD - 2 * k;
+    out[e] = (j - 1 >= -PAD && j < n + PAD) ? (uint16_t)((17u * b[j] + 128u) | ((17u * b[j - 1] + 196u) << 8)) : 0;
+  }
+}
+
 __global__ void k_sel16(const uint8_t* __restrict__ codes, long long len, uint16_t* __restrict__ sel) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len;
        i += (long long)gridDim.x * blockDim.x)
@@ -98,7 +111,7 @@ __global__ void __launch_bounds__(32) k_fill_pair(FillArgs A) {
     if (lane == 0) s = atomicAdd(A.ticket, 1);
     s = __shfl_sync(FULL, s, 0);
     if (s >= A.nstrips) break;
-    if constexpr (D16 == 3) strip_sweep_h16<KR>(A, s, lane);
+    if constexpr (D16 == 3) strip_sweep_h16<KR, DIRS, PI>(A, s, lane);
     else if constexpr (D16 == 2) strip_sweep_d16x2<KR, true>(A, s, lane);
     else if constexpr (D16 == 1) strip_sweep_d16<KR, true>(A, s, lane);
     else strip_sweep<KR, DIRS, PROFREG, PI, true>(A, s, lane, smem);

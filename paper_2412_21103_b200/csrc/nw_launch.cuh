@@ -17,6 +17,9 @@ void launch_fill_dirs(const FillArgs& A, int kr, bool profreg, int grid, size_t 
 template <int PI>
 void launch_batch_dirs(const BatchArgs& B, bool profreg, int packed_kr, int grid, size_t smem,
                        cudaStream_t st);
+// the packed H' single-pair fill with decision bits (nw_fill_h16.cuh), KR 4 or 8
+template <int PI>
+void launch_fill_dirs_h16(const FillArgs& A, int kr, int grid, cudaStream_t st);
 
 template <int KR, bool DIRS, bool PROFREG, int PI, int D16 = 0>
 void launch_fill_t(const FillArgs& A, int grid, size_t smem, cudaStream_t st) {
@@ -54,6 +57,11 @@ void launch_batch_t(const BatchArgs& B, int grid, size_t smem, cudaStream_t st) 
       if (profreg) launch_fill_t<8, true, true, PI>(A, grid, smem, st);                       \
       else launch_fill_t<8, true, false, PI>(A, grid, smem, st);                              \
     }                                                                                         \
+  }                                                                                           \
+  template <>                                                                                 \
+  void launch_fill_dirs_h16<PI>(const FillArgs& A, int kr, int grid, cudaStream_t st) {       \
+    if (kr == 8) launch_fill_t<8, true, true, PI, 3>(A, grid, 0, st);                         \
+    else launch_fill_t<4, true, true, PI, 3>(A, grid, 0, st);                                 \
   }                                                                                           \
   template <>                                                                                 \
   void launch_batch_dirs<PI>(const BatchArgs& B, bool profreg, int packed_kr, int grid,      \

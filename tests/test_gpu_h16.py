@@ -98,3 +98,24 @@ def test_h16_watchdog(ctx, opts):
     with pytest.raises(nwb.NWError) as e:
         nwb.nw_score_only(ctx, a, b, nwgen.PAPER_DNA)
     assert e.value.status == nwb.NW_E_DEADLOCK
+
+
+ORDERS = [(1, 2, 3), (1, 3, 2), (2, 1, 3), (2, 3, 1), (3, 1, 2), (3, 2, 1)]
+
+
+@pytest.mark.parametrize("tie", ORDERS)
+@pytest.mark.parametrize("kr", [0, 8])
+def test_h16_direction_fill_traceback(ctx, opts, tie, kr):
+    """pair_form 2: direction fills of DNA pairs in the packed H' form, flags re-phased
+    into the int32 layout so the strip traceback reads them unchanged: score and op string
+    vs the oracle for every tie order, several strips, ragged edges, a degenerate column."""
+    opts(ctx, "pair_form", 2)
+    opts(ctx, "rows_per_lane", kr)
+    for k, (m, n) in enumerate([(1000, 1000), (700, 2300), (2600, 333), (129, 1), (5, 77)]):
+        a, b = nwgen.random_pair(9900 + 7 * k + kr, m, n)
+        for sc in (nwgen.Scoring(tie=tie), nwgen.Scoring(match=2, mismatch=-1, gap=-3, tie=tie)):
+            want_score, want_ops = oracle.align(a, b, sc)
+            got, tb = nwb.nw_align_pair(ctx, a, b, sc)
+            ops = nwb.nw_traceback(ctx, tb)
+            tb.free()
+            assert got == want_score and ops.tolist() == want_ops.tolist(), (tie, kr, m, n)

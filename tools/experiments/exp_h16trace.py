@@ -27,10 +27,10 @@ k = L.nw_debug_trace(buf.ctypes.data, S)
 t = buf[:k].astype(np.float64)
 t0 = t[0, 0]
 ng = (len(b) + 63 + 7) // 8
-nslot = (ng + 1023) // 1024
+nslot = min((ng + 255) // 256, 256)
 t = (t[:, :nslot] - t0) / 1e3  # us
 start = t[:, 0]
-pace = (t[:, nslot - 1] - t[:, 1]) / ((nslot - 2) * 1024 * 8) * 1e3  # ns per step
+pace = (t[:, nslot - 1] - t[:, 1]) / ((nslot - 2) * 256 * 8) * 1e3  # ns per step
 print(json.dumps({"form": form, "kr": kr, "strips": int(k),
                   "start_us": {"s1": float(start[1]), "s100": float(start[100]), "last": float(start[-1])},
                   "lag_steps_mean": float(np.mean(np.diff(start)) / np.median(pace) * 1e3),
@@ -38,6 +38,6 @@ print(json.dumps({"form": form, "kr": kr, "strips": int(k),
                   "pace_cycles_median": float(np.median(pace) * 1.965),
                   "end_slot_us_last": float(t[-1, nslot - 1])}))
 # per-strip pace over the middle slots: is any strip consistently slower?
-mid = np.diff(t[:, 2:nslot - 2], axis=1) / (1024 * 8) * 1e3
+mid = np.diff(t[:, 2:nslot - 2], axis=1) / (256 * 8) * 1e3
 print("pace spread per slot (ns/step): median of per-slot max-min", float(np.median(mid.max(0) - mid.min(0))))
 print("strip 0..7 pace", [round(float(x), 1) for x in pace[:8]])

@@ -24,7 +24,7 @@ __global__ void k_step(uint32_t* out, long long* cyc, int steps, const uint16_t*
                        unsigned long long* sink) {
   constexpr int H = KR / 2;
   const int lane = threadIdx.x & 31;
-  uint32_t PA[C][H], PB[C][H], Hp[C][H], up0p[C];
+  uint32_t PA[C][H], PB[C][H], Hp[C][H], up0p[C], acc[C][H];
 #pragma unroll
   for (int c = 0; c < C; ++c) {
 #pragma unroll
@@ -32,6 +32,7 @@ __global__ void k_step(uint32_t* out, long long* cyc, int steps, const uint16_t*
       PA[c][k] = 0x01030103u * (lane + k + c);
       PB[c][k] = 0x03010301u * (lane + k + 2 * c);
       Hp[c][k] = 0;
+      acc[c][k] = 0;
     }
     up0p[c] = 0;
   }
@@ -60,13 +61,25 @@ __global__ void k_step(uint32_t* out, long long* cyc, int steps, const uint16_t*
         for (int k = 0; k < H; ++k) {
           const uint32_t sp = prmt2(PA[c][k], PB[c][k], s);
           const uint32_t left = Hp[c][k];
-          const uint32_t h = __vimax3_u16x2(diag + sp, left, up);
+          const uint32_t cd = diag + sp;
+          const uint32_t h = __vimax3_u16x2(cd, left, up);
+          if (F & 16) {  // decision flags (tie order D, U, L): nbX = [h != cD], nbY = [h != cU]
+            const uint32_t m = __vminu2(h - up, 0x00010001u) * 2u + __vminu2(h - cd, 0x00010001u);
+            acc[c][k] = acc[c][k] * 4u + m;
+          }
           diag = left;
           up = h;
           Hp[c][k] = h;
         }
         if ((F & 2) && lane == 31) sink[((t + q) & 1023) * 4 + c] = ((unsigned long long)(t + q) << 32) | Hp[c][H - 1];
       }
+    }
+    if (F & 16) {  // the group's flag words, as the batch traceback sweep stores them
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+#pragma unroll
+        for (int k = 0; k < H; k += 2)
+          *reinterpret_cast<uint2*>(sink + 8192 + ((((t >> 3) & 255) * 32 + lane) * H + k) / 2) = make_uint2(acc[c][k], acc[c][k + 1]);
     }
     if (F & 8) {
       chunk = (int)(unsigned)raw;
@@ -75,12 +88,12 @@ __global__ void k_step(uint32_t* out, long long* cyc, int steps, const uint16_t*
     selx ^= 0x1111u;
   }
   const long long t1 = clock64();
-  uint32_t acc = 0;
+  uint32_t sum = 0;
 #pragma unroll
   for (int c = 0; c < C; ++c)
 #pragma unroll
-    for (int k = 0; k < H; ++k) acc += Hp[c][k];
-  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+    for (int k = 0; k < H; ++k) sum += Hp[c][k] + acc[c][k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = sum;
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
@@ -107,8 +120,8 @@ int main() {
   unsigned long long* sink;
   cudaMalloc(&tab, 2 * 4096);
   cudaMemset(tab, 0x2c, 2 * 4096);
-  cudaMalloc(&sink, 8 * 16384);
-  cudaMemset(sink, 0, 8 * 16384);
+  cudaMalloc(&sink, 8 * 65536);
+  cudaMemset(sink, 0, 8 * 65536);
   printf("{\n");
   for (int W : {1, 2}) {
     run<28, 1, 0>(out, cyc, W, tab, sink);
@@ -118,6 +131,13 @@ int main() {
     run<28, 1, 8>(out, cyc, W, tab, sink);
     run<28, 1, 15>(out, cyc, W, tab, sink);
   }
+  // C2-like: lone warp, KR 4 / 6 / 8 with and without decision flags (+ per-step store)
+  run<4, 1, 0>(out, cyc, 1, tab, sink);
+  run<4, 1, 16>(out, cyc, 1, tab, sink);
+  run<4, 1, 18>(out, cyc, 1, tab, sink);
+  run<8, 1, 16>(out, cyc, 1, tab, sink);
+  run<8, 1, 18>(out, cyc, 1, tab, sink);
+  run<6, 1, 18>(out, cyc, 1, tab, sink);
   printf("  \"end\": 0\n}\n");
   return 0;
 }
