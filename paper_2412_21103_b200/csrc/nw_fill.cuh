@@ -195,9 +195,6 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
   constexpr int R = 32 * KR;
   using T = Tie<PI>;
   const int lane = C.lane, n = C.n;
-#ifdef NW_I32_GROUPSTORE
-  int bot[8];
-#endif
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int t = t0 + q;
@@ -251,16 +248,13 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
     }
     st.diag = MASKED ? ((j >= 1) ? up : 0) : up;
     st.send = st.Hl[KR - 1];
-#ifdef NW_I32_GROUPSTORE
-    bot[q] = st.send;
-    if (false) {
-#else
     if (lane == 31 && (!MASKED || (j >= 1 && j <= n))) {
-#endif
       // lane 31's column is j = t - 30: stores step through the group's base pointers
       // (stored per step: buffering the group's 8 values for one vector store, as the
       // packed H' sweep does, made C2 slower, 1.59 -> 1.68 ms: the later publication
-      // lengthens every strip hand-off)
+      // lengthens every strip hand-off; publishing per consumer chunk at the step its
+      // last column completes, 1.54 -> 1.61 ms: the burst of stores costs that step more
+      // than the per-step stores cost the pace, tools/experiments/exp_c2trace.py)
       if (MULTIWARP) {
         unsigned long long v;
         asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "r"(st.send), "r"(C.s + 1));  // (tag << 32) | H'
@@ -276,30 +270,6 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
       *C.hm = w;
     }
   }
-#ifdef NW_I32_GROUPSTORE
-  if (lane == 31) {
-#pragma unroll
-    for (int q = 0; q < 8; q += 2) {
-      const int j0 = t0 - 30 + q;
-      const bool both = !MASKED || (j0 >= 1 && j0 + 1 <= n);
-      if (MULTIWARP) {
-        unsigned long long* p = static_cast<unsigned long long*>(C.bnd_out) + j0;
-        const unsigned long long tg = (unsigned long long)(unsigned)(C.s + 1) << 32;
-        const unsigned long long e0 = tg | (unsigned)bot[q], e1 = tg | (unsigned)bot[q + 1];
-        if (both) {
-          asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(e0), "l"(e1) : "memory");
-        } else {
-          if (j0 >= 1 && j0 <= n) st_relaxed_u64(p, e0);
-          if (j0 + 1 >= 1 && j0 + 1 <= n) st_relaxed_u64(p + 1, e1);
-        }
-      } else {
-        int* p = static_cast<int*>(C.bnd_out) + j0;
-        if (j0 >= 1 && j0 <= n) p[0] = bot[q];
-        if (j0 + 1 >= 1 && j0 + 1 <= n) p[1] = bot[q + 1];
-      }
-    }
-  }
-#endif
   if (DIRS) {  // group g = t0/8: halfword (g, r, lane), step k at bits (15-2k, 14-2k) = (nbX, nbY)
     uint16_t* d = C.dir_base + (long long)(t0 >> 3) * (KR * 32);
 #pragma unroll
