@@ -684,6 +684,16 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
 #ifdef NW_TRACE
     if (!h16) A.trace = nw_trace_buffer(nstrips);
 #endif
+    if (!h16 && profreg && kr <= 4) {  // 8 shifted copies of the per-column selectors (FillArgs::sel8)
+      const long long ls = (n + 2 * PAD + 15) & ~7LL;
+      st = grow(c, c->d_sel16, c->sel16_cap, sizeof(uint16_t) * 8 * (size_t)ls);
+      if (st) return st;
+      const int blocks = (int)std::min<long long>((8 * ls + 255) / 256, (long long)c->sm_count * 8);
+      k_sel8x8<<<std::max(blocks, 1), 256, 0, c->stream>>>(cb, n, c->d_sel16, ls);
+      LAUNCHED(c);
+      A.sel8 = c->d_sel16 + PAD;
+      A.sel8_stride = ls;
+    }
     // persistent grid: one warp per CTA, at most the resident capacity
     int per_sm = 16;
     int grid = std::min<long long>(nstrips, (long long)c->sm_count * per_sm);

@@ -60,6 +60,9 @@ struct FillArgs {
                                       //   (17 b[i] + 128) | (17 b[i-1] + 196) << 8 (prmt2 of PA/PB)
   long long watchdog = 1LL << 28;     // re-polls of a late boundary chunk before *err is raised
   unsigned long long* trace = nullptr;  // experiment builds only (NW_TRACE): per-strip timestamps
+  const uint16_t* sel8 = nullptr;     // int32 MULTIWARP sweep with register profiles: 8 copies of the
+  long long sel8_stride = 0;          //   per-column PRMT selector (b*0x1111 + 0x8880), copy k holding
+                                      //   column code b[i - k] at entry i (16-byte-aligned lane loads)
   const uint16_t* sel4 = nullptr;     // h16 sweep: 4 copies of the selector table, copy k (stride
   long long sel4_stride = 0;          //   sel4_stride entries) holding sel[i - 2k] at entry i
   int reb_groups = 64;                // h16 single-pair sweep: rebase period (8-step groups, power of 2)
@@ -121,6 +124,8 @@ struct LaneState {
   int send;          // H'(bottom, j): sent to lane+1
   int chunk_cur, chunk_nxt;  // boundary values for 8 columns (lane q < 8 holds column t0+1+q)
   uint32_t bc_nxt;   // prefetched column code for the next step
+  uint4 selw;        // (MULTIWARP, PROFREG) the next group's 8 selectors, one 16-byte load
+  const uint16_t* seltab;  // this lane's copy of A.sel8, offset so that seltab[i] is b[i]'s selector
 };
 
 // Strip geometry / pointers that stay fixed during one sweep.
@@ -195,15 +200,29 @@ __device__ __forceinline__ void sweep_group(LaneState<KR>& st, const StripCtx& C
   constexpr int R = 32 * KR;
   using T = Tie<PI>;
   const int lane = C.lane, n = C.n;
+  constexpr bool VSEL = MULTIWARP && PROFREG && KR <= 4;  // (taller strips, e.g. the checkpointed refills: slower)
+  uint4 wsel = make_uint4(0, 0, 0, 0);
+  if constexpr (VSEL) {  // this group's selectors (loaded a group ahead), and the next group's
+    wsel = st.selw;
+    st.selw = __ldg(reinterpret_cast<const uint4*>(st.seltab + (t0 + 8 - lane)));
+  }
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int t = t0 + q;
     const int j = t - lane + 1;  // this lane's column (1-based)
-    const uint32_t bc = st.bc_nxt;
-    st.bc_nxt = __ldg(C.b + j);  // next step's b_{j+1} (PAD makes j in [-31, n+62] readable)
+    uint32_t bc = 0;
+    if constexpr (!VSEL) {
+      bc = st.bc_nxt;
+      st.bc_nxt = __ldg(C.b + j);  // next step's b_{j+1} (PAD makes j in [-31, n+62] readable)
+    }
     uint32_t sel = 0;
     uint2 pw = make_uint2(0, 0);
-    if constexpr (PROFREG) {
+    if constexpr (VSEL) {
+      // b[j-1]'s selector: entry q of the group's 16-byte block (odd entries: the high half,
+      // moved down by an IMAD.HI; PRMT reads only the low 16 bits of its selector)
+      const uint32_t w = (q >> 1) == 0 ? wsel.x : (q >> 1) == 1 ? wsel.y : (q >> 1) == 2 ? wsel.z : wsel.w;
+      sel = (q & 1) ? __umulhi(w, 65536u) : w;
+    } else if constexpr (PROFREG) {
       sel = bc * 0x1111u + 0x8880u;  // byte bc, sign-replicated into bytes 1..3 (bc < 8: no carry)
     } else if constexpr (KR == 8) {
       pw = *reinterpret_cast<const uint2*>(C.sprof + bc * R + lane * KR);
@@ -343,6 +362,11 @@ __device__ __forceinline__ void strip_sweep(const FillArgs& A, int s, int lane, 
     C.hm_lane = rr / KR; C.hm_r = rr % KR; C.hm_t = n - 1 + C.hm_lane;
   }
   st.bc_nxt = __ldg(A.b - lane);  // b_{j-1} for step 0 (j = 1 - lane)
+  if (MULTIWARP && PROFREG && KR <= 4) {  // lane's copy k = lane % 8 of the selector table: t0 - lane
+    const int k = lane & 7;    // + k are multiples of 8 (16-byte aligned)
+    st.seltab = A.sel8 + (long long)k * A.sel8_stride + k;
+    st.selw = __ldg(reinterpret_cast<const uint4*>(st.seltab - lane));  // group 0
+  }
   const bool has_top = C.bnd_in != nullptr;
   if (has_top) st.chunk_nxt = chunk_verify<MULTIWARP>(C, 0, chunk_issue<MULTIWARP>(C, 0));
   const int ngrp = (n + 31 + 7) / 8;  // steps 0 .. n+30 in groups of 8

@@ -87,6 +87,18 @@ __global__ void k_sel16x4(const uint8_t* __restrict__ b, long long n, uint16_t* 
   }
 }
 
+// Eight shifted copies of the int32 sweep's per-column PRMT selector (b * 0x1111 + 0x8880:
+// byte b of the profile word, sign-replicated): out[k*stride + PAD + i] = sel(b[i - k]) for
+// i - k in [-PAD, n + PAD), else 0 (nw_fill.cuh, FillArgs::sel8).
+__global__ void k_sel8x8(const uint8_t* __restrict__ b, long long n, uint16_t* __restrict__ out,
+                         long long stride) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < 8 * stride;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long k = e / stride, j = (e % stride) - PAD - k;
+    out[e] = (j >= -PAD && j < n + PAD) ? (uint16_t)(b[j] * 0x1111u + 0x8880u) : 0;
+  }
+}
+
 __global__ void k_sel16(const uint8_t* __restrict__ codes, long long len, uint16_t* __restrict__ sel) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len;
        i += (long long)gridDim.x * blockDim.x)
