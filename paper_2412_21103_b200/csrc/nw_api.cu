@@ -665,7 +665,7 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     }
     const bool profreg = sc->K <= 4;
     const size_t smem = profreg ? 0 : (size_t)sc->K * R;
-    const bool h16 = !ckpt && !top_row && h16_reb > 0;  // with dirs: KR 4 or 8 (the caller checks)
+    const bool h16 = !top_row && h16_reb > 0 && !(dirs && ckpt);  // with dirs: KR 4 or 8 (the caller checks)
     const bool d16 = !dirs && (kr >= 12 || (!ckpt && c->opt[NW_OPT_D16_FORCE] && d16_ok(c, sc)));
     if (h16) {  // 4 shifted copies of the selector table over cb[-PAD, n + PAD) (FillArgs::sel4)
       const long long ls = (n + 2 * PAD + 7) & ~7LL;
@@ -2720,6 +2720,8 @@ nw_status linear_core(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b
   // (its rows carry V; k_ckpt_prefix turns them into H' for the refills)
   const bool ck_d16 = d16_ok(c, sc) && m >= 32LL * 16 * 150 && !c->opt[NW_OPT_LINEAR_INT32];
   const int kr_ck = ck_d16 ? d16_kr(c, m) : choose_kr(c, m, n, false, sc->K);
+  // the packed H' form of §3.16 when it fits: its checkpoint rows already hold H'
+  const int ck_reb = (ck_d16 && c->opt[NW_OPT_PAIR_FORM] != 1) ? h16_rebase_groups(c, sc, kr_ck) : 0;
   const long long Rck = 32LL * kr_ck;
   const long long rows_max = std::max<long long>(1, budget / ((n + 38) / 4 + 1));
   const long long K = std::max<long long>(1, rows_max / Rck);
@@ -2732,9 +2734,9 @@ nw_status linear_core(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b
     CUDA_TRY(c, cudaMemsetAsync(ckpt, 0, ckb, c->stream));
   }
   auto done = [&](nw_status e) { if (ckpt) cudaFreeAsync(ckpt, c->stream); return e; };
-  st = pair_core(c, ca, m, cb, n, sc, c->d_score, nullptr, kr_ck, ckpt, (int)K, bstr, nullptr);
+  st = pair_core(c, ca, m, cb, n, sc, c->d_score, nullptr, kr_ck, ckpt, (int)K, bstr, nullptr, 0, ck_reb);
   if (st) return done(st);
-  if (ck_d16 && nseg > 1) {
+  if (ck_d16 && ck_reb == 0 && nseg > 1) {
     k_ckpt_prefix<<<(unsigned)nseg, 1024, 0, c->stream>>>(ckpt, bstr, (int)n, (int)nseg);
     LAUNCHED(c);
     CUDA_TRY(c, cudaGetLastError());

@@ -138,6 +138,7 @@ struct StripCtx {
   void* bnd_out;                    // boundary row written (this strip's bottom)
   uint16_t* dir_base;               // this lane's decision-bit halfwords
   long long wpl;                    // h16 with directions: 8-step (int32) groups per strip
+  int out_aligned;                  // h16: bnd_out is the ring shifted one slot (16-byte pairs), not a checkpoint row
   int* err;
   int* hm;
   unsigned poll_ns;

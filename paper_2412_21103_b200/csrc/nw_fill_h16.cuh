@@ -111,7 +111,7 @@ __device__ __forceinline__ void h16_group(H16State<KR>& st, const StripCtx& C, c
                                        tg | (bot[3] + b), tg | (bot[4] + b), tg | (bot[5] + b), tg | (bot[6] + b)};
       unsigned long long* p = static_cast<unsigned long long*>(C.bnd_out) + (t0 - 63);
       const int j0 = t0 - 63;
-      if (!MASKED || (j0 >= 1 && j0 + 7 <= n)) {
+      if (C.out_aligned && (!MASKED || (j0 >= 1 && j0 + 7 <= n))) {
 #pragma unroll
         for (int u = 0; u < 8; u += 2)
           asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p + u), "l"(e[u]), "l"(e[u + 1]) : "memory");
@@ -213,6 +213,16 @@ __device__ __forceinline__ void strip_sweep_h16(const FillArgs& A, int s, int la
   // h16_group stores 16-byte-aligned pairs
   C.bnd_in = (s > 0) ? bnd + 8 * (size_t)((s % A.nslots) * A.bstride + 1) : nullptr;
   C.bnd_out = bnd + 8 * (size_t)(((s + 1) % A.nslots) * A.bstride + 1);
+  C.out_aligned = 1;
+  if (A.ckpt != nullptr) {  // checkpointed traceback pass: every ck_every-th
+    // strip leaves its bottom row (absolute H', tagged s + 1, column j at index j: the refills'
+    // layout) in a kept slot, which the next strip reads instead of the ring
+    if ((s + 1) % A.ck_every == 0) {
+      C.bnd_out = A.ckpt + (long long)((s + 1) / A.ck_every - 1) * A.ck_stride;
+      C.out_aligned = 0;
+    }
+    if (s > 0 && s % A.ck_every == 0) C.bnd_in = A.ckpt + (long long)(s / A.ck_every - 1) * A.ck_stride;
+  }
   if (s + 1 == A.withhold) C.bnd_out = static_cast<char*>(A.sink) + 8;
   st.bot7 = 0;
   C.dir_base = DIRS ? A.dirs + (long long)s * A.wpl * (KR * 32) + lane : nullptr;
