@@ -665,7 +665,7 @@ nw_status pair_core(nw_ctx* c, const uint8_t* ca, long long m, const uint8_t* cb
     }
     const bool profreg = sc->K <= 4;
     const size_t smem = profreg ? 0 : (size_t)sc->K * R;
-    const bool h16 = !top_row && h16_reb > 0 && !(dirs && ckpt);  // with dirs: KR 4 or 8 (the caller checks)
+    const bool h16 = h16_reb > 0 && !(dirs && ckpt);  // with dirs: KR 4 or 8 (the caller checks)
     const bool d16 = !dirs && (kr >= 12 || (!ckpt && c->opt[NW_OPT_D16_FORCE] && d16_ok(c, sc)));
     if (h16) {  // 4 shifted copies of the selector table over cb[-PAD, n + PAD) (FillArgs::sel4)
       const long long ls = (n + 2 * PAD + 7) & ~7LL;
@@ -2757,14 +2757,21 @@ nw_status linear_core(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b
     ZeroRanges zb{{c->d_bnd, nullptr, nullptr, nullptr}, {bbytes, 0, 0, 0}};
     st = init_small(c, 8, zb);  // fresh ticket, error flag and ring tags for this fill
     if (st) break;
-    const int kr = choose_kr(c, mm, col, true, sc->K);
+    int kr = choose_kr(c, mm, col, true, sc->K);
+    // tall refills of DNA-size pairs: the packed H' direction fill (§3.16) at 8 rows per
+    // lane, its flags in the int32 layout (NW_OPT_PAIR_FORM = 1: the int32 fill)
+    int rf_reb = 0;
+    if (ck_d16 && kr >= 8 && c->opt[NW_OPT_PAIR_FORM] != 1 && !c->opt[NW_OPT_LINEAR_INT32]) {
+      rf_reb = h16_rebase_groups(c, sc, 8);
+      if (rf_reb > 0) kr = 8;
+    }
     nw_tb* tb = nullptr;
     st = new_tb(c, mm, col, sc, kr, &tb);
     if (st) break;
     const unsigned long long* top = sg > 0 ? ckpt + (sg - 1) * bstr : nullptr;
     // the checkpoint row above segment sg was written by strip sg*K - 1: tag sg*K
     st = pair_core(c, ca + r0, mm, cb, col, sc, c->d_score, tb, kr, nullptr, 0, 0, top,
-                   (unsigned)(sg * K));
+                   (unsigned)(sg * K), rf_reb);
     int* d_exit = c->d_ints + 6;
     if (!st) st = grow(c, c->d_rev, c->rev_cap, (size_t)(mm + col));
     if (!st) st = traceback_core(c, tb, d_ops, sg == 0, d_exit);

@@ -223,6 +223,10 @@ __device__ __forceinline__ void strip_sweep_h16(const FillArgs& A, int s, int la
     }
     if (s > 0 && s % A.ck_every == 0) C.bnd_in = A.ckpt + (long long)(s / A.ck_every - 1) * A.ck_stride;
   }
+  if (s == 0 && A.top_row != nullptr) {  // a refill segment's strip 0: the checkpoint row above
+    C.bnd_in = A.top_row;                 // (absolute H', column j at index j; tag top_tag)
+    C.tag_in = A.top_tag;
+  }
   if (s + 1 == A.withhold) C.bnd_out = static_cast<char*>(A.sink) + 8;
   st.bot7 = 0;
   C.dir_base = DIRS ? A.dirs + (long long)s * A.wpl * (KR * 32) + lane : nullptr;
@@ -244,7 +248,8 @@ __device__ __forceinline__ void strip_sweep_h16(const FillArgs& A, int s, int la
     C.hm_r = rr % KR;  // packed row hm_r % h, high half iff hm_r >= h
     C.hm_t = n - 1 + 2 * C.hm_lane + (C.hm_r >= H ? 1 : 0);
   }
-  if (s > 0) st.chunk_nxt = chunk_verify<true>(C, 0, chunk_issue<true>(C, 0));
+  const bool has_top = C.bnd_in != nullptr;
+  if (has_top) st.chunk_nxt = chunk_verify<true>(C, 0, chunk_issue<true>(C, 0));
   const int ngrp = (n + 63 + 7) / 8;  // last lane's high half reaches column n at t = n + 62
   const int rmask = A.reb_groups - 1;  // power of two
 #pragma unroll 1
@@ -259,7 +264,7 @@ __device__ __forceinline__ void strip_sweep_h16(const FillArgs& A, int s, int la
     }
 #endif
     st.chunk_cur = st.chunk_nxt;
-    const bool more = s > 0 && t0 + 8 < n;
+    const bool more = has_top && t0 + 8 < n;
     unsigned long long raw = 0;
     if (more) raw = chunk_issue<true>(C, t0 + 8);
     const bool masked = t0 < 64 || t0 + 7 >= n - 1;
