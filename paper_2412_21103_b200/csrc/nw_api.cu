@@ -870,6 +870,15 @@ nw_status pair_entry(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b,
   // unchanged (C2: 1.88 vs 1.59 ms for the int32 fill, not the default)
   if (want_dirs && d16_ok(c, sc) && (kr == 4 || kr == 8) && c->opt[NW_OPT_PAIR_FORM] == 2)
     h16_reb = h16_rebase_groups(c, sc, kr);
+  // tall direction fills (8+ rows per lane) with long rows take it by default: at 8 rows per
+  // lane the four packed registers amortise the per-step overhead (~20% faster steps) but
+  // the lane skew doubles, so the rows must be long against the strips' start lag:
+  // n >= 128 x strips (checkpointed refills, 1M columns: 501 -> 411 ms; 100k x 3k: slower)
+  if (want_dirs && d16_ok(c, sc) && kr >= 8 && c->opt[NW_OPT_PAIR_FORM] == 0 &&
+      !c->opt[NW_OPT_ROWS_PER_LANE] && n >= 128 * ((m + 255) / 256)) {
+    const int rb = h16_rebase_groups(c, sc, 8);
+    if (rb > 0) { h16_reb = rb; kr = 8; }
+  }
   st = grow(c, c->d_codes, c->codes_cap, (size_t)(la + lb));
   if (st) return st;
   // two ring slots (+ a sink slot for the NW_OPT_TEST_WITHHOLD hook)
@@ -2761,7 +2770,8 @@ nw_status linear_core(nw_ctx* c, const uint8_t* a, long long m, const uint8_t* b
     // tall refills of DNA-size pairs: the packed H' direction fill (§3.16) at 8 rows per
     // lane, its flags in the int32 layout (NW_OPT_PAIR_FORM = 1: the int32 fill)
     int rf_reb = 0;
-    if (ck_d16 && kr >= 8 && c->opt[NW_OPT_PAIR_FORM] != 1 && !c->opt[NW_OPT_LINEAR_INT32]) {
+    if (ck_d16 && kr >= 8 && c->opt[NW_OPT_PAIR_FORM] != 1 && !c->opt[NW_OPT_LINEAR_INT32] &&
+        col >= 128 * ((mm + 255) / 256)) {
       rf_reb = h16_rebase_groups(c, sc, 8);
       if (rf_reb > 0) kr = 8;
     }
