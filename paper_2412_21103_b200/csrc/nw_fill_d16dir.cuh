@@ -35,7 +35,11 @@ struct D16DirState {
   int usum;
 };
 
-template <int KR, bool PROFREG, int PI, bool MASKED>
+// MASKED groups hold the cell column n (the score's sum of U) or columns outside [1, n];
+// HEAD groups (t0 < 64) hold halves left of column 1: their s' is forced to 0 (selector
+// override / zero profile words), which keeps U = V = Z = 0 there with no mask (the
+// other inputs are 0 by induction).
+template <int KR, bool PROFREG, int PI, bool MASKED, bool HEAD = MASKED>
 __device__ __forceinline__ void d16dir_group(D16DirState<KR>& st, const FillArgs& A, int lane,
                                              int t0, const int* bnd_in, int* bnd_out,
                                              uint32_t* dir_base, const int8_t* sprof,
@@ -68,12 +72,18 @@ __device__ __forceinline__ void d16dir_group(D16DirState<KR>& st, const FillArgs
       }
       st.bc_prev = bT;
     }
+    if (HEAD) {  // halves left of column 1: s' = 0 (low half iff jT < 1, high half iff jT < 2)
+      if (PROFREG) {
+        if (jT < 2) sel = (jT < 1) ? 0xcc88u : ((sel & 0xffu) | 0xcc00u);
+      } else {
+        if (jT < 1) lo8 = make_uint2(0, 0);
+        if (jT < 2) hi8 = make_uint2(0, 0);
+      }
+    }
     const int recv = __shfl_up_sync(FULL, (int)st.vlast, 1);
     const int bval = __shfl_sync(FULL, chunk, (t & 31));
     const uint32_t upsrc = (lane == 0) ? ((uint32_t)bval << 16) : (uint32_t)recv;
     uint32_t vup = prmt2(upsrc, st.vlast, 0x5432u);
-    uint32_t mask = 0xffffffffu;
-    if (MASKED) mask = (jT >= 1 ? 0x0000ffffu : 0u) | (jT >= 2 ? 0xffff0000u : 0u);
 #pragma unroll
     for (int k = 0; k < H; ++k) {
       uint32_t sp;
@@ -97,13 +107,13 @@ __device__ __forceinline__ void d16dir_group(D16DirState<KR>& st, const FillArgs
       // the word restarting every 8-step group
       const uint32_t m = __vminu2(qY, 0x00010001u) * 2u + __vminu2(qX, 0x00010001u);
       st.acc[k] = (q == 0 ? 0u : st.acc[k] * 4u) + m;
-      if (MASKED) un &= mask;  // U(i, 0) = 0 until each half reaches column 1
       st.Up[k] = un;
       vup = vn;
     }
     st.vlast = vup;
     const int jB = jT - 1;
-    if (lane == 31 && (!MASKED || (jB >= 1 && jB <= n))) bnd_out[(t0 - 62) + q] = (int)(vup >> 16);
+    // (past column n the row has >= 64 entries of slack: only the head needs the check)
+    if (lane == 31 && (!HEAD || (jB >= 1 && jB <= n))) bnd_out[(t0 - 62) + q] = (int)(vup >> 16);
     if (MASKED) {
       if (jT == n) {
 #pragma unroll
@@ -177,8 +187,8 @@ __device__ __forceinline__ void strip_sweep_d16dir(const FillArgs& A, int s, int
       const int jj = t0 + 1 + lane;
       chunk = (s > 0 && jj <= n) ? bnd_in[jj] : 0;
     }
-    const bool masked = t0 < 64 || t0 + 7 >= n - 1;
-    if (masked)
+    const bool masked = t0 < 64 || t0 + 7 >= n - 1;  // (one masked variant: a third, tail-only
+    if (masked)                                       //  one cost more in code size than it saved)
       d16dir_group<KR, PROFREG, PI, true>(st, A, lane, t0, bnd_in, bnd_out, dir_base, sprof,
                                           rows_lo, rows_hi, chunk);
     else
