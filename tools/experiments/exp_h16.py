@@ -1,5 +1,5 @@
 """C5 (1M x 1M score-only): fill-kernel time of the packed H' sweep with a moving base
-(nw_fill_h16.cuh) at several rows per lane / rebase periods, against the difference
+(nw_fill_h16.cuh) at several rows per lane / rebase periods (EXP_FORMS: pair_form values), against the difference
 form (pair_form 1). Scores must equal the committed oracle digest.
 usage: python tools/experiments/exp_h16.py KR,KR,... REB,REB,... [out.json]"""
 import json, os, sys
@@ -33,7 +33,7 @@ def run(name):
 
 ctx.set_option("pair_form", 1)
 run("d16_default")
-for form in os.environ.get("EXP_FORMS", "2,3").split(","):
+for form in os.environ.get("EXP_FORMS", "0").split(","):
     ctx.set_option("pair_form", int(form))
     for kr in sys.argv[1].split(","):
         for reb in sys.argv[2].split(","):
