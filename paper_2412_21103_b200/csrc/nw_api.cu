@@ -319,8 +319,13 @@ int tb_lstep(const nw_ctx* c) {
   while ((2LL << l) <= k) ++l;
   return l;
 }
-int tb_band(const nw_ctx* c) {
-  const long long k = c->opt[NW_OPT_TB_BAND] >= 32 ? std::min(c->opt[NW_OPT_TB_BAND], 4096LL) : 256;
+// Default: 256 samples (C2, profiles/r01_exp_tbband.json); 32 when a row has at most 512
+// samples (n <= ~2k columns): the wide band's warps mostly stage and walk for nothing
+// (C1: 93 -> 72 us of traceback, tools/experiments/exp_c1tb.py).
+int tb_band(const nw_ctx* c, long long n, int lstep) {
+  const long long nq = (n >> lstep) + 1;
+  const long long dflt = nq <= 512 ? 32 : 256;
+  const long long k = c->opt[NW_OPT_TB_BAND] >= 32 ? std::min(c->opt[NW_OPT_TB_BAND], 4096LL) : dflt;
   return (int)((k + 31) / 32 * 32);
 }
 
@@ -796,7 +801,7 @@ nw_status new_tb(nw_ctx* c, long long m, long long n, const nw_scoring* sc, int 
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t b_dirs = al((size_t)S * tb->wpl * kr * 32 * sizeof(uint16_t));
   tb->lstep = tb_lstep(c);
-  tb->nb = tb_band(c);
+  tb->nb = tb_band(c, n, tb->lstep);
   const size_t b_spec = al((size_t)S * tb->nb * sizeof(int));
   const size_t b_cs = al((size_t)S * sizeof(int)), b_len = b_cs;
   const size_t b_seg = al((size_t)S * tb->segstride);
