@@ -336,10 +336,13 @@ enum {
                                  the median sequence length: 1 from 1,024, else 16 or 8) */
   NW_OPT_BATCH_BND_GLOBAL = 22, /* 1: the packed H' batch sweep keeps its boundary rows in global
                                   scratch instead of shared memory */
-  NW_OPT_PAIR_FORM = 23,       /* tall score-only pairs (and the column-block pipeline): 0 = packed
-                                  H' with a moving base (nw_fill_h16, default), 1 = packed
-                                  difference form (nw_fill_d16); 2 = as 0, and direction fills of
-                                  DNA-size pairs in the packed H' form too (default: int32) */
+  NW_OPT_PAIR_FORM = 23,       /* DNA-size alphabets with s - 2g >= 0. 0 (default): tall score-only
+                                  pairs, the column-block pipeline and the checkpoint pass of
+                                  nw_align_pair_linear in packed H' with a moving base (nw_fill_h16),
+                                  direction fills at 8+ rows per lane with long rows (n >= 128 x
+                                  strips, e.g. the checkpointed refills) in its direction form;
+                                  1 = the packed difference form / int32 fills throughout;
+                                  2 = as 0, plus every direction fill at 4 or 8 rows per lane */
   NW_OPT_H16_REBASE = 24,      /* packed H' pair sweep: rebase period in 8-step groups (power of two,
                                   0: the largest <= 64 the value range allows); test hook */
   NW_OPT_H16_KR = 25,          /* rows per lane of the packed H' pair sweep (even, 12..32; 0: rule) */
