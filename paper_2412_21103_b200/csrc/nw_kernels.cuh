@@ -560,8 +560,11 @@ __device__ __forceinline__ void task_pair(const BatchArgs& B, long long task, in
 template <int KR16, bool COHERENT>
 __device__ __forceinline__ void walk_lanes(const BatchArgs& B, long long task, bool act, int lane);
 
+// The mixed-height H' sweep (PACKED 4: three sweeps, 124 registers unbounded) is held to 96
+// registers (5 CTAs per SM instead of 4, no spills): C3 298 -> 291 ms (6 CTAs: 80 registers
+// with spills, 338 ms)
 template <int KR, bool DIRS, bool PROFREG, int PI, int PACKED = 0, int KR16 = 16>
-__global__ void __launch_bounds__(128) k_batch(BatchArgs B) {
+__global__ void __launch_bounds__(128, (PACKED == 4 ? 5 : 1)) k_batch(BatchArgs B) {
   constexpr int R = 32 * KR;
   extern __shared__ __align__(16) int8_t smem[];
   const int lane = threadIdx.x & 31;
