@@ -2065,7 +2065,7 @@ nw_status batch_core(nw_ctx* c, const uint8_t* d_codes_raw_or_codes, bool alread
   const size_t smem = smem_prof + (bnd_smem ? smem_bnd : 0);
   // 6 x 4 warps per SM (24 warps, 72 registers each): C4 2.11 -> 2.26 TCUPS, C3 6.73 -> 6.84
   // over 4 per SM; 8 no better (tools/exp_ctas.sh, profiles/r01_exp_ctas.txt)
-  int ctas_per_sm = 6;
+  int ctas_per_sm = 6;  // (8 measured equal on C3 and C4 in round 2)
   // no more warps than pairs: the int32 traceback path sizes its per-warp direction
   // scratch (~maxlen^2/4 bytes) per launched warp
   const long long nwarps = std::min<long long>((long long)c->sm_count * ctas_per_sm * warps_per_cta,
